@@ -1,0 +1,181 @@
+/*
+ * lamina_b200 — C ABI of the B200-native layout-copy / bit-pack / instrumentation /
+ * n-body hot path of the LLAMA-paper reference library `lamina`
+ * (/root/reference/proj, arXiv 2302.08251).
+ *
+ * Drop-in boundary: every entry point replaces one reference interface on the hot
+ * path (file:line relative to /root/reference/proj).  Plain pointers and sizes only;
+ * no torch or C++ types cross this line.  All device work is stream-ordered on the
+ * cudaStream_t passed as `void* stream` (NULL = legacy default stream).
+ *
+ * Errors: every int-returning call returns LAM_OK (0) or one of the LAM_E* codes,
+ * which map 1:1 onto the exception types the reference throws
+ * (include/lamina_b200.hpp rethrows them):
+ *   LAM_EINVAL    std::invalid_argument  ("incompatible views", "type mismatch",
+ *                 "blob count mismatch", "blob size mismatch", "unknown layout", ...)
+ *   LAM_ERANGE    std::out_of_range      ("index out of range")
+ *   LAM_EOVERFLOW std::overflow_error    ("index type overflow")
+ *   LAM_ELOGIC    std::logic_error       ("computed leaf has no physical offset")
+ *   LAM_ERUNTIME  std::runtime_error
+ *   LAM_ECUDA     CUDA runtime failure (no reference counterpart)
+ * lam_last_error() returns the thread-local message of the last failing call.
+ */
+#ifndef LAMINA_B200_H
+#define LAMINA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAM_OK 0
+#define LAM_EINVAL 1
+#define LAM_ERANGE 2
+#define LAM_EOVERFLOW 3
+#define LAM_ELOGIC 4
+#define LAM_ERUNTIME 5
+#define LAM_ECUDA 6
+
+/* Scalar kinds, same numbering as lamina::Scalar (core/include/lamina/scalar.hpp:16-29). */
+#define LAM_I8 0
+#define LAM_I16 1
+#define LAM_I32 2
+#define LAM_I64 3
+#define LAM_U8 4
+#define LAM_U16 5
+#define LAM_U32 6
+#define LAM_U64 7
+#define LAM_F32 8
+#define LAM_F64 9
+#define LAM_BOOL 10
+
+/* Instrumentation wrappers (lamina::FieldAccessCount / lamina::Heatmap,
+ * core/include/lamina/instrument.hpp:27-127).  Heatmap is outermost when both. */
+#define LAM_WRAP_FIELD_ACCESS_COUNT 1
+#define LAM_WRAP_HEATMAP 2
+
+/* n-body arithmetic modes (tools/nbody/kernel.hpp:15-41). */
+#define LAM_NBODY_EXACT 0 /* IEEE add/mul/sqrt/div in the reference's order: bit-identical */
+#define LAM_NBODY_FAST 1  /* FMA + rsqrt, j-tile reassociation: within stated tolerance */
+
+typedef struct lam_layout lam_layout; /* lowered mapping (schema + extents + layout) */
+typedef struct lam_view lam_view;     /* device blobs bound to a layout (+ device counters) */
+
+/* ---- errors --------------------------------------------------------------------- */
+const char* lam_last_error(void);
+const char* lam_version(void);
+
+/* ---- layouts ------------------------------------------------------------------------
+ * Replaces lamina::parseLayout(text, schema, extents)  (core/include/lamina/layout_spec.hpp:19,
+ * core/src/layout_spec.cpp:164-167) together with RecordSchema::parse (core/src/record.cpp:480)
+ * and ArrayExtents::parse (core/src/extents.cpp:135).  `layout` is the reference grammar
+ * (aos-packed, aos-aligned, soa-sb, soa-mb, aosoa:L, one, null, split:..., bitpack-int:b,
+ * bitpack-float:E,M, changetype:..., bytesplit:...) and additionally accepts the names the
+ * reference prints for its wrappers, "field-access-count(<inner>)" and "heatmap:<g>(<inner>)",
+ * so Mapping::name() of any reference mapping round-trips. `wrap`/`granularity` add the
+ * wrappers programmatically (FieldAccessCount(inner) / Heatmap(inner, g)). */
+int lam_layout_create(const char* schema, const char* extents, const uint64_t* dyn_values, size_t n_dyn,
+                      const char* layout, int wrap, uint64_t granularity, lam_layout** out);
+void lam_layout_destroy(lam_layout* layout);
+/* Mapping::name() (core/include/lamina/mapping.hpp:72); returns the length, copies up to cap-1. */
+size_t lam_layout_name(const lam_layout* layout, char* buf, size_t cap);
+/* RecordSchema::toString (core/src/record.cpp:472) / ArrayExtents::toString (core/src/extents.cpp:118). */
+size_t lam_layout_schema(const lam_layout* layout, char* buf, size_t cap);
+size_t lam_layout_extents(const lam_layout* layout, char* buf, size_t cap);
+/* Mapping::blobCount/blobSize (mapping.hpp:74-75). */
+size_t lam_layout_blob_count(const lam_layout* layout);
+uint64_t lam_layout_blob_size(const lam_layout* layout, size_t nr);
+uint64_t lam_layout_element_count(const lam_layout* layout);
+size_t lam_layout_leaf_count(const lam_layout* layout);
+/* Leaf table entry (RecordSchema::leaf, record.hpp:173): scalar kind, size, packed offset. */
+int lam_layout_leaf(const lam_layout* layout, size_t flat_leaf, int* kind, size_t* size, size_t* offset_packed);
+size_t lam_layout_leaf_path(const lam_layout* layout, size_t flat_leaf, char* buf, size_t cap);
+/* Mapping::isComputed / isFullyPhysical / hasMutableState (mapping.hpp:86-105). */
+int lam_layout_is_computed(const lam_layout* layout, size_t flat_leaf);
+int lam_layout_is_fully_physical(const lam_layout* layout);
+int lam_layout_has_mutable_state(const lam_layout* layout);
+/* Mapping::physicalOffset (mapping.hpp:109); LAM_ELOGIC for computed leaves. */
+int lam_layout_physical_offset(const lam_layout* layout, uint64_t linear, size_t flat_leaf, size_t* nr,
+                               uint64_t* offset);
+/* Heatmap::blockCount summed over blobs (instrument.hpp:107); 0 when not wrapped. */
+uint64_t lam_layout_heatmap_blocks(const lam_layout* layout, size_t nr);
+/* Element alignment unit for sharding/chunking: every multiple of it starts every blob
+ * stream on a 16-byte boundary (AoSoA lanes, bit-stream words). */
+uint64_t lam_layout_shard_unit(const lam_layout* layout);
+
+/* ---- device views ---------------------------------------------------------------------
+ * Replaces lamina::View(MappingPtr) (core/src/view.cpp:97-103): allocates blobCount()
+ * device blobs of exactly blobSize(nr) bytes, zero-filled (parity with Blob,
+ * core/include/lamina/blob.hpp:22-29).  Counters (FieldAccessCount / Heatmap) live in
+ * device memory and start at zero. */
+int lam_view_alloc(const lam_layout* layout, int device, void* stream, lam_view** out);
+/* Replaces lamina::View(MappingPtr, std::vector<Blob>) (core/src/view.cpp:105-118): adopts
+ * caller-owned device blobs (not freed by lam_view_free).  `blob_bytes` (optional) is
+ * checked like the reference ("blob count mismatch" / "blob size mismatch").  Blob
+ * pointers must be 16-byte aligned. */
+int lam_view_wrap(const lam_layout* layout, int device, void* const* device_blobs, const uint64_t* blob_bytes,
+                  size_t n_blobs, lam_view** out);
+void lam_view_free(lam_view* view);
+const lam_layout* lam_view_layout(const lam_view* view);
+void* lam_view_blob(const lam_view* view, size_t nr);
+/* Stream-ordered host<->device blob transfer (pinned host memory makes them async). */
+int lam_view_upload(lam_view* view, size_t nr, const void* host, void* stream);
+int lam_view_download(const lam_view* view, size_t nr, void* host, void* stream);
+
+/* ---- the hot path: layout-aware copy ---------------------------------------------------
+ * Replaces lamina::copyView(const View& src, View& dst)  (core/include/lamina/view.hpp:285,
+ * core/src/view.cpp:168-189).  Same contract: schema and extents must be equal
+ * ("incompatible views"); equal fully-physical, uninstrumented layouts copy blob-wise
+ * (view.cpp:175-181); everything else copies fieldwise with dst's projection applied
+ * (truncation, type change, byte split, bit packing, counting).  Bit-exact to the
+ * reference, including bytes it never writes (padding, AoSoA tail lanes, bit-stream tail). */
+int lam_copy(const lam_view* src, lam_view* dst, void* stream);
+/* Same, over the element range [begin, end) only (both multiples of lam_layout_shard_unit
+ * of src and dst, or end == element count): the per-shard call of a multi-GPU copy. */
+int lam_copy_range(const lam_view* src, lam_view* dst, uint64_t begin, uint64_t end, void* stream);
+/* copyView over HOST views: host blobs in, host blobs out (dst blobs are in/out so that
+ * bytes the copy never writes keep their values).  Streams chunks through the GPU with
+ * overlapped H2D / kernel / D2H.  Synchronous.  Host memory should be pinned. */
+int lam_copy_host(const lam_layout* src_layout, const void* const* src_host_blobs, const lam_layout* dst_layout,
+                  void* const* dst_host_blobs, int device, uint64_t* src_counters, uint64_t* dst_counters);
+
+/* ---- instrumentation ---------------------------------------------------------------------
+ * FieldAccessCount::counters()/reset() (instrument.hpp:56-58): reads[leaves], writes[leaves]. */
+int lam_counters_read(const lam_view* view, uint64_t* reads, uint64_t* writes);
+int lam_counters_reset(lam_view* view, void* stream);
+/* Heatmap::blockCounter over blob nr (instrument.hpp:112): out[blocks(nr)]. */
+int lam_heatmap_read(const lam_view* view, size_t nr, uint64_t* out);
+
+/* ---- scalar access (host-side convenience; generic funnel View::read/write, view.cpp:120-128)
+ * Values are storage bits of the leaf's logical type (ScalarValue::storageBits, scalar.hpp:231).
+ * Runs one tiny device launch per call batch: n (linear, leaf) pairs. */
+int lam_view_read_values(const lam_view* view, const uint64_t* linear, const uint32_t* leaf, uint64_t* bits_out,
+                         size_t n, void* stream);
+int lam_view_write_values(lam_view* view, const uint64_t* linear, const uint32_t* leaf, const uint64_t* bits,
+                          size_t n, void* stream);
+
+/* ---- n-body (tools/nbody) ------------------------------------------------------------------
+ * The paper's all-pairs benchmark over any mapping of
+ * Record{Pos:{x,y,z},Vel:{x,y,z},Mass} (f32 or f64 leaves).
+ * lam_nbody_init   = drawInitValues(seed) + initView  (tools/nbody/runner.cpp:30-58)
+ * lam_nbody_update = updateStep   (tools/nbody/steps.hpp:13-42, kernel.hpp:15-41); updates
+ *                    Vel of elements [i_begin, i_end) against ALL j in index order.
+ * lam_nbody_move   = moveStep     (tools/nbody/steps.hpp:97-118) over [i_begin, i_end).
+ * lam_nbody_checksum = checksumView (runner.cpp:62-72): Σ pos in double, index order. */
+int lam_nbody_init(lam_view* view, uint64_t seed, void* stream);
+int lam_nbody_update(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
+int lam_nbody_move(lam_view* view, uint64_t i_begin, uint64_t i_end, void* stream);
+int lam_nbody_checksum(const lam_view* view, double* out);
+
+/* ---- misc ------------------------------------------------------------------------------- */
+/* Number of kernels this library launched on the calling process (all devices). */
+uint64_t lam_launch_count(void);
+int lam_device_sync(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAMINA_B200_H */

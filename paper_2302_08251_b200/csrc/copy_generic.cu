@@ -1,0 +1,217 @@
+// Generic fieldwise copy: the reference hot loop
+//     for i in [0,N) for f in [0,leaves): dst.write(i, f, src.read(i, f))   (view.cpp:184-188)
+// with one thread per element i and the mapping trees resolved by the device plan
+// interpreter (device_common.cuh).  Handles every mapping composition the layout grammar
+// can express (Split, One, Null, nested ChangeType/Bytesplit, bit packing, instrumentation);
+// the specialised tile engine (copy_tile.cu) takes the common shapes.  Bit-stream
+// writes use word atomics, so neighbouring fields never race (bitpack.hpp:16-17).
+#include "device_common.cuh"
+#include "launch.h"
+
+#include <atomic>
+
+namespace lamk
+{
+    static std::atomic<uint64_t> g_launches{0};
+    void count_launch(uint64_t n)
+    {
+        g_launches.fetch_add(n, std::memory_order_relaxed);
+    }
+    uint64_t launch_count()
+    {
+        return g_launches.load(std::memory_order_relaxed);
+    }
+
+    int sm_count(int device)
+    {
+        static int cache[64] = {0};
+        if(device < 0 || device >= 64)
+            return 148;
+        if(cache[device] == 0)
+        {
+            int v = 0;
+            if(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+                v = 148;
+            cache[device] = v;
+        }
+        return cache[device];
+    }
+
+    // FieldAccessCount: warp-aggregated per-field shared counters, one global atomic per
+    // CTA per field (instrument.cpp:57-72 counts one relaxed increment per access)
+    template<typename Idx>
+    __global__ void __launch_bounds__(256) k_generic_copy(const lamp_view* __restrict__ S, const lamp_view* __restrict__ D,
+                                                           uint64_t begin, uint64_t end, uint32_t nleaves, int facS, int facD)
+    {
+        extern __shared__ unsigned long long s_cnt[]; // [nleaves] reads, [nleaves] writes
+        const lamd::ViewCtx sv = lamd::make_ctx(S);
+        const lamd::ViewCtx dv = lamd::make_ctx(D);
+        const uint16_t* sroots = S->roots;
+        const uint16_t* droots = D->roots;
+        if(facS | facD)
+        {
+            for(uint32_t k = threadIdx.x; k < 2 * nleaves; k += blockDim.x)
+                s_cnt[k] = 0;
+            __syncthreads();
+        }
+        const Idx stride = static_cast<Idx>(gridDim.x) * blockDim.x;
+        const Idx n = static_cast<Idx>(end - begin);
+        uint32_t mine = 0;
+        for(Idx k = static_cast<Idx>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride)
+        {
+            const uint64_t i = begin + k;
+            for(uint32_t f = 0; f < nleaves; ++f)
+            {
+                const uint64_t v = lamd::read_node<LAMP_MAX_DEPTH>(sv, sroots[f], i);
+                lamd::write_node<LAMP_MAX_DEPTH>(dv, droots[f], i, v);
+            }
+            ++mine;
+        }
+        if(facS | facD)
+        {
+            const uint32_t warpTotal = __reduce_add_sync(0xFFFFFFFFu, mine);
+            if((threadIdx.x & 31) == 0 && warpTotal)
+                for(uint32_t f = 0; f < nleaves; ++f)
+                {
+                    if(facS)
+                        atomicAdd(&s_cnt[f], static_cast<unsigned long long>(warpTotal));
+                    if(facD)
+                        atomicAdd(&s_cnt[nleaves + f], static_cast<unsigned long long>(warpTotal));
+                }
+            __syncthreads();
+            for(uint32_t f = threadIdx.x; f < nleaves; f += blockDim.x)
+            {
+                if(facS && s_cnt[f])
+                    atomicAdd(&S->fac_counters[f], s_cnt[f]); // src reads
+                if(facD && s_cnt[nleaves + f])
+                    atomicAdd(&D->fac_counters[nleaves + f], s_cnt[nleaves + f]); // dst writes
+            }
+        }
+    }
+
+    cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,
+                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s)
+    {
+        if(end <= begin || nleaves == 0)
+            return cudaSuccess;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t n = end - begin;
+        const uint64_t want = (n + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 8;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        const size_t smem = (facSrc || facDst) ? 2 * nleaves * sizeof(unsigned long long) : 0;
+        if(end <= 0x7FFFFFFFull)
+            k_generic_copy<uint32_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst);
+        else
+            k_generic_copy<uint64_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst);
+        count_launch();
+        return cudaGetLastError();
+    }
+
+    // ---- blob copy: vectorised 16-byte path when both sides are aligned ----------------
+    __global__ void __launch_bounds__(512) k_blob_copy16(uint4* __restrict__ d, const uint4* __restrict__ s, uint64_t n16)
+    {
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        for(; i + 3 * stride < n16; i += 4 * stride)
+        {
+            const uint4 a = __ldcs(s + i), b = __ldcs(s + i + stride), c = __ldcs(s + i + 2 * stride),
+                        e = __ldcs(s + i + 3 * stride);
+            __stcs(d + i, a);
+            __stcs(d + i + stride, b);
+            __stcs(d + i + 2 * stride, c);
+            __stcs(d + i + 3 * stride, e);
+        }
+        for(; i < n16; i += stride)
+            __stcs(d + i, __ldcs(s + i));
+    }
+
+    __global__ void k_blob_copy1(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, uint64_t n)
+    {
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        for(uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+            d[i] = s[i];
+    }
+
+    cudaError_t blob_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s)
+    {
+        if(bytes == 0)
+            return cudaSuccess;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const unsigned sms = static_cast<unsigned>(sm_count(dev));
+        const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+        uint64_t head = 0;
+        if(aligned)
+        {
+            const uint64_t n16 = bytes / 16;
+            if(n16)
+            {
+                const uint64_t want = (n16 + 511) / 512;
+                const unsigned grid = static_cast<unsigned>(want < sms * 4ull ? want : sms * 4ull);
+                k_blob_copy16<<<grid, 512, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+                count_launch();
+            }
+            head = n16 * 16;
+        }
+        if(head < bytes)
+        {
+            const uint64_t rest = bytes - head;
+            const uint64_t want = (rest + 255) / 256;
+            const unsigned grid = static_cast<unsigned>(want < sms * 8ull ? want : sms * 8ull);
+            k_blob_copy1<<<grid, 256, 0, s>>>(static_cast<uint8_t*>(dst) + head, static_cast<const uint8_t*>(src) + head,
+                                              rest);
+            count_launch();
+        }
+        return cudaGetLastError();
+    }
+
+    // ---- funnel access by (linear, leaf) pairs (View::read / View::write) ------------------
+    __global__ void k_read_values(const lamp_view* __restrict__ V, const uint64_t* __restrict__ lin,
+                                  const uint32_t* __restrict__ leaf, uint64_t* __restrict__ out, size_t n)
+    {
+        const lamd::ViewCtx c = lamd::make_ctx(V);
+        for(size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+            k += static_cast<size_t>(gridDim.x) * blockDim.x)
+            out[k] = lamd::read_node<LAMP_MAX_DEPTH>(c, V->roots[leaf[k]], lin[k]);
+    }
+
+    __global__ void k_write_values(const lamp_view* __restrict__ V, const uint64_t* __restrict__ lin,
+                                   const uint32_t* __restrict__ leaf, const uint64_t* __restrict__ in, size_t n)
+    {
+        const lamd::ViewCtx c = lamd::make_ctx(V);
+        for(size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+            k += static_cast<size_t>(gridDim.x) * blockDim.x)
+        {
+            const uint32_t r = V->roots[leaf[k]];
+            uint64_t bits = in[k];
+            const int t = V->nodes[r].type;
+            // ScalarValue::fromStorageBits canonicalisation of the incoming value (scalar.hpp:251-271)
+            bits = t == lamd::BOOL ? uint64_t((bits & 0xFF) != 0) : (bits & lamd::low_mask(8 * lamd::scalar_size(t)));
+            lamd::write_node<LAMP_MAX_DEPTH>(c, r, lin[k], bits);
+        }
+    }
+
+    cudaError_t read_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, uint64_t* out, size_t n,
+                            cudaStream_t s)
+    {
+        if(n == 0)
+            return cudaSuccess;
+        const unsigned grid = static_cast<unsigned>(n / 256 + 1 < 4096 ? n / 256 + 1 : 4096);
+        k_read_values<<<grid, 256, 0, s>>>(v, lin, leaf, out, n);
+        count_launch();
+        return cudaGetLastError();
+    }
+
+    cudaError_t write_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, const uint64_t* in,
+                             size_t n, cudaStream_t s)
+    {
+        if(n == 0)
+            return cudaSuccess;
+        const unsigned grid = static_cast<unsigned>(n / 256 + 1 < 4096 ? n / 256 + 1 : 4096);
+        k_write_values<<<grid, 256, 0, s>>>(v, lin, leaf, in, n);
+        count_launch();
+        return cudaGetLastError();
+    }
+} // namespace lamk

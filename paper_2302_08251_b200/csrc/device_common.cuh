@@ -1,0 +1,449 @@
+// Device-side value semantics of the reference, restated for sm_100a:
+//   * values travel as the storage bits of their scalar kind, zero-extended to 64 bits
+//     (ScalarValue::storageBits, scalar.hpp:231-246);
+//   * type conversion = ScalarValue::convertTo (scalar.hpp:295-306) with x86 SSE NaN rules
+//     (cvtsd2ss / cvtss2sd keep sign and top payload bits and set the quiet bit) — the
+//     reference is compiled for x86-64 without -march, so those are its semantics;
+//   * minifloat codec = floatEncode / floatDecode (bitpack.cpp:96-188), integer-exact;
+//   * bit streams = LSB-first little-endian u32 words (bitpack.cpp:11-47).
+// All arithmetic is integer or correctly-rounded IEEE (no fast-math, no FTZ).
+#pragma once
+
+#include "lam_plan.h"
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define LAM_DEV __device__ __forceinline__
+
+namespace lamd
+{
+    enum : int
+    {
+        I8 = 0,
+        I16,
+        I32,
+        I64,
+        U8,
+        U16,
+        U32,
+        U64,
+        F32,
+        F64,
+        BOOL
+    };
+
+    LAM_DEV uint32_t scalar_size(int t)
+    {
+        // i8 i16 i32 i64 u8 u16 u32 u64 f32 f64 bool
+        return (0x18484218421ull >> (4 * t)) & 0xF;
+    }
+    LAM_DEV bool is_signed(int t)
+    {
+        return t <= I64;
+    }
+    LAM_DEV uint64_t low_mask(uint32_t bits)
+    {
+        return bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+    }
+
+    // ---- conversions (ScalarValue::convertTo) -----------------------------------------
+    LAM_DEV uint64_t f32_to_f64_bits(uint32_t b)
+    {
+        if((b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu) != 0u)
+            return (uint64_t(b >> 31) << 63) | 0x7FF8000000000000ull | (uint64_t(b & 0x007FFFFFu) << 29);
+        return static_cast<uint64_t>(__double_as_longlong(static_cast<double>(__uint_as_float(b))));
+    }
+    LAM_DEV uint32_t f64_to_f32_bits(uint64_t b)
+    {
+        if((b & 0x7FF0000000000000ull) == 0x7FF0000000000000ull && (b & 0x000FFFFFFFFFFFFFull) != 0ull)
+            return (uint32_t(b >> 63) << 31) | 0x7FC00000u | uint32_t((b >> 29) & 0x003FFFFFu);
+        return __float_as_uint(__double2float_rn(__longlong_as_double(static_cast<long long>(b))));
+    }
+
+    LAM_DEV uint64_t convert_value(uint64_t v, int from, int to)
+    {
+        if(from == to)
+            return v;
+        if(from == F32 && to == F64)
+            return f32_to_f64_bits(static_cast<uint32_t>(v));
+        if(from == F64 && to == F32)
+            return f64_to_f32_bits(v);
+        const uint32_t fw = 8 * scalar_size(from);
+        const uint32_t tw = 8 * scalar_size(to);
+        if(is_signed(from) && fw < 64)
+        {
+            // sign-extend from the source width, keep the low bits of the target width
+            const uint64_t s = 1ull << (fw - 1);
+            v = ((v & low_mask(fw)) ^ s) - s;
+        }
+        return v & low_mask(tw);
+    }
+
+    // ---- minifloat codec (bitpack.cpp:51-188) ------------------------------------------
+    LAM_DEV uint64_t rne_shift(uint64_t x, int s)
+    {
+        if(s <= 0)
+            return x << static_cast<unsigned>(-s);
+        if(s >= 64)
+            return 0;
+        const uint64_t q = x >> s;
+        const uint64_t rem = x & low_mask(static_cast<uint32_t>(s));
+        const uint64_t half = 1ull << (s - 1);
+        return (rem > half || (rem == half && (q & 1ull))) ? q + 1 : q;
+    }
+
+    // floatEncode(value, E, M) on the double's bit pattern
+    __device__ __noinline__ uint64_t float_encode(uint64_t bits64, uint32_t E, uint32_t M)
+    {
+        const uint64_t signBit = (bits64 >> 63) << (E + M);
+        const uint64_t expMask = low_mask(E);
+        const uint64_t inf = signBit | (expMask << M);
+        const uint32_t rawExp = static_cast<uint32_t>((bits64 >> 52) & 0x7FF);
+        uint64_t frac = bits64 & low_mask(52);
+        if(rawExp == 0x7FF)
+        {
+            if(frac == 0 || M == 0)
+                return inf;
+            return inf | (1ull << (M - 1));
+        }
+        if(rawExp == 0 && frac == 0)
+            return signBit;
+        int64_t e2;
+        if(rawExp == 0)
+        {
+            const int shift = 52 - (63 - __clzll(static_cast<long long>(frac)));
+            frac <<= shift;
+            e2 = 1 - 1023 - 52 - shift;
+        }
+        else
+        {
+            frac |= 1ull << 52;
+            e2 = static_cast<int64_t>(rawExp) - 1023 - 52;
+        }
+        const int64_t bias = (int64_t(1) << (E - 1)) - 1;
+        int64_t biasedExp = e2 + 52 + bias;
+        const int64_t maxExpField = static_cast<int64_t>(expMask);
+        if(biasedExp >= 1)
+        {
+            uint64_t q = rne_shift(frac, 52 - static_cast<int>(M));
+            if((q >> (M + 1)) != 0)
+            {
+                q >>= 1;
+                ++biasedExp;
+            }
+            if(biasedExp >= maxExpField)
+                return inf;
+            return signBit | (static_cast<uint64_t>(biasedExp) << M) | (q - (1ull << M));
+        }
+        const int64_t shift = (1 - bias - static_cast<int64_t>(M)) - e2;
+        const uint64_t q = rne_shift(frac, shift > 64 ? 64 : static_cast<int>(shift));
+        if((q >> M) != 0)
+        {
+            if(1 >= maxExpField)
+                return inf;
+            return signBit | (1ull << M);
+        }
+        return signBit | q;
+    }
+
+    // floatDecode(pattern, E, M) -> double bit pattern
+    __device__ __noinline__ uint64_t float_decode(uint64_t p, uint32_t E, uint32_t M)
+    {
+        p &= low_mask(1 + E + M);
+        const uint64_t sign = (p >> (E + M)) & 1ull;
+        const uint64_t expField = (p >> M) & low_mask(E);
+        const uint64_t man = p & low_mask(M);
+        const int64_t bias = (int64_t(1) << (E - 1)) - 1;
+        auto clampExp = [](int64_t e) { return static_cast<int>(e < -5000 ? -5000 : (e > 5000 ? 5000 : e)); };
+        uint64_t mag;
+        if(expField == low_mask(E))
+            mag = man != 0 ? 0x7FF8000000000000ull : 0x7FF0000000000000ull;
+        else if(expField == 0)
+            mag = static_cast<uint64_t>(__double_as_longlong(
+                ldexp(__ull2double_rn(man), clampExp(1 - bias - static_cast<int64_t>(M)))));
+        else
+            mag = static_cast<uint64_t>(__double_as_longlong(ldexp(
+                __ull2double_rn((1ull << M) + man),
+                clampExp(static_cast<int64_t>(expField) - bias - static_cast<int64_t>(M)))));
+        return mag | (sign << 63);
+    }
+
+    // Fast f32 encoders, equal to floatEncode((double)f, E, M) on every f32 input
+    // (checked exhaustively against the reference on the GPU, tests/test_gpu_codec.py).
+    LAM_DEV uint32_t encode_e8m10_f32(uint32_t b)
+    {
+        const uint32_t s = (b >> 31) << 18;
+        const uint32_t a = b & 0x7FFFFFFFu;
+        if(a > 0x7F800000u)
+            return s | 0x3FE00u; // NaN: exp all ones | quiet bit
+        if(a == 0x7F800000u)
+            return s | 0x3FC00u;
+        // RNE of the low 13 mantissa bits, carry propagates into the exponent;
+        // 0x7F7FF000.. round up into 0x7F800000 = Inf, which is the overflow rule
+        return s | ((a + 0xFFFu + ((a >> 13) & 1u)) >> 13);
+    }
+
+    LAM_DEV uint32_t encode_e5m10_f32(uint32_t b)
+    {
+        const uint32_t a = b & 0x7FFFFFFFu;
+        if(a > 0x7F800000u)
+            return ((b >> 31) << 15) | 0x7E00u;
+        return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__uint_as_float(b))));
+    }
+
+    // ---- raw byte access ----------------------------------------------------------------
+    LAM_DEV uint64_t load_bytes(const uint8_t* p, uint32_t size, bool aligned)
+    {
+        if(aligned)
+        {
+            switch(size)
+            {
+            case 1:
+                return *p;
+            case 2:
+                return *reinterpret_cast<const uint16_t*>(p);
+            case 4:
+                return *reinterpret_cast<const uint32_t*>(p);
+            default:
+                return *reinterpret_cast<const unsigned long long*>(p);
+            }
+        }
+        uint64_t v = 0;
+        for(uint32_t k = 0; k < size; ++k)
+            v |= uint64_t(p[k]) << (8 * k);
+        return v;
+    }
+
+    LAM_DEV void store_bytes(uint8_t* p, uint32_t size, bool aligned, uint64_t v)
+    {
+        if(aligned)
+        {
+            switch(size)
+            {
+            case 1:
+                *p = static_cast<uint8_t>(v);
+                return;
+            case 2:
+                *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
+                return;
+            case 4:
+                *reinterpret_cast<uint32_t*>(p) = static_cast<uint32_t>(v);
+                return;
+            default:
+                *reinterpret_cast<unsigned long long*>(p) = v;
+                return;
+            }
+        }
+        for(uint32_t k = 0; k < size; ++k)
+            p[k] = static_cast<uint8_t>(v >> (8 * k));
+    }
+
+    // ---- bit streams (readBits/writeBits, bitpack.cpp:11-47) -----------------------------
+    LAM_DEV uint64_t read_bits(const uint32_t* w, uint64_t bitOff, uint32_t bits)
+    {
+        const uint64_t wi = bitOff >> 5;
+        const uint32_t sh = static_cast<uint32_t>(bitOff & 31);
+        const uint32_t need = sh + bits; // 1..95
+        uint64_t lo = w[wi];
+        if(need > 32)
+            lo |= uint64_t(w[wi + 1]) << 32;
+        uint64_t v = lo >> sh;
+        if(need > 64)
+            v |= uint64_t(w[wi + 2]) << (64 - sh);
+        return v & low_mask(bits);
+    }
+
+    // race-free against other threads writing other fields of the same words
+    LAM_DEV void write_bits_atomic(uint32_t* w, uint64_t bitOff, uint32_t bits, uint64_t v)
+    {
+        uint64_t wi = bitOff >> 5;
+        uint32_t sh = static_cast<uint32_t>(bitOff & 31);
+        uint32_t left = bits;
+        v &= low_mask(bits);
+        while(left > 0)
+        {
+            const uint32_t take = (32 - sh) < left ? (32 - sh) : left;
+            const uint32_t mask = static_cast<uint32_t>(low_mask(take)) << sh;
+            const uint32_t chunk = static_cast<uint32_t>(v & low_mask(take)) << sh;
+            if(mask == 0xFFFFFFFFu)
+                w[wi] = chunk;
+            else
+            {
+                atomicAnd(&w[wi], ~mask);
+                atomicOr(&w[wi], chunk);
+            }
+            v >>= take;
+            left -= take;
+            sh = 0;
+            ++wi;
+        }
+    }
+
+    // ---- plan interpreter ----------------------------------------------------------------
+    struct ViewCtx
+    {
+        const lamp_node* nodes;
+        const lamp_stream* streams;
+        uint8_t* const* sptr;
+        unsigned long long* heat;
+        const uint64_t* heatOff;
+        uint64_t gran;
+    };
+
+    LAM_DEV ViewCtx make_ctx(const lamp_view* v)
+    {
+        ViewCtx c;
+        c.nodes = v->nodes;
+        c.streams = v->streams;
+        c.sptr = v->stream_ptr;
+        c.heat = v->heat ? v->heat_counters : nullptr;
+        c.heatOff = v->heat_offset;
+        c.gran = v->heat_gran;
+        return c;
+    }
+
+    LAM_DEV uint64_t block_rel(const lamp_stream& st, uint64_t i, uint32_t inblock, uint32_t ls)
+    {
+        if(st.lanes == 1)
+            return i * st.block_stride + inblock;
+        uint64_t blk, lane;
+        if(st.lane_shift != 0xFFFFFFFFu)
+        {
+            blk = i >> st.lane_shift;
+            lane = i & (st.lanes - 1);
+        }
+        else
+        {
+            blk = i / st.lanes;
+            lane = i - blk * st.lanes;
+        }
+        return blk * st.block_stride + inblock + lane * ls;
+    }
+
+    LAM_DEV void heat_touch(const ViewCtx& v, uint32_t nr, uint64_t begin, uint64_t end)
+    {
+        if(begin >= end)
+            return;
+        const uint64_t first = begin / v.gran, last = (end - 1) / v.gran;
+        for(uint64_t b = first; b <= last; ++b)
+            atomicAdd(&v.heat[v.heatOff[nr] + b], 1ull);
+    }
+
+    template<int D>
+    __device__ __noinline__ uint64_t read_node(const ViewCtx& v, uint32_t n, uint64_t i)
+    {
+        const lamp_node nd = v.nodes[n];
+        switch(nd.kind)
+        {
+        case LAMP_PHYS:
+        {
+            const lamp_stream st = v.streams[nd.stream];
+            const uint64_t rel = block_rel(st, i, nd.a, nd.b);
+            const uint32_t size = scalar_size(nd.type);
+            uint64_t bits = load_bytes(v.sptr[nd.stream] + rel, size, nd.flags & LAMP_FLAG_ALIGNED);
+            if(v.heat)
+                heat_touch(v, st.nr, st.base0 + rel, st.base0 + rel + size);
+            return nd.type == BOOL ? uint64_t(bits != 0) : bits;
+        }
+        case LAMP_BITS_INT:
+        {
+            const uint64_t off = i * nd.a;
+            uint64_t p = read_bits(reinterpret_cast<const uint32_t*>(v.sptr[nd.stream]), off, nd.a);
+            if(v.heat)
+                heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + nd.a + 7) / 8);
+            if(nd.flags & LAMP_FLAG_SIGNED)
+            {
+                const uint64_t s = 1ull << (nd.a - 1);
+                p = (p ^ s) - s;
+            }
+            return p & low_mask(8 * scalar_size(nd.type));
+        }
+        case LAMP_BITS_FLT:
+        {
+            const uint32_t w = 1 + nd.a + nd.b;
+            const uint64_t off = i * w;
+            const uint64_t p = read_bits(reinterpret_cast<const uint32_t*>(v.sptr[nd.stream]), off, w);
+            if(v.heat)
+                heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + w + 7) / 8);
+            const uint64_t d = float_decode(p, nd.a, nd.b);
+            return nd.type == F32 ? f64_to_f32_bits(d) : d;
+        }
+        case LAMP_CONVERT:
+            if constexpr(D > 1)
+            {
+                const uint64_t c = read_node<D - 1>(v, nd.child, i);
+                return convert_value(c, v.nodes[nd.child].type, nd.type);
+            }
+            else
+                __trap();
+        case LAMP_SPLIT:
+            if constexpr(D > 1)
+            {
+                uint64_t acc = 0;
+                for(uint32_t k = 0; k < nd.nchild; ++k)
+                    acc |= (read_node<D - 1>(v, nd.child + k, i) & 0xFFull) << (8 * k);
+                return nd.type == BOOL ? uint64_t(acc != 0) : acc;
+            }
+            else
+                __trap();
+        default: // LAMP_NULL
+            return 0;
+        }
+    }
+
+    template<int D>
+    __device__ __noinline__ void write_node(const ViewCtx& v, uint32_t n, uint64_t i, uint64_t bits)
+    {
+        const lamp_node nd = v.nodes[n];
+        switch(nd.kind)
+        {
+        case LAMP_PHYS:
+        {
+            const lamp_stream st = v.streams[nd.stream];
+            const uint64_t rel = block_rel(st, i, nd.a, nd.b);
+            const uint32_t size = scalar_size(nd.type);
+            store_bytes(v.sptr[nd.stream] + rel, size, nd.flags & LAMP_FLAG_ALIGNED, bits);
+            if(v.heat)
+                heat_touch(v, st.nr, st.base0 + rel, st.base0 + rel + size);
+            return;
+        }
+        case LAMP_BITS_INT:
+        {
+            const uint64_t off = i * nd.a;
+            write_bits_atomic(reinterpret_cast<uint32_t*>(v.sptr[nd.stream]), off, nd.a, bits);
+            if(v.heat)
+                heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + nd.a + 7) / 8);
+            return;
+        }
+        case LAMP_BITS_FLT:
+        {
+            const uint32_t w = 1 + nd.a + nd.b;
+            const uint64_t off = i * w;
+            const uint64_t d = nd.type == F32 ? f32_to_f64_bits(static_cast<uint32_t>(bits)) : bits;
+            write_bits_atomic(reinterpret_cast<uint32_t*>(v.sptr[nd.stream]), off, w, float_encode(d, nd.a, nd.b));
+            if(v.heat)
+                heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + w + 7) / 8);
+            return;
+        }
+        case LAMP_CONVERT:
+            if constexpr(D > 1)
+                write_node<D - 1>(v, nd.child, i, convert_value(bits, nd.type, v.nodes[nd.child].type));
+            else
+                __trap();
+            return;
+        case LAMP_SPLIT:
+            if constexpr(D > 1)
+            {
+                for(uint32_t k = 0; k < nd.nchild; ++k)
+                    write_node<D - 1>(v, nd.child + k, i, (bits >> (8 * k)) & 0xFFull);
+            }
+            else
+                __trap();
+            return;
+        default: // LAMP_NULL: discarded
+            return;
+        }
+    }
+} // namespace lamd

@@ -1,0 +1,326 @@
+// lam_copy_host: copyView over HOST views, streamed through the GPU in element chunks.
+//
+//   h2d stream :  src stream regions of chunk k (+ dst regions that hold bytes the copy
+//                 never writes: padding, AoSoA tail lanes, the bit-stream tail word)
+//   comp stream:  chunk-view stream pointers -> tile / generic copy kernel over [a, e)
+//   d2h stream :  dst stream regions of chunk k back to the host blobs
+// with kSlots rotating device slots, so H2D(k+1), copy(k) and D2H(k-1) overlap and
+// PCIe runs full duplex.  A chunk starts on a multiple of both layouts' shard unit,
+// hence every stream region starts on a fresh AoSoA block / bit-stream word and is
+// 16-byte aligned; chunk views address the slot through "virtual" stream pointers
+// (slot address minus the region's blob offset), so kernels keep global indices —
+// heatmap blocks and counters stay exact.
+#include "capi_internal.hpp"
+
+#include <cstring>
+#include <map>
+#include <mutex>
+
+using namespace lamb;
+
+namespace lamhost
+{
+    namespace
+    {
+        std::mutex g_mu;
+        std::map<int, HostPipeline*> g_pipes;
+
+        uint64_t gcd64(uint64_t a, uint64_t b)
+        {
+            while(b)
+            {
+                const uint64_t t = a % b;
+                a = b;
+                b = t;
+            }
+            return a;
+        }
+
+        struct Region
+        {
+            uint64_t lo = 0, hi = 0; // blob byte range
+        };
+
+        Region regionOf(const lamp_stream& st, uint64_t a, uint64_t e, uint64_t blobSize)
+        {
+            Region r;
+            if(st.kind == LAMS_BITS)
+            {
+                const uint64_t b = st.block_stride;
+                r.lo = (a * b / 32) * 4;
+                r.hi = ((e * b + 31) / 32) * 4;
+            }
+            else
+            {
+                r.lo = st.base0 + (a / st.lanes) * st.block_stride;
+                r.hi = st.base0 + ((e + st.lanes - 1) / st.lanes) * st.block_stride;
+            }
+            if(r.hi > blobSize)
+                r.hi = blobSize;
+            if(r.lo > r.hi)
+                r.lo = r.hi;
+            return r;
+        }
+
+        uint64_t maxRegion(const lamp_stream& st, uint64_t C)
+        {
+            if(st.kind == LAMS_BITS)
+                return (C * st.block_stride + 31) / 32 * 4 + 16;
+            return (C / st.lanes + 2) * st.block_stride + 16;
+        }
+
+        bool sameLayout(const Map& a, const Map& b)
+        {
+            return a.name() == b.name() && !a.hasMutableState() && !b.hasMutableState() && a.isFullyPhysical()
+                && b.isFullyPhysical();
+        }
+
+        constexpr uint64_t kSlotTarget = uint64_t{192} << 20; // bytes of src+dst per chunk
+    } // namespace
+
+    HostPipeline& HostPipeline::get(int device)
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_pipes.find(device);
+        if(it == g_pipes.end())
+            it = g_pipes.emplace(device, new HostPipeline(device)).first;
+        return *it->second;
+    }
+
+    HostPipeline::HostPipeline(int device) : device_(device)
+    {
+        lam_cuda_check(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "stream");
+        lam_cuda_check(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking), "stream");
+        lam_cuda_check(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "stream");
+        for(int k = 0; k < kSlots; ++k)
+        {
+            lam_cuda_check(cudaEventCreateWithFlags(&evIn_[k], cudaEventDisableTiming), "event");
+            lam_cuda_check(cudaEventCreateWithFlags(&evDone_[k], cudaEventDisableTiming), "event");
+            lam_cuda_check(cudaEventCreateWithFlags(&evFree_[k], cudaEventDisableTiming), "event");
+        }
+    }
+
+    HostPipeline::~HostPipeline() = default; // process-lifetime singleton
+
+    void HostPipeline::ensure(size_t bytes)
+    {
+        if(bytes <= slotBytes_)
+            return;
+        lam_cuda_check(cudaDeviceSynchronize(), "sync");
+        for(auto& p : slot_)
+        {
+            if(p)
+                cudaFree(p);
+            p = nullptr;
+        }
+        for(auto& p : slot_)
+            lam_cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(pipeline slot)");
+        slotBytes_ = bytes;
+    }
+
+    void HostPipeline::run(const lam_layout& sl, const void* const* sb, const lam_layout& dl, void* const* db,
+                           uint64_t* srcCounters, uint64_t* dstCounters)
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        const Lowered& S = *sl.L;
+        const Lowered& D = *dl.L;
+        const Map& a = *S.map;
+        const Map& b = *D.map;
+        const uint64_t n = a.elementCount();
+        const size_t leaves = a.schema().leafCount();
+
+        // ---- copyView fast path: blob bytes streamed through the device blob copy ----------
+        if(sameLayout(a, b))
+        {
+            const uint64_t cb = (kSlotTarget / 2) & ~uint64_t{15};
+            ensure(2 * cb);
+            int k = 0;
+            for(size_t nr = 0; nr < a.blobCount(); ++nr)
+                for(uint64_t off = 0; off < a.blobSize(nr); off += cb, ++k)
+                {
+                    const int s = k % kSlots;
+                    const uint64_t len = std::min(cb, a.blobSize(nr) - off);
+                    uint8_t* in = static_cast<uint8_t*>(slot_[s]);
+                    uint8_t* out = in + cb;
+                    lam_cuda_check(cudaStreamWaitEvent(h2d_, evFree_[s], 0), "wait");
+                    lam_cuda_check(cudaMemcpyAsync(in, static_cast<const uint8_t*>(sb[nr]) + off, len,
+                                                   cudaMemcpyHostToDevice, h2d_), "h2d");
+                    lam_cuda_check(cudaEventRecord(evIn_[s], h2d_), "record");
+                    lam_cuda_check(cudaStreamWaitEvent(comp_, evIn_[s], 0), "wait");
+                    lam_cuda_check(lamk::blob_copy(out, in, len, comp_), "blob_copy");
+                    lam_cuda_check(cudaEventRecord(evDone_[s], comp_), "record");
+                    lam_cuda_check(cudaStreamWaitEvent(d2h_, evDone_[s], 0), "wait");
+                    lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(db[nr]) + off, out, len,
+                                                   cudaMemcpyDeviceToHost, d2h_), "d2h");
+                    lam_cuda_check(cudaEventRecord(evFree_[s], d2h_), "record");
+                }
+            lam_cuda_check(cudaStreamSynchronize(d2h_), "sync");
+            if(srcCounters && S.fac)
+                std::memset(srcCounters, 0, 2 * leaves * 8);
+            if(dstCounters && D.fac)
+                std::memset(dstCounters, 0, 2 * leaves * 8);
+            return;
+        }
+        if(n == 0 || leaves == 0)
+            return;
+
+        // ---- chunking ---------------------------------------------------------------------
+        const uint64_t unit = S.shardUnit / gcd64(S.shardUnit, D.shardUnit) * D.shardUnit;
+        double bpe = 0;
+        for(const auto& st : S.streams)
+            bpe += st.kind == LAMS_BITS ? st.block_stride / 8.0 : double(st.block_stride) / st.lanes;
+        for(const auto& st : D.streams)
+            bpe += st.kind == LAMS_BITS ? st.block_stride / 8.0 : double(st.block_stride) / st.lanes;
+        uint64_t C = bpe > 0 ? static_cast<uint64_t>(kSlotTarget / bpe) : n;
+        C = std::max<uint64_t>(unit, C / unit * unit);
+        if(C > n)
+            C = (n + unit - 1) / unit * unit;
+
+        // fixed per-stream offsets inside a slot
+        std::vector<uint64_t> soff(S.streams.size()), doff(D.streams.size());
+        uint64_t used = 0;
+        for(size_t s = 0; s < S.streams.size(); ++s)
+        {
+            soff[s] = used;
+            used += (maxRegion(S.streams[s], C) + 15) & ~uint64_t{15};
+        }
+        for(size_t s = 0; s < D.streams.size(); ++s)
+        {
+            doff[s] = used;
+            used += (maxRegion(D.streams[s], C) + 15) & ~uint64_t{15};
+        }
+        ensure(used);
+
+        // shared heatmaps (global block indices), per-slot images
+        void* sheat = nullptr;
+        void* dheat = nullptr;
+        if(S.heat && S.heatTotal)
+        {
+            lam_cuda_check(cudaMalloc(&sheat, S.heatTotal * 8), "cudaMalloc(heat)");
+            lam_cuda_check(cudaMemset(sheat, 0, S.heatTotal * 8), "memset");
+        }
+        if(D.heat && D.heatTotal)
+        {
+            lam_cuda_check(cudaMalloc(&dheat, D.heatTotal * 8), "cudaMalloc(heat)");
+            lam_cuda_check(cudaMemset(dheat, 0, D.heatTotal * 8), "memset");
+        }
+        struct HeatFree
+        {
+            void* p;
+            ~HeatFree()
+            {
+                if(p)
+                    cudaFree(p);
+            }
+        } hf1{sheat}, hf2{dheat};
+
+        std::vector<uint8_t*> zeroS(S.streams.size(), nullptr), zeroD(D.streams.size(), nullptr);
+        DeviceImage simg[kSlots], dimg[kSlots];
+        for(int k = 0; k < kSlots; ++k)
+        {
+            simg[k].build(S, device_, zeroS, sheat);
+            dimg[k].build(D, device_, zeroD, dheat);
+        }
+        const size_t ptrBytes = (S.streams.size() + D.streams.size()) * sizeof(uint8_t*);
+        std::vector<uint8_t*> pinned; // per slot table lives in pinned host memory
+        void* ptab = nullptr;
+        lam_cuda_check(cudaMallocHost(&ptab, std::max<size_t>(ptrBytes, 8) * kSlots), "cudaMallocHost");
+        struct HostFree
+        {
+            void* p;
+            ~HostFree()
+            {
+                cudaFreeHost(p);
+            }
+        } hfree{ptab};
+
+        const uint64_t nchunks = (n + C - 1) / C;
+        for(uint64_t k = 0; k < nchunks; ++k)
+        {
+            const int s = static_cast<int>(k % kSlots);
+            const uint64_t lo = k * C, hi = std::min(n, lo + C);
+            const bool last = k + 1 == nchunks;
+            if(k >= static_cast<uint64_t>(kSlots))
+                lam_cuda_check(cudaEventSynchronize(evFree_[s]), "sync slot");
+            uint8_t* slot = static_cast<uint8_t*>(slot_[s]);
+            auto* tab = reinterpret_cast<uint8_t**>(static_cast<uint8_t*>(ptab) + s * std::max<size_t>(ptrBytes, 8));
+
+            lam_cuda_check(cudaStreamWaitEvent(h2d_, evFree_[s], 0), "wait");
+            for(size_t t = 0; t < S.streams.size(); ++t)
+            {
+                const auto& st = S.streams[t];
+                const Region r = regionOf(st, lo, hi, a.blobSize(st.nr));
+                uint8_t* dev = slot + soff[t] + (r.lo & 15);
+                tab[t] = dev - (r.lo - st.base0);
+                if(r.hi > r.lo)
+                    lam_cuda_check(cudaMemcpyAsync(dev, static_cast<const uint8_t*>(sb[st.nr]) + r.lo, r.hi - r.lo,
+                                                   cudaMemcpyHostToDevice, h2d_), "h2d");
+            }
+            for(size_t t = 0; t < D.streams.size(); ++t)
+            {
+                const auto& st = D.streams[t];
+                const Region r = regionOf(st, lo, hi, b.blobSize(st.nr));
+                uint8_t* dev = slot + doff[t] + (r.lo & 15);
+                tab[S.streams.size() + t] = dev - (r.lo - st.base0);
+                if((!st.holefree || last) && r.hi > r.lo)
+                    lam_cuda_check(cudaMemcpyAsync(dev, static_cast<const uint8_t*>(db[st.nr]) + r.lo, r.hi - r.lo,
+                                                   cudaMemcpyHostToDevice, h2d_), "h2d");
+            }
+            lam_cuda_check(cudaEventRecord(evIn_[s], h2d_), "record");
+
+            lam_cuda_check(cudaStreamWaitEvent(comp_, evIn_[s], 0), "wait");
+            if(!S.streams.empty())
+                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(simg[s].mem) + simg[s].offPtrs, tab,
+                                               S.streams.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice, comp_),
+                               "ptr table");
+            if(!D.streams.empty())
+                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dimg[s].mem) + dimg[s].offPtrs,
+                                               tab + S.streams.size(), D.streams.size() * sizeof(uint8_t*),
+                                               cudaMemcpyHostToDevice, comp_),
+                               "ptr table");
+            if(!tileCopyImages(S, simg[s], D, dimg[s], lo, hi, comp_))
+                lam_cuda_check(lamk::generic_copy(simg[s].hdr, dimg[s].hdr, lo, hi, static_cast<uint32_t>(leaves), S.fac,
+                                                  D.fac, comp_),
+                               "generic_copy");
+            lam_cuda_check(cudaEventRecord(evDone_[s], comp_), "record");
+
+            lam_cuda_check(cudaStreamWaitEvent(d2h_, evDone_[s], 0), "wait");
+            for(size_t t = 0; t < D.streams.size(); ++t)
+            {
+                const auto& st = D.streams[t];
+                const Region r = regionOf(st, lo, hi, b.blobSize(st.nr));
+                if(r.hi > r.lo)
+                    lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(db[st.nr]) + r.lo, slot + doff[t] + (r.lo & 15),
+                                                   r.hi - r.lo, cudaMemcpyDeviceToHost, d2h_), "d2h");
+            }
+            lam_cuda_check(cudaEventRecord(evFree_[s], d2h_), "record");
+        }
+        lam_cuda_check(cudaStreamSynchronize(d2h_), "sync");
+        lam_cuda_check(cudaStreamSynchronize(comp_), "sync");
+
+        // counters: FieldAccessCount summed over slots, then the heatmap blocks
+        auto gather = [&](const Lowered& L, DeviceImage* imgs, void* heat, uint64_t* out)
+        {
+            if(!out)
+                return;
+            size_t pos = 0;
+            if(L.fac)
+            {
+                std::vector<uint64_t> sum(2 * leaves, 0), part(2 * leaves);
+                for(int k = 0; k < kSlots; ++k)
+                {
+                    lam_cuda_check(cudaMemcpy(part.data(), imgs[k].facDev, 2 * leaves * 8, cudaMemcpyDeviceToHost),
+                                   "counters");
+                    for(size_t j = 0; j < 2 * leaves; ++j)
+                        sum[j] += part[j];
+                }
+                std::memcpy(out, sum.data(), 2 * leaves * 8);
+                pos = 2 * leaves;
+            }
+            if(L.heat && L.heatTotal)
+                lam_cuda_check(cudaMemcpy(out + pos, heat, L.heatTotal * 8, cudaMemcpyDeviceToHost), "heatmap");
+        };
+        gather(S, simg, sheat, srcCounters);
+        gather(D, dimg, dheat, dstCounters);
+    }
+} // namespace lamhost

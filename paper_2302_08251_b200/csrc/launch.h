@@ -1,0 +1,28 @@
+// Host-callable launchers implemented in the .cu translation units.
+#pragma once
+
+#include "lam_plan.h"
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace lamk
+{
+    // counts every kernel this library launches (reported as gpu_launches)
+    void count_launch(uint64_t n = 1);
+    uint64_t launch_count();
+
+    int sm_count(int device);
+
+    // generic fieldwise copy over [begin, end): one thread per element, all leaves,
+    // plan interpreter on both sides (copy_generic.cu)
+    cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,
+                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s);
+    // byte-exact blob copy (copyView's sameLayout memcpy path)
+    cudaError_t blob_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
+    cudaError_t read_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, uint64_t* out, size_t n,
+                            cudaStream_t s);
+    cudaError_t write_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, const uint64_t* in,
+                             size_t n, cudaStream_t s);
+} // namespace lamk
