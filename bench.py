@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 layout-copy hot path (BASELINE.json config C2).
+
+Step = one pass of lamina::copyView over all 25 ordered pairs of
+{aos-packed, soa-sb, soa-mb, aosoa:8, aosoa:32} on 2^26 n-body records
+(Record{Pos{x,y,z},Vel{x,y,z},Mass}, 7 x f32 = 28 B) per GPU.  5 pairs take the
+reference's blob-memcpy path (view.cpp:175-181), 20 the fieldwise layout transpose.
+Algorithmic bytes = source leaf bytes read + destination leaf bytes written
+= 56 B per record per pair.
+
+  value  : whole-job GB/s, device-resident views, CUDA events, max over ranks
+  e2e    : same metric through lam_copy_host (host pinned blobs in and out, H2D/D2H
+           inside the timed region)
+  roofline: dominant kernel k_tile_copy, algorithmic bytes / mean launch time vs the
+           measured HBM copy peak (MEASURED_PEAKS.json)
+  cpu_baseline: the reference itself (oracle/_ref, compiled from /root/reference) on a
+           bounded sample, 1 host core
+
+--impl reference : the reference's CPU copyView loop (oracle/_ref) on all host cores.
+--suite          : additionally time configs C1, C3, C5 and n-body (C4) on this GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+R32 = "Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}"
+R64 = "Record{Pos:Record{x:f64,y:f64,z:f64},Vel:Record{x:f64,y:f64,z:f64},Mass:f64}"
+C2_LAYOUTS = ["aos-packed", "soa-sb", "soa-mb", "aosoa:8", "aosoa:32"]
+METRIC = "layout-copy and bitpack GB/s (frac of HBM peak) at 1/2/4/8 B200; n-body interactions/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p.get("hbm_gbs", 6650.0)), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if parts[2 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def fill_source(L, view, layout_text, n, seed, stream):
+    """Synthetic source content: random u32 patterns per (i, f) including NaN/sNaN/±0/
+    denormal bit patterns — a layout copy is a byte permutation, so every pattern must
+    survive.  Generated once in aos-packed on the device, then copied into `view`."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    raw = torch.randint(0, 2**31 - 1, (n * 7,), device="cuda", dtype=torch.int32, generator=g)
+    raw = raw.view(torch.uint8)
+    aos = L.Layout(R32, f"i32:[{n}]", "aos-packed")
+    tmp = L.View(aos, blobs=[raw.data_ptr()], blob_bytes=[raw.numel()])
+    L.copy_view(tmp, view, stream=stream)
+    torch.cuda.synchronize()
+    del tmp, raw
+
+
+def run_c2(L, n, steps, warmup, world, local):
+    import torch
+    stream = torch.cuda.Stream()
+    ext = f"i32:[{n}]"
+    lays = {a: L.Layout(R32, ext, a) for a in C2_LAYOUTS}
+    srcs = {a: L.View(lays[a], device=local) for a in C2_LAYOUTS}
+    dsts = {a: L.View(lays[a], device=local) for a in C2_LAYOUTS}
+    for k, a in enumerate(C2_LAYOUTS):
+        fill_source(L, srcs[a], a, n, 1234 + k, stream)
+    pairs = [(a, b) for a in C2_LAYOUTS for b in C2_LAYOUTS]
+    bytes_pair = 56 * n
+    ev = [{p: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for p in pairs}
+          for _ in range(steps)]
+    for _ in range(warmup):
+        for a, b in pairs:
+            L.copy_view(srcs[a], dsts[b], stream=stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches0 = L.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for s in range(steps):
+            for p in pairs:
+                ev[s][p][0].record(stream)
+                L.copy_view(srcs[p[0]], dsts[p[1]], stream=stream)
+                ev[s][p][1].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = L.launch_count() - launches0
+    total_ms = e0.elapsed_time(e1)
+    pair_ms = {p: sum(ev[s][p][0].elapsed_time(ev[s][p][1]) for s in range(steps)) for p in pairs}
+    ms_max = max_over_ranks(total_ms / steps, world)
+    bytes_step = bytes_pair * len(pairs)
+    value = sum_over_ranks(bytes_step, world) / (ms_max * 1e-3) / 1e9
+    cross = [p for p in pairs if p[0] != p[1]]
+    tile_ms = sum(pair_ms[p] for p in cross) / (steps * len(cross))
+    achieved = bytes_pair / (tile_ms * 1e-3) / 1e9
+    per_pair = {f"{a}->{b}": round(bytes_pair / (pair_ms[(a, b)] / steps * 1e-3) / 1e9, 1) for a, b in pairs}
+    out = {"ms_per_step": ms_max, "value": value, "launches": launches, "clocks": clk.summary(),
+           "achieved_tile": achieved, "tile_ms": tile_ms, "per_pair_gbs": per_pair, "bytes_step": bytes_step,
+           "wall_ms_per_step": total_ms / steps}
+    del srcs, dsts
+    torch.cuda.synchronize()
+    return out
+
+
+def run_c2_e2e(L, n, steps, local):
+    """Same workload through lam_copy_host: pinned host blobs, H2D + copy + D2H per pair."""
+    import torch
+    ext = f"i32:[{n}]"
+    lays = {a: L.Layout(R32, ext, a) for a in C2_LAYOUTS}
+    rng = np.random.default_rng(7)
+    src = {}
+    for a in C2_LAYOUTS:
+        blobs = []
+        for s in lays[a].blob_sizes:
+            t = torch.empty(s, dtype=torch.uint8, pin_memory=True)
+            arr = t.numpy()
+            arr[:] = rng.integers(0, 256, s, dtype=np.uint8)
+            blobs.append((t, arr))
+        src[a] = blobs
+    dst = {a: [(lambda t: (t, t.numpy()))(torch.zeros(s, dtype=torch.uint8, pin_memory=True))
+               for s in lays[a].blob_sizes] for a in C2_LAYOUTS}
+    pairs = [(a, b) for a in C2_LAYOUTS for b in C2_LAYOUTS]
+    h2d = sum(sum(lays[a].blob_sizes) for a, b in pairs)
+    d2h = sum(sum(lays[b].blob_sizes) for a, b in pairs)
+    # warm-up: one pass (allocates the pipeline slots)
+    for a, b in pairs[:6]:
+        L.copy_view_host(lays[a], [x for _, x in src[a]], lays[b], [x for _, x in dst[b]], device=local)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for a, b in pairs:
+            L.copy_view_host(lays[a], [x for _, x in src[a]], lays[b], [x for _, x in dst[b]], device=local)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": 56 * n * len(pairs) / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "s_per_step": dt, "api": "lam_copy_host (pinned host blobs)"}
+
+
+def cpu_reference_c2(n, nthreads, repeats=1):
+    """The reference's copyView (oracle/_ref) over the 25 pairs on n records."""
+    from oracle import ref
+    ext = f"i32:[{n}]"
+    rng = np.random.default_rng(3)
+    total_s = 0.0
+    src = {}
+    for a in C2_LAYOUTS:
+        src[a] = [rng.integers(0, 256, s, dtype=np.uint8) for s in ref.layout_info(R32, ext, a)["blob_sizes"]]
+    for a in C2_LAYOUTS:
+        for b in C2_LAYOUTS:
+            dst = ref.zero_blobs(R32, ext, b)
+            r = ref.copy(R32, ext, a, src[a], b, dst, nthreads=nthreads, repeats=repeats)
+            total_s += r["seconds"]
+    return 56 * n * 25 / total_s / 1e9, total_s
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--records", type=int, default=1 << 26)
+    ap.add_argument("--cpu-records", type=int, default=1 << 20)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--suite", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    n = args.records
+    config = {"workload": "C2: copyView over all 25 ordered pairs of {aos-packed, soa-sb, soa-mb, aosoa:8, aosoa:32}",
+              "record": "n-body Record{Pos{x,y,z},Vel{x,y,z},Mass} 7 x f32 = 28 B", "records_per_gpu": n,
+              "extents": f"i32:[{n}]", "bytes_per_record_pair": 56, "pairs": 25,
+              "l2": "no flush needed: every view is 28 B x 2^26 = 1.88 GB >> 126 MB L2",
+              "parallelism": f"weak: {world} independent shard(s), no collective"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import ref
+        if not ref.available():
+            ref.build()
+        threads = os.cpu_count() or 1
+        samples = []
+        for _ in range(args.warmup):
+            cpu_reference_c2(args.cpu_records * 4, threads)
+        for _ in range(args.steps):
+            v, s = cpu_reference_c2(args.cpu_records * 4, threads)
+            samples.append(s)
+        total = float(np.median(samples))
+        value = 56 * args.cpu_records * 4 * 25 / total / 1e9
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+                "config": dict(config, records_per_step=args.cpu_records * 4),
+                "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
+                                 "sample": f"25 pairs x {args.cpu_records * 4} records per step (bounded sample of C2)"},
+                "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2302_08251_b200 import lamina as L
+    res = run_c2(L, n, args.steps, max(3, args.warmup), world, local)
+    peak, peak_kind = peaks()
+    line = {"metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (random u32 bit patterns)",
+            "config": config, "gpu_launches": res["launches"], "clocks": res["clocks"]}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "tile_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    line["roofline"] = {"bound": "hbm", "kernel": "k_tile_copy (20 cross-layout pairs)",
+                        "achieved": res["achieved_tile"], "peak": peak, "unit": "GB/s",
+                        "frac": res["achieved_tile"] / peak, "traffic": traffic,
+                        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                        "algorithmic_bytes_per_launch": 56 * n}
+    line["per_pair_gbs"] = res["per_pair_gbs"]
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = run_c2_e2e(L, n, args.e2e_steps, local)
+    if rank == 0 and not args.no_cpu:
+        from oracle import ref
+        if ref.available():
+            v, s = cpu_reference_c2(args.cpu_records, 1)
+            line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": 1, "kind": "reference",
+                                    "sample": f"25 pairs x {args.cpu_records} records (bounded sample of C2), "
+                                              f"reference copyView single-threaded, {s:.1f} s"}
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
+                                    "sample": "oracle/_ref not built"}
+    if args.suite and rank == 0:
+        from bench_suite import run_suite
+        line["suite"] = run_suite(L, local)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

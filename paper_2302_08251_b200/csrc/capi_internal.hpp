@@ -106,6 +106,10 @@ namespace lamhost
     // same on raw images (used by the host pipeline's chunk views)
     bool tileCopyImages(const lamb::Lowered& SL, const DeviceImage& si, const lamb::Lowered& DL, DeviceImage& di,
                         uint64_t begin, uint64_t end, cudaStream_t s);
+    // same with explicit (virtual) stream pointers, as chunk views use them
+    bool tileCopyPtrs(const lamb::Lowered& SL, const DeviceImage& si, uint8_t* const* sptr, const lamb::Lowered& DL,
+                      DeviceImage& di, uint8_t* const* dptr, uint64_t begin, uint64_t end, cudaStream_t s);
+    bool tileEligible(const lamb::Lowered& SL, const lamb::Lowered& DL);
 
     // per-device chunked H2D -> copy -> D2H pipeline behind lam_copy_host (host_pipeline.cpp)
     class HostPipeline

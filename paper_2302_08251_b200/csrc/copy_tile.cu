@@ -1,0 +1,503 @@
+// Tile engine: persistent, double-buffered, TMA-bulk-staged layout copy (K1/K3/K4/K5/K6).
+//
+// Per CTA, per tile of T elements:
+//   load      every source stream image  HBM -> smem   (cp.async.bulk + mbarrier tx count)
+//   transform per leaf, per element: read terminal(s) from the source image, convert,
+//             write terminal(s) into the destination image (PHYS / byte planes) or into
+//             a per-element pattern scratch (bit-packed destinations)
+//   pack      bit-packed destinations: each thread owns whole 32-bit words and
+//             funnel-shifts them together from the scratch (no RMW, no atomics)
+//   store     every destination image smem -> HBM   (cp.async.bulk bulk_group)
+// The next tile's loads are in flight during the transform of the current one, and the
+// stores of tile k drain while tile k+1 is transformed.  HBM traffic is exactly the
+// algorithmic bytes (each source/destination byte moves once); the element-granular
+// shuffling happens in shared memory, where AoS strides (7 words for the 28-byte
+// record) are bank-conflict free.
+#include "device_common.cuh"
+#include "launch.h"
+#include "tile.h"
+
+namespace lamk
+{
+    namespace
+    {
+        __device__ __forceinline__ uint32_t smem_u32(const void* p)
+        {
+            return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+        }
+
+        __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+        {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+        }
+
+        __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+        {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                         : "memory");
+        }
+
+        __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+        {
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "LAB_WAIT:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra LAB_WAIT;\n"
+                "}\n" ::"r"(smem_u32(bar)),
+                "r"(parity)
+                : "memory");
+        }
+
+        __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar)
+        {
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(smem)),
+                "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                : "memory");
+        }
+
+        __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes)
+        {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+                         "r"(bytes)
+                         : "memory");
+        }
+
+        __device__ __forceinline__ void bulk_commit()
+        {
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+
+        template<int N>
+        __device__ __forceinline__ void bulk_wait_read()
+        {
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+        }
+
+        __device__ __forceinline__ void bulk_wait_all()
+        {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+
+        __device__ __forceinline__ void fence_async_smem()
+        {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+
+        __device__ __forceinline__ uint64_t tile_global_off(const lamt_stream& s, uint64_t tileStart)
+        {
+            if(s.kind == 1)
+                return (tileStart * s.bs) >> 3; // tileStart*bits is a multiple of 128
+            const uint64_t blk = s.lshift != 0xFFFFFFFFu ? (tileStart >> s.lshift) : tileStart / s.lanes;
+            return blk * s.bs;
+        }
+
+        __device__ __forceinline__ uint32_t image_rel(const lamt_stream& s, uint32_t e, const lamt_term& t)
+        {
+            if(s.lanes == 1)
+                return e * s.bs + t.inblock;
+            uint32_t blk, lane;
+            if(s.lshift != 0xFFFFFFFFu)
+            {
+                blk = e >> s.lshift;
+                lane = e & (s.lanes - 1);
+            }
+            else
+            {
+                blk = e / s.lanes;
+                lane = e - blk * s.lanes;
+            }
+            return blk * s.bs + t.inblock + lane * t.ls;
+        }
+
+        __device__ __forceinline__ uint64_t lds_bytes(const uint8_t* p, uint32_t size, bool aligned)
+        {
+            return lamd::load_bytes(p, size, aligned);
+        }
+
+        // cooperative copy for images whose global start is not 16-byte aligned
+        __device__ void coop_g2s(uint8_t* smem, const uint8_t* g, uint32_t bytes)
+        {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+            if((a & 3) == 0 && (bytes & 3) == 0)
+            {
+                const uint32_t* gs = reinterpret_cast<const uint32_t*>(g);
+                uint32_t* ss = reinterpret_cast<uint32_t*>(smem);
+                for(uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x)
+                    ss[k] = __ldg(gs + k);
+            }
+            else
+                for(uint32_t k = threadIdx.x; k < bytes; k += blockDim.x)
+                    smem[k] = __ldg(g + k);
+        }
+
+        __device__ void coop_s2g(uint8_t* g, const uint8_t* smem, uint32_t bytes)
+        {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+            if((a & 3) == 0 && (bytes & 3) == 0)
+            {
+                uint32_t* gd = reinterpret_cast<uint32_t*>(g);
+                const uint32_t* ss = reinterpret_cast<const uint32_t*>(smem);
+                for(uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x)
+                    gd[k] = ss[k];
+            }
+            else
+                for(uint32_t k = threadIdx.x; k < bytes; k += blockDim.x)
+                    g[k] = smem[k];
+        }
+
+        // read the storage value of one leaf for tile-local element e from the source images
+        __device__ __forceinline__ uint64_t tile_read(const lamt_params& p, const lamt_leaf& L, const uint8_t* sbuf,
+                                                      uint32_t e)
+        {
+            switch(L.skind)
+            {
+            case LAMT_K_PHYS:
+            {
+                const lamt_term& t = L.s[0];
+                const lamt_stream& s = p.st[t.stream];
+                uint64_t v = lds_bytes(sbuf + s.smem_off + image_rel(s, e, t), t.size, t.aligned);
+                return L.stype == lamd::BOOL ? uint64_t(v != 0) : v;
+            }
+            case LAMT_K_SPLIT:
+            {
+                uint64_t v = 0;
+                for(uint32_t k = 0; k < L.sn; ++k)
+                {
+                    const lamt_term& t = L.s[k];
+                    const lamt_stream& s = p.st[t.stream];
+                    v |= uint64_t(sbuf[s.smem_off + image_rel(s, e, t)]) << (8 * k);
+                }
+                return L.stype == lamd::BOOL ? uint64_t(v != 0) : v;
+            }
+            case LAMT_K_BITS_INT:
+            {
+                const lamt_stream& s = p.st[L.s[0].stream];
+                uint64_t pat = lamd::read_bits(reinterpret_cast<const uint32_t*>(sbuf + s.smem_off),
+                                               uint64_t(e) * L.sE, L.sE);
+                if(L.ssigned)
+                {
+                    const uint64_t sb = 1ull << (L.sE - 1);
+                    pat = (pat ^ sb) - sb;
+                }
+                return pat & lamd::low_mask(8 * lamd::scalar_size(L.stype));
+            }
+            case LAMT_K_BITS_FLT:
+            {
+                const lamt_stream& s = p.st[L.s[0].stream];
+                const uint32_t w = 1 + L.sE + L.sM;
+                const uint64_t pat = lamd::read_bits(reinterpret_cast<const uint32_t*>(sbuf + s.smem_off),
+                                                     uint64_t(e) * w, w);
+                if(L.stype == lamd::F32 && L.sE == 8 && L.sM == 10)
+                {
+                    const uint32_t pp = static_cast<uint32_t>(pat);
+                    const uint32_t sign = (pp >> 18) << 31;
+                    if((pp & 0x3FC00u) == 0x3FC00u && (pp & 0x3FFu))
+                        return sign | 0x7FC00000u;
+                    return sign | ((pp & 0x3FFFFu) << 13);
+                }
+                if(L.stype == lamd::F32 && L.sE == 5 && L.sM == 10)
+                {
+                    const uint32_t pp = static_cast<uint32_t>(pat);
+                    if((pp & 0x7C00u) == 0x7C00u && (pp & 0x3FFu))
+                        return ((pp >> 15) << 31) | 0x7FC00000u;
+                    return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pp))));
+                }
+                const uint64_t d = lamd::float_decode(pat, L.sE, L.sM);
+                return L.stype == lamd::F32 ? lamd::f64_to_f32_bits(d) : d;
+            }
+            default:
+                return 0;
+            }
+        }
+
+        __device__ __forceinline__ void tile_write(const lamt_params& p, const lamt_leaf& L, uint8_t* dbuf, uint32_t e,
+                                                   uint64_t v)
+        {
+            switch(L.dkind)
+            {
+            case LAMT_K_PHYS:
+            {
+                const lamt_term& t = L.d[0];
+                const lamt_stream& s = p.st[t.stream];
+                lamd::store_bytes(dbuf + s.smem_off + image_rel(s, e, t), t.size, t.aligned, v);
+                return;
+            }
+            case LAMT_K_SPLIT:
+                for(uint32_t k = 0; k < L.dn; ++k)
+                {
+                    const lamt_term& t = L.d[k];
+                    const lamt_stream& s = p.st[t.stream];
+                    dbuf[s.smem_off + image_rel(s, e, t)] = static_cast<uint8_t>(v >> (8 * k));
+                }
+                return;
+            case LAMT_K_BITS_INT:
+            {
+                const lamt_stream& s = p.st[L.d[0].stream];
+                const uint64_t pat = v & lamd::low_mask(L.dE);
+                if(s.scratch64)
+                    reinterpret_cast<unsigned long long*>(dbuf + s.scratch_off)[e] = pat;
+                else
+                    reinterpret_cast<uint32_t*>(dbuf + s.scratch_off)[e] = static_cast<uint32_t>(pat);
+                return;
+            }
+            case LAMT_K_BITS_FLT:
+            {
+                const lamt_stream& s = p.st[L.d[0].stream];
+                uint64_t pat;
+                if(L.dtype == lamd::F32 && L.dE == 8 && L.dM == 10)
+                    pat = lamd::encode_e8m10_f32(static_cast<uint32_t>(v));
+                else if(L.dtype == lamd::F32 && L.dE == 5 && L.dM == 10)
+                    pat = lamd::encode_e5m10_f32(static_cast<uint32_t>(v));
+                else
+                {
+                    const uint64_t d = L.dtype == lamd::F32 ? lamd::f32_to_f64_bits(static_cast<uint32_t>(v)) : v;
+                    pat = lamd::float_encode(d, L.dE, L.dM);
+                }
+                if(s.scratch64)
+                    reinterpret_cast<unsigned long long*>(dbuf + s.scratch_off)[e] = pat;
+                else
+                    reinterpret_cast<uint32_t*>(dbuf + s.scratch_off)[e] = static_cast<uint32_t>(pat);
+                return;
+            }
+            default:
+                return;
+            }
+        }
+
+        // whole-word assembly of a bit-packed destination image from its pattern scratch
+        __device__ __forceinline__ void pack_words(const lamt_stream& s, uint8_t* dbuf, uint32_t T)
+        {
+            const uint32_t w = s.bs;
+            const uint32_t words = T * w / 32;
+            uint32_t* out = reinterpret_cast<uint32_t*>(dbuf + s.smem_off);
+            if(!s.scratch64)
+            {
+                const uint32_t* sc = reinterpret_cast<const uint32_t*>(dbuf + s.scratch_off);
+                for(uint32_t q = threadIdx.x; q < words; q += blockDim.x)
+                {
+                    const uint32_t bit = q * 32;
+                    uint32_t k = bit / w;
+                    const uint32_t o = bit - k * w;
+                    uint64_t acc = uint64_t(sc[k]) >> o;
+                    uint32_t pos = w - o;
+                    ++k;
+                    while(pos < 32)
+                    {
+                        acc |= uint64_t(sc[k]) << pos;
+                        pos += w;
+                        ++k;
+                    }
+                    out[q] = static_cast<uint32_t>(acc);
+                }
+            }
+            else
+            {
+                const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(dbuf + s.scratch_off);
+                for(uint32_t q = threadIdx.x; q < words; q += blockDim.x)
+                {
+                    const uint64_t bit = uint64_t(q) * 32;
+                    uint64_t k = bit / w;
+                    const uint32_t o = static_cast<uint32_t>(bit - k * w);
+                    uint64_t acc = sc[k] >> o;
+                    const uint32_t pos = w - o;
+                    if(pos < 32)
+                        acc |= sc[k + 1] << pos;
+                    out[q] = static_cast<uint32_t>(acc);
+                }
+            }
+        }
+    } // namespace
+
+    __global__ void __launch_bounds__(512, 2) k_tile_copy(const __grid_constant__ lamt_params p)
+    {
+        extern __shared__ __align__(128) uint8_t smem[];
+        __shared__ __align__(8) uint64_t mbar[2];
+        uint8_t* sbuf[2] = {smem, smem + p.src_bytes};
+        uint8_t* dbuf[2] = {smem + 2 * p.src_bytes, smem + 2 * p.src_bytes + p.dst_bytes};
+        const bool lead = threadIdx.x == 0;
+        if(lead)
+        {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+
+        auto issue_load = [&](uint32_t tile, int stage)
+        {
+            const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+            if(p.tma_bytes)
+                mbar_expect_tx(&mbar[stage], p.tma_bytes);
+            else
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[stage])) : "memory");
+            for(uint32_t k = 0; k < p.nsrc; ++k)
+            {
+                const lamt_stream& s = p.st[k];
+                if(s.tma && s.tile_bytes)
+                    bulk_g2s(sbuf[stage] + s.smem_off,
+                             reinterpret_cast<const uint8_t*>(s.gptr) + tile_global_off(s, t0), s.tile_bytes,
+                             &mbar[stage]);
+            }
+        };
+
+        const uint32_t first = blockIdx.x;
+        if(lead && first < p.ntiles)
+            issue_load(first, 0);
+        uint32_t done = 0;
+        for(uint32_t k = 0;; ++k)
+        {
+            const uint32_t tile = first + k * gridDim.x;
+            if(tile >= p.ntiles)
+                break;
+            const int st = k & 1;
+            const uint32_t next = tile + gridDim.x;
+            if(lead && next < p.ntiles)
+                issue_load(next, st ^ 1);
+            const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+            // non-TMA source images: cooperative loads
+            for(uint32_t j = 0; j < p.nsrc; ++j)
+            {
+                const lamt_stream& s = p.st[j];
+                if(!s.tma && s.tile_bytes)
+                    coop_g2s(sbuf[st] + s.smem_off, reinterpret_cast<const uint8_t*>(s.gptr) + tile_global_off(s, t0),
+                             s.tile_bytes);
+            }
+            mbar_wait(&mbar[st], (k >> 1) & 1);
+            if(lead)
+                bulk_wait_read<1>(); // stores of tile k-2 have left dbuf[st]
+            __syncthreads();
+
+            // ---- transform ----
+            const uint8_t* sb = sbuf[st];
+            uint8_t* db = dbuf[st];
+            for(uint32_t f = 0; f < p.nleaves; ++f)
+            {
+                const lamt_leaf& L = p.leaf[f];
+                if(L.pure)
+                {
+                    // PHYS -> PHYS, same scalar: a byte permutation (Bool still canonicalises)
+                    const lamt_term& ts = L.s[0];
+                    const lamt_term& td = L.d[0];
+                    const lamt_stream& ss = p.st[ts.stream];
+                    const lamt_stream& ds = p.st[td.stream];
+                    const uint8_t* sbase = sb + ss.smem_off;
+                    uint8_t* dbase = db + ds.smem_off;
+                    if(ts.size == 4 && ts.aligned && td.aligned)
+                    {
+                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                            *reinterpret_cast<uint32_t*>(dbase + image_rel(ds, e, td))
+                                = *reinterpret_cast<const uint32_t*>(sbase + image_rel(ss, e, ts));
+                    }
+                    else if(ts.size == 8 && ts.aligned && td.aligned)
+                    {
+                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                            *reinterpret_cast<unsigned long long*>(dbase + image_rel(ds, e, td))
+                                = *reinterpret_cast<const unsigned long long*>(sbase + image_rel(ss, e, ts));
+                    }
+                    else
+                    {
+                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                        {
+                            uint64_t v = lds_bytes(sbase + image_rel(ss, e, ts), ts.size, ts.aligned);
+                            if(L.stype == lamd::BOOL)
+                                v = v != 0;
+                            lamd::store_bytes(dbase + image_rel(ds, e, td), td.size, td.aligned, v);
+                        }
+                    }
+                    continue;
+                }
+                for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                {
+                    uint64_t v = tile_read(p, L, sb, e);
+                    v = lamd::convert_value(v, L.stype, L.ltype);
+                    v = lamd::convert_value(v, L.ltype, L.dtype);
+                    tile_write(p, L, db, e, v);
+                }
+            }
+            // ---- pack bit-packed destinations ----
+            bool anyBits = false;
+            for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                anyBits |= p.st[j].kind == 1;
+            if(anyBits)
+            {
+                __syncthreads();
+                for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                    if(p.st[j].kind == 1)
+                        pack_words(p.st[j], db, p.T);
+            }
+            done += p.T;
+            // non-TMA destination images: cooperative stores
+            bool anyCoop = false;
+            for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                anyCoop |= !p.st[j].tma;
+            if(anyCoop)
+            {
+                __syncthreads();
+                for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                {
+                    const lamt_stream& s = p.st[j];
+                    if(!s.tma && s.tile_bytes)
+                        coop_s2g(reinterpret_cast<uint8_t*>(s.gptr) + tile_global_off(s, t0), db + s.smem_off,
+                                 s.tile_bytes);
+                }
+            }
+            fence_async_smem();
+            __syncthreads();
+            if(lead)
+            {
+                for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                {
+                    const lamt_stream& s = p.st[j];
+                    if(s.tma && s.tile_bytes)
+                        bulk_s2g(reinterpret_cast<uint8_t*>(s.gptr) + tile_global_off(s, t0), db + s.smem_off,
+                                 s.tile_bytes);
+                }
+                bulk_commit();
+            }
+        }
+        if(lead)
+            bulk_wait_all();
+        // FieldAccessCount: every element of every leaf of a tile is accessed once; one
+        // global atomic per CTA per field (instrument.cpp:57-72)
+        if((p.facS || p.facD) && done)
+        {
+            for(uint32_t f = threadIdx.x; f < p.nleaves; f += blockDim.x)
+            {
+                if(p.facS)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + f, static_cast<unsigned long long>(done));
+                if(p.facD)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(p.facDst) + p.nleaves + f,
+                              static_cast<unsigned long long>(done));
+            }
+        }
+    }
+
+    cudaError_t tile_copy(const lamt_params& p, uint32_t smemBytes, uint32_t ctasPerSm, cudaStream_t s)
+    {
+        if(p.ntiles == 0)
+            return cudaSuccess;
+        static uint32_t attrSet[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if(dev >= 64 || attrSet[dev] < smemBytes)
+        {
+            cudaError_t e = cudaFuncSetAttribute(k_tile_copy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smemBytes));
+            if(e != cudaSuccess)
+                return e;
+            if(dev < 64)
+                attrSet[dev] = smemBytes;
+        }
+        const uint32_t sms = static_cast<uint32_t>(sm_count(dev));
+        uint32_t grid = sms * ctasPerSm;
+        if(grid > p.ntiles)
+            grid = p.ntiles;
+        k_tile_copy<<<grid, 512, smemBytes, s>>>(p);
+        count_launch();
+        return cudaGetLastError();
+    }
+} // namespace lamk

@@ -95,7 +95,7 @@ namespace lamd
     }
 
     // floatEncode(value, E, M) on the double's bit pattern
-    __device__ __noinline__ uint64_t float_encode(uint64_t bits64, uint32_t E, uint32_t M)
+    static __device__ __noinline__ uint64_t float_encode(uint64_t bits64, uint32_t E, uint32_t M)
     {
         const uint64_t signBit = (bits64 >> 63) << (E + M);
         const uint64_t expMask = low_mask(E);
@@ -149,7 +149,7 @@ namespace lamd
     }
 
     // floatDecode(pattern, E, M) -> double bit pattern
-    __device__ __noinline__ uint64_t float_decode(uint64_t p, uint32_t E, uint32_t M)
+    static __device__ __noinline__ uint64_t float_decode(uint64_t p, uint32_t E, uint32_t M)
     {
         p &= low_mask(1 + E + M);
         const uint64_t sign = (p >> (E + M)) & 1ull;

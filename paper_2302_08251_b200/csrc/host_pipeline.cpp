@@ -278,7 +278,7 @@ namespace lamhost
                                                tab + S.streams.size(), D.streams.size() * sizeof(uint8_t*),
                                                cudaMemcpyHostToDevice, comp_),
                                "ptr table");
-            if(!tileCopyImages(S, simg[s], D, dimg[s], lo, hi, comp_))
+            if(!tileCopyPtrs(S, simg[s], tab, D, dimg[s], tab + S.streams.size(), lo, hi, comp_))
                 lam_cuda_check(lamk::generic_copy(simg[s].hdr, dimg[s].hdr, lo, hi, static_cast<uint32_t>(leaves), S.fac,
                                                   D.fac, comp_),
                                "generic_copy");

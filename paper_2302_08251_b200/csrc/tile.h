@@ -1,0 +1,72 @@
+// Tile engine parameter block (host <-> device).
+//
+// A tile is T consecutive elements (T a multiple of every AoSoA lane count, of 32 and of
+// both layouts' shard units).  Each blob stream of the source and destination occupies
+// one contiguous byte range per tile ("image"), moved between HBM and shared memory with
+// 1-D TMA bulk copies (cp.async.bulk) when 16-byte aligned.  The transform step runs the
+// per-leaf value pipeline (read terminal(s) -> convert -> write terminal(s)) entirely in
+// shared memory; bit-packed destinations are assembled word by word by their owning
+// thread (no read-modify-write anywhere, bitpack.hpp:16-17).
+#pragma once
+
+#include <stdint.h>
+
+#define LAMT_MAX_LEAVES 32
+#define LAMT_MAX_STREAMS 48
+#define LAMT_MAX_TERMS 8
+
+#define LAMT_K_PHYS 0
+#define LAMT_K_SPLIT 1
+#define LAMT_K_BITS_INT 2
+#define LAMT_K_BITS_FLT 3
+#define LAMT_K_NULL 4
+
+struct lamt_stream
+{
+    unsigned long long gptr; // stream pointer (blob + base0; virtual for chunk views)
+    uint32_t smem_off;       // image offset inside a stage buffer
+    uint32_t tile_bytes;     // image bytes per full tile
+    uint32_t bs;             // PHYS: block stride bytes ; BITS: bits per element
+    uint32_t lanes;          // PHYS: L ; BITS: 1
+    uint32_t lshift;         // log2(L) or 0xFFFFFFFF
+    uint32_t kind;           // 0 PHYS, 1 BITS
+    uint32_t tma;            // image start is 16-byte aligned in global memory
+    uint32_t scratch_off;    // BITS destination: per-element pattern scratch (stage-relative)
+    uint32_t scratch64;      // scratch slots are 8 bytes (field width > 32)
+    uint32_t pad;
+};
+
+struct lamt_term
+{
+    uint16_t stream;
+    uint8_t size;
+    uint8_t aligned; // naturally aligned inside the smem image
+    uint32_t inblock;
+    uint32_t ls;
+};
+
+struct lamt_leaf
+{
+    uint8_t skind, stype, ltype, dkind, dtype, sn, dn, pure;
+    uint8_t sE, sM, dE, dM; // BITS_INT: E = bits ; BITS_FLT: (E, M)
+    uint8_t ssigned, pad0, pad1, pad2;
+    lamt_term s[LAMT_MAX_TERMS];
+    lamt_term d[LAMT_MAX_TERMS];
+};
+
+struct lamt_params
+{
+    unsigned long long begin; // first element of tile 0
+    uint32_t T;               // elements per tile
+    uint32_t ntiles;
+    uint32_t nleaves;
+    uint32_t nsrc, ndst; // streams [0, nsrc) source, [nsrc, nsrc+ndst) destination
+    uint32_t src_bytes;  // stage buffer bytes (source images)
+    uint32_t dst_bytes;  // stage buffer bytes (destination images + scratch)
+    uint32_t tma_bytes;  // source bytes delivered by TMA per tile
+    uint32_t facS, facD;
+    unsigned long long facSrc; // device counters (reads) or 0
+    unsigned long long facDst; // device counters (writes) or 0
+    lamt_stream st[LAMT_MAX_STREAMS];
+    lamt_leaf leaf[LAMT_MAX_LEAVES];
+};

@@ -1,0 +1,186 @@
+"""GPU parity: lam_copy (sm_100a kernels, through the C ABI) vs the oracle on the same inputs.
+
+Bit-exact on every blob byte (including bytes the copy must not write: padding,
+AoSoA tail lanes, bit-stream tails) and on FieldAccessCount / Heatmap counters.
+"""
+import numpy as np
+import pytest
+
+from conftest import MIXED, R32, R64, random_values
+from oracle import lamina_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS_R32 = ["aos-packed", "aos-aligned", "soa-sb", "soa-mb", "aosoa:8", "aosoa:32", "aosoa:3",
+               "bytesplit:soa-mb", "bytesplit:aos-packed", "changetype:f32=f64:soa-mb", "split:Pos:soa-mb:aos-packed",
+               "bitpack-float:5,10", "bitpack-float:8,10", "bitpack-float:11,30", "null", "one"]
+LAYOUTS_MIXED = ["aos-packed", "aos-aligned", "soa-sb", "soa-mb", "aosoa:4", "bytesplit:soa-sb",
+                 "changetype:f64=f32,i8=i64,u16=u8:aosoa:2", "split:h:bytesplit:soa-mb:aos-aligned",
+                 "changetype:h.y=f64:bytesplit:aosoa:3"]
+
+
+def lm():
+    from paper_2302_08251_b200 import lamina
+    return lamina
+
+
+def run_pair(schema, n, a, b, vals, src_wrap=0, dst_wrap=0, gran=3, dst_prefill=None):
+    L = lm()
+    ext = f"i32:[{n}]"
+    ms = O.make(schema, ext, a, wrap=src_wrap, gran=gran)
+    md = O.make(schema, ext, b, wrap=dst_wrap, gran=gran)
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    if O._fac_of(ms) is not None:
+        O._fac_of(ms).writes[:] = 0
+    if O._heat_of(ms) is not None:
+        for x in O._heat_of(ms).blocks:
+            x[:] = 0
+    db = O.zero_blobs(md) if dst_prefill is None else [x.copy() for x in dst_prefill]
+    gs = L.View(L.Layout(schema, ext, a, wrap=src_wrap, granularity=gran))
+    gd = L.View(L.Layout(schema, ext, b, wrap=dst_wrap, granularity=gran))
+    gs.upload_all(sb)
+    gd.upload_all(db)
+    O.copy_view(ms, sb, md, db)
+    L.copy_view(gs, gd)
+    got = gd.download_all()
+    for nr, (x, y) in enumerate(zip(got, db)):
+        assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
+    for m, v in ((ms, gs), (md, gd)):
+        fac = O._fac_of(m)
+        if fac is not None:
+            r, w = v.counters()
+            assert np.array_equal(r, fac.reads) and np.array_equal(w, fac.writes)
+        h = O._heat_of(m)
+        if h is not None:
+            for nr, blk in enumerate(h.blocks):
+                assert np.array_equal(v.heatmap(nr), blk), f"heatmap blob {nr}"
+
+
+@pytest.mark.parametrize("n", [1, 37, 1000, 4099])
+@pytest.mark.parametrize("a", LAYOUTS_R32)
+def test_copy_matrix_r32(a, n):
+    rng = np.random.default_rng(n)
+    vals = random_values(rng, [8] * 7, n)
+    for b in LAYOUTS_R32:
+        if "one" in (a, b) and n != 1:
+            continue
+        run_pair(R32, n, a, b, vals)
+
+
+@pytest.mark.parametrize("n", [1, 53, 777])
+@pytest.mark.parametrize("a", LAYOUTS_MIXED)
+def test_copy_matrix_mixed(a, n):
+    rng = np.random.default_rng(100 + n)
+    types = [l.type for l in O.Schema.parse(MIXED).leaves]
+    vals = random_values(rng, types, n)
+    for b in LAYOUTS_MIXED:
+        run_pair(MIXED, n, a, b, vals)
+
+
+@pytest.mark.parametrize("b", [3, 7, 11, 12, 16, 24, 31, 32])
+def test_bitpack_int_roundtrip(b):
+    schema = "Record{v:u32,w:i32}"
+    n = 5003
+    rng = np.random.default_rng(b)
+    vals = random_values(rng, [6, 2], n)
+    run_pair(schema, n, "soa-mb", f"bitpack-int:{b}", vals)
+    run_pair(schema, n, "aos-packed", f"bitpack-int:{b}", vals)
+    # unpack: from a packed view back to physical
+    packed = O.make(schema, f"i32:[{n}]", f"bitpack-int:{b}")
+    pb = O.zero_blobs(packed)
+    O.write_all(packed, pb, vals)
+    back = O.read_all(packed, pb)
+    run_pair(schema, n, f"bitpack-int:{b}", "soa-mb", back)
+
+
+@pytest.mark.parametrize("wrap", [1, 2, 3])
+@pytest.mark.parametrize("gran", [1, 5, 64])
+def test_instrumented_copy(wrap, gran):
+    rng = np.random.default_rng(7)
+    n = 300
+    vals = random_values(rng, [8] * 7, n)
+    for a, b in [("aos-packed", "soa-mb"), ("soa-mb", "aosoa:8"), ("aos-packed", "bytesplit:soa-mb"),
+                 ("aos-packed", "bitpack-float:5,10"), ("aosoa:8", "aosoa:8")]:
+        run_pair(R32, n, a, b, vals, dst_wrap=wrap, gran=gran)
+        run_pair(R32, n, a, b, vals, src_wrap=wrap, gran=gran)
+
+
+def test_c5_layout_r64():
+    """Config 5 shape: aos-packed f64 -> FieldAccessCount(changetype:f64=f32:bytesplit:soa-mb)."""
+    rng = np.random.default_rng(5)
+    n = 10007
+    vals = random_values(rng, [9] * 7, n)
+    run_pair(R64, n, "aos-packed", "changetype:f64=f32:bytesplit:soa-mb", vals, dst_wrap=1)
+    run_pair(R64, n, "aos-packed", "bytesplit:changetype:f64=f32", vals, dst_wrap=1)
+
+
+def test_untouched_bytes_survive():
+    """Bytes copyView never writes keep their prior content (padding, tails)."""
+    rng = np.random.default_rng(9)
+    n = 13
+    vals = random_values(rng, [l.type for l in O.Schema.parse(MIXED).leaves], n)
+    for b in ["aos-aligned", "aosoa:4", "bitpack-int:3"]:
+        schema = MIXED if b != "bitpack-int:3" else "Record{v:u32}"
+        v = vals if b != "bitpack-int:3" else random_values(rng, [6], n)
+        md = O.make(schema, f"i32:[{n}]", b)
+        prefill = [rng.integers(0, 256, s, dtype=np.uint8) for s in md.blob_sizes()]
+        run_pair(schema, n, "soa-mb", b, v, dst_prefill=prefill)
+
+
+def test_errors_match_reference():
+    L = lm()
+    a = L.View(L.Layout(R32, "i32:[4]", "aos-packed"))
+    b = L.View(L.Layout(R32, "i32:[5]", "aos-packed"))
+    with pytest.raises(L.InvalidArgument, match="incompatible views"):
+        L.copy_view(a, b)
+    c = L.View(L.Layout("Record{x:f64}", "i32:[4]", "aos-packed"))
+    with pytest.raises(L.InvalidArgument):
+        L.copy_view(a, c)
+
+
+@pytest.mark.parametrize("a,b", [("aos-packed", "soa-mb"), ("soa-mb", "aosoa:32"), ("aosoa:8", "bytesplit:soa-mb"),
+                                 ("soa-mb", "bitpack-float:8,10"), ("aos-aligned", "soa-sb")])
+def test_copy_host_pipeline(a, b):
+    """lam_copy_host: host blobs in, host blobs out, chunked through the GPU."""
+    L = lm()
+    rng = np.random.default_rng(11)
+    n = 3_000_001
+    ext = f"i32:[{n}]"
+    vals = random_values(rng, [8] * 7, n)
+    ms, md = O.make(R32, ext, a), O.make(R32, ext, b, wrap=1)
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    db = O.zero_blobs(md)
+    O.copy_view(ms, sb, md, db)
+    got = [np.zeros_like(x) for x in db]
+    _, dc = L.copy_view_host(L.Layout(R32, ext, a), sb, L.Layout(R32, ext, b, wrap=1), got)
+    for nr, (x, y) in enumerate(zip(got, db)):
+        assert np.array_equal(x, y), f"blob {nr}"
+    assert np.array_equal(dc, O.counters(md))
+
+
+def test_copy_range_shards_concatenate():
+    """Sharded copies over disjoint ranges == one whole copy (multi-GPU decomposition)."""
+    L = lm()
+    rng = np.random.default_rng(12)
+    n = 100_003
+    ext = f"i32:[{n}]"
+    vals = random_values(rng, [8] * 7, n)
+    for a, b in [("aos-packed", "aosoa:32"), ("soa-mb", "bitpack-float:5,10"), ("aosoa:8", "soa-sb")]:
+        ms, md = O.make(R32, ext, a), O.make(R32, ext, b)
+        sb = O.zero_blobs(ms)
+        O.write_all(ms, sb, vals)
+        db = O.zero_blobs(md)
+        O.copy_view(ms, sb, md, db)
+        ls, ld = L.Layout(R32, ext, a), L.Layout(R32, ext, b)
+        gs, gd = L.View(ls), L.View(ld)
+        gs.upload_all(sb)
+        unit = np.lcm(ls.shard_unit, ld.shard_unit)
+        cuts = [0] + [int(k * n // 4 // unit * unit) for k in range(1, 4)] + [n]
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            L.copy_view_range(gs, gd, lo, hi)
+        for x, y in zip(gd.download_all(), db):
+            assert np.array_equal(x, y)
+        with pytest.raises(L.InvalidArgument):
+            L.copy_view_range(gs, gd, 1, n)
