@@ -1,0 +1,140 @@
+// Header-only C++ host mirror of the reference's hot-path API over the C ABI
+// (include/lamina_b200.h).  Same names, argument meaning and exception types as
+// lamina (/root/reference/proj/core/include/lamina/{layout_spec,view,instrument}.hpp),
+// so reference-style host code switches by changing the namespace:
+//
+//   auto m = lamina_b200::parseLayout("aosoa:32", schemaText, "i32:[1048576]");
+//   lamina_b200::View src(lamina_b200::parseLayout("aos-packed", schemaText, "i32:[1048576]"));
+//   lamina_b200::View dst(m);
+//   lamina_b200::copyView(src, dst);          // sm_100a kernels, stream-ordered
+//
+// Errors are rethrown as std::invalid_argument / std::out_of_range / std::overflow_error /
+// std::logic_error with the reference's messages; CUDA failures as std::runtime_error.
+#pragma once
+
+#include "lamina_b200.h"
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace lamina_b200
+{
+    inline void check(int rc)
+    {
+        if(rc == LAM_OK)
+            return;
+        const std::string msg = lam_last_error();
+        switch(rc)
+        {
+        case LAM_EINVAL:
+            throw std::invalid_argument(msg);
+        case LAM_ERANGE:
+            throw std::out_of_range(msg);
+        case LAM_EOVERFLOW:
+            throw std::overflow_error(msg);
+        case LAM_ELOGIC:
+            throw std::logic_error(msg);
+        default:
+            throw std::runtime_error(msg);
+        }
+    }
+
+    /// lamina::MappingPtr equivalent: a lowered mapping (schema + extents + layout).
+    class Mapping
+    {
+    public:
+        Mapping(const std::string& schema, const std::string& extents, const std::string& layout,
+                const std::vector<std::uint64_t>& dyn = {}, int wrap = 0, std::uint64_t granularity = 0)
+        {
+            lam_layout* h = nullptr;
+            check(lam_layout_create(schema.c_str(), extents.c_str(), dyn.data(), dyn.size(), layout.c_str(), wrap,
+                                    granularity, &h));
+            h_.reset(h, lam_layout_destroy);
+        }
+
+        std::string name() const
+        {
+            std::string s(lam_layout_name(h_.get(), nullptr, 0), '\0');
+            lam_layout_name(h_.get(), s.data(), s.size() + 1);
+            return s;
+        }
+        std::size_t blobCount() const
+        {
+            return lam_layout_blob_count(h_.get());
+        }
+        std::uint64_t blobSize(std::size_t nr) const
+        {
+            return lam_layout_blob_size(h_.get(), nr);
+        }
+        std::uint64_t elementCount() const
+        {
+            return lam_layout_element_count(h_.get());
+        }
+        const lam_layout* handle() const
+        {
+            return h_.get();
+        }
+
+    private:
+        std::shared_ptr<lam_layout> h_;
+    };
+
+    using MappingPtr = std::shared_ptr<const Mapping>;
+
+    /// lamina::parseLayout(text, schema, extents) (layout_spec.hpp:19), schema/extents as text.
+    inline MappingPtr parseLayout(const std::string& text, const std::string& schema, const std::string& extents,
+                                  const std::vector<std::uint64_t>& dyn = {})
+    {
+        return std::make_shared<const Mapping>(schema, extents, text, dyn);
+    }
+
+    /// lamina::View on a device: zero-filled blobs in HBM (or adopted device pointers).
+    class View
+    {
+    public:
+        explicit View(MappingPtr m, int device = 0, void* stream = nullptr) : m_(std::move(m))
+        {
+            lam_view* v = nullptr;
+            check(lam_view_alloc(m_->handle(), device, stream, &v));
+            v_.reset(v, lam_view_free);
+        }
+        View(MappingPtr m, const std::vector<void*>& deviceBlobs, int device = 0) : m_(std::move(m))
+        {
+            lam_view* v = nullptr;
+            check(lam_view_wrap(m_->handle(), device, deviceBlobs.data(), nullptr, deviceBlobs.size(), &v));
+            v_.reset(v, lam_view_free);
+        }
+        const Mapping& mapping() const
+        {
+            return *m_;
+        }
+        void* blob(std::size_t nr) const
+        {
+            return lam_view_blob(v_.get(), nr);
+        }
+        lam_view* handle() const
+        {
+            return v_.get();
+        }
+
+    private:
+        MappingPtr m_;
+        std::shared_ptr<lam_view> v_;
+    };
+
+    /// lamina::copyView(const View&, View&) (view.hpp:285) on the GPU, stream-ordered.
+    inline void copyView(const View& src, View& dst, void* stream = nullptr)
+    {
+        check(lam_copy(src.handle(), dst.handle(), stream));
+    }
+
+    /// copyView over host blobs (dst blobs in/out), streamed through the GPU.
+    inline void copyViewHost(const Mapping& src, const std::vector<const void*>& srcBlobs, const Mapping& dst,
+                             const std::vector<void*>& dstBlobs, int device = 0)
+    {
+        check(lam_copy_host(src.handle(), srcBlobs.data(), dst.handle(), dstBlobs.data(), device, nullptr, nullptr));
+    }
+} // namespace lamina_b200

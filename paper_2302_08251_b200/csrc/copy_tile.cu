@@ -118,7 +118,19 @@ namespace lamk
             return lamd::load_bytes(p, size, aligned);
         }
 
-        // cooperative copy for images whose global start is not 16-byte aligned
+        __device__ __forceinline__ void bulk_wait_read_dyn(uint32_t n)
+        {
+            if(n == 0)
+                bulk_wait_read<0>();
+            else if(n == 1)
+                bulk_wait_read<1>();
+            else if(n == 2)
+                bulk_wait_read<2>();
+            else
+                bulk_wait_read<3>();
+        }
+
+        // CTA-cooperative copy for images whose global start is not 16-byte aligned
         __device__ void coop_g2s(uint8_t* smem, const uint8_t* g, uint32_t bytes)
         {
             const uintptr_t a = reinterpret_cast<uintptr_t>(g);
@@ -269,7 +281,8 @@ namespace lamk
         }
 
         // whole-word assembly of a bit-packed destination image from its pattern scratch
-        __device__ __forceinline__ void pack_words(const lamt_stream& s, uint8_t* dbuf, uint32_t T)
+        __device__ __forceinline__ void pack_words(const lamt_stream& s, uint8_t* dbuf, uint32_t T, uint32_t lane,
+                                                   uint32_t nthreads)
         {
             const uint32_t w = s.bs;
             const uint32_t words = T * w / 32;
@@ -277,7 +290,7 @@ namespace lamk
             if(!s.scratch64)
             {
                 const uint32_t* sc = reinterpret_cast<const uint32_t*>(dbuf + s.scratch_off);
-                for(uint32_t q = threadIdx.x; q < words; q += blockDim.x)
+                for(uint32_t q = lane; q < words; q += nthreads)
                 {
                     const uint32_t bit = q * 32;
                     uint32_t k = bit / w;
@@ -297,7 +310,7 @@ namespace lamk
             else
             {
                 const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(dbuf + s.scratch_off);
-                for(uint32_t q = threadIdx.x; q < words; q += blockDim.x)
+                for(uint32_t q = lane; q < words; q += nthreads)
                 {
                     const uint64_t bit = uint64_t(q) * 32;
                     uint64_t k = bit / w;
@@ -312,151 +325,168 @@ namespace lamk
         }
     } // namespace
 
-    __global__ void __launch_bounds__(512, 2) k_tile_copy(const __grid_constant__ lamt_params p)
+    // CTA-wide pipeline: `stages` source stage buffers (TMA bulk loads in flight ahead of the
+    // transform) and `dstages` destination buffers (TMA bulk stores draining behind it).
+    // One __syncthreads per tile: after it, thread 0 issues the tile's stores, refills the
+    // freed source stage and retires the store that last used the next destination buffer.
+    __device__ __forceinline__ uint32_t uni_off(uint32_t e, uint32_t L, uint32_t sh, uint32_t bs, uint32_t ls)
+    {
+        if(L == 1)
+            return e * bs;
+        if(sh != 0xFFFFFFFFu)
+            return (e >> sh) * bs + (e & (L - 1)) * ls;
+        return (e / L) * bs + (e % L) * ls;
+    }
+
+    __global__ void __launch_bounds__(512, 1) k_tile_copy(const __grid_constant__ lamt_params p)
     {
         extern __shared__ __align__(128) uint8_t smem[];
-        __shared__ __align__(8) uint64_t mbar[2];
-        uint8_t* sbuf[2] = {smem, smem + p.src_bytes};
-        uint8_t* dbuf[2] = {smem + 2 * p.src_bytes, smem + 2 * p.src_bytes + p.dst_bytes};
+        __shared__ __align__(8) uint64_t mbar[LAMT_MAX_STAGES];
         const bool lead = threadIdx.x == 0;
+        uint8_t* srcBase = smem;
+        uint8_t* dstBase = smem + p.stages * p.src_bytes;
         if(lead)
         {
-            mbar_init(&mbar[0], 1);
-            mbar_init(&mbar[1], 1);
+            for(uint32_t s = 0; s < p.stages; ++s)
+                mbar_init(&mbar[s], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
 
-        auto issue_load = [&](uint32_t tile, int stage)
+        auto issue_load = [&](uint32_t tile, uint32_t s)
         {
             const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+            uint8_t* sb = srcBase + s * p.src_bytes;
             if(p.tma_bytes)
-                mbar_expect_tx(&mbar[stage], p.tma_bytes);
+                mbar_expect_tx(&mbar[s], p.tma_bytes);
             else
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[stage])) : "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[s])) : "memory");
             for(uint32_t k = 0; k < p.nsrc; ++k)
             {
-                const lamt_stream& s = p.st[k];
-                if(s.tma && s.tile_bytes)
-                    bulk_g2s(sbuf[stage] + s.smem_off,
-                             reinterpret_cast<const uint8_t*>(s.gptr) + tile_global_off(s, t0), s.tile_bytes,
-                             &mbar[stage]);
+                const lamt_stream& st = p.st[k];
+                if(st.tma && st.tile_bytes)
+                    bulk_g2s(sb + st.smem_off, reinterpret_cast<const uint8_t*>(st.gptr) + tile_global_off(st, t0),
+                             st.tile_bytes, &mbar[s]);
             }
         };
 
-        const uint32_t first = blockIdx.x;
-        if(lead && first < p.ntiles)
-            issue_load(first, 0);
+        if(lead)
+            for(uint32_t s = 0; s < p.stages; ++s)
+                if(blockIdx.x + s * gridDim.x < p.ntiles)
+                    issue_load(blockIdx.x + s * gridDim.x, s);
+
+        uint32_t os[LAMT_UNI_LEAVES], od[LAMT_UNI_LEAVES];
+#pragma unroll
+        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+        {
+            os[f] = p.uoff_s[f];
+            od[f] = p.uoff_d[f];
+        }
+
         uint32_t done = 0;
         for(uint32_t k = 0;; ++k)
         {
-            const uint32_t tile = first + k * gridDim.x;
+            const uint32_t tile = blockIdx.x + k * gridDim.x;
             if(tile >= p.ntiles)
                 break;
-            const int st = k & 1;
-            const uint32_t next = tile + gridDim.x;
-            if(lead && next < p.ntiles)
-                issue_load(next, st ^ 1);
+            const uint32_t s = k % p.stages;
+            const uint32_t d = k % p.dstages;
+            uint8_t* sb = srcBase + s * p.src_bytes;
+            uint8_t* db = dstBase + d * p.dst_bytes;
             const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
-            // non-TMA source images: cooperative loads
-            for(uint32_t j = 0; j < p.nsrc; ++j)
+            if(p.any_coop)
             {
-                const lamt_stream& s = p.st[j];
-                if(!s.tma && s.tile_bytes)
-                    coop_g2s(sbuf[st] + s.smem_off, reinterpret_cast<const uint8_t*>(s.gptr) + tile_global_off(s, t0),
-                             s.tile_bytes);
+                for(uint32_t j = 0; j < p.nsrc; ++j)
+                {
+                    const lamt_stream& st = p.st[j];
+                    if(!st.tma && st.tile_bytes)
+                        coop_g2s(sb + st.smem_off, reinterpret_cast<const uint8_t*>(st.gptr) + tile_global_off(st, t0),
+                                 st.tile_bytes);
+                }
+                __syncthreads();
             }
-            mbar_wait(&mbar[st], (k >> 1) & 1);
-            if(lead)
-                bulk_wait_read<1>(); // stores of tile k-2 have left dbuf[st]
-            __syncthreads();
+            mbar_wait(&mbar[s], (k / p.stages) & 1);
 
             // ---- transform ----
-            const uint8_t* sb = sbuf[st];
-            uint8_t* db = dbuf[st];
-            for(uint32_t f = 0; f < p.nleaves; ++f)
+            if(p.uni)
             {
-                const lamt_leaf& L = p.leaf[f];
-                if(L.pure)
+                const uint32_t nl = p.nleaves;
+                for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
                 {
-                    // PHYS -> PHYS, same scalar: a byte permutation (Bool still canonicalises)
-                    const lamt_term& ts = L.s[0];
-                    const lamt_term& td = L.d[0];
-                    const lamt_stream& ss = p.st[ts.stream];
-                    const lamt_stream& ds = p.st[td.stream];
-                    const uint8_t* sbase = sb + ss.smem_off;
-                    uint8_t* dbase = db + ds.smem_off;
-                    if(ts.size == 4 && ts.aligned && td.aligned)
+                    const uint32_t es = uni_off(e, p.ul_s, p.ush_s, p.ubs_s, p.uls_s);
+                    const uint32_t ed = uni_off(e, p.ul_d, p.ush_d, p.ubs_d, p.uls_d);
+                    if(p.usize == 4)
                     {
-                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
-                            *reinterpret_cast<uint32_t*>(dbase + image_rel(ds, e, td))
-                                = *reinterpret_cast<const uint32_t*>(sbase + image_rel(ss, e, ts));
-                    }
-                    else if(ts.size == 8 && ts.aligned && td.aligned)
-                    {
-                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
-                            *reinterpret_cast<unsigned long long*>(dbase + image_rel(ds, e, td))
-                                = *reinterpret_cast<const unsigned long long*>(sbase + image_rel(ss, e, ts));
+                        uint32_t v[LAMT_UNI_LEAVES];
+#pragma unroll
+                        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                            if(f < nl)
+                                v[f] = *reinterpret_cast<const uint32_t*>(sb + os[f] + es);
+#pragma unroll
+                        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                            if(f < nl)
+                                *reinterpret_cast<uint32_t*>(db + od[f] + ed) = v[f];
                     }
                     else
                     {
-                        for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
-                        {
-                            uint64_t v = lds_bytes(sbase + image_rel(ss, e, ts), ts.size, ts.aligned);
-                            if(L.stype == lamd::BOOL)
-                                v = v != 0;
-                            lamd::store_bytes(dbase + image_rel(ds, e, td), td.size, td.aligned, v);
-                        }
+#pragma unroll
+                        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                            if(f < nl)
+                                *reinterpret_cast<unsigned long long*>(db + od[f] + ed)
+                                    = *reinterpret_cast<const unsigned long long*>(sb + os[f] + es);
                     }
-                    continue;
-                }
-                for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
-                {
-                    uint64_t v = tile_read(p, L, sb, e);
-                    v = lamd::convert_value(v, L.stype, L.ltype);
-                    v = lamd::convert_value(v, L.ltype, L.dtype);
-                    tile_write(p, L, db, e, v);
                 }
             }
-            // ---- pack bit-packed destinations ----
-            bool anyBits = false;
-            for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
-                anyBits |= p.st[j].kind == 1;
-            if(anyBits)
+            else
             {
-                __syncthreads();
-                for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
-                    if(p.st[j].kind == 1)
-                        pack_words(p.st[j], db, p.T);
+                for(uint32_t f = 0; f < p.nleaves; ++f)
+                {
+                    const lamt_leaf& L = p.leaf[f];
+                    for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                    {
+                        uint64_t v = tile_read(p, L, sb, e);
+                        v = lamd::convert_value(v, L.stype, L.ltype);
+                        v = lamd::convert_value(v, L.ltype, L.dtype);
+                        tile_write(p, L, db, e, v);
+                    }
+                }
+                if(p.any_bits)
+                {
+                    __syncthreads();
+                    for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
+                        if(p.st[j].kind == 1)
+                            pack_words(p.st[j], db, p.T, threadIdx.x, blockDim.x);
+                }
             }
             done += p.T;
-            // non-TMA destination images: cooperative stores
-            bool anyCoop = false;
-            for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
-                anyCoop |= !p.st[j].tma;
-            if(anyCoop)
+            if(p.any_coop)
             {
                 __syncthreads();
                 for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
                 {
-                    const lamt_stream& s = p.st[j];
-                    if(!s.tma && s.tile_bytes)
-                        coop_s2g(reinterpret_cast<uint8_t*>(s.gptr) + tile_global_off(s, t0), db + s.smem_off,
-                                 s.tile_bytes);
+                    const lamt_stream& st = p.st[j];
+                    if(!st.tma && st.tile_bytes)
+                        coop_s2g(reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0), db + st.smem_off,
+                                 st.tile_bytes);
                 }
             }
             fence_async_smem();
+            if(lead)
+                bulk_wait_read_dyn(p.dstages - 2); // the store that used the NEXT dst buffer has left smem
             __syncthreads();
             if(lead)
             {
                 for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
                 {
-                    const lamt_stream& s = p.st[j];
-                    if(s.tma && s.tile_bytes)
-                        bulk_s2g(reinterpret_cast<uint8_t*>(s.gptr) + tile_global_off(s, t0), db + s.smem_off,
-                                 s.tile_bytes);
+                    const lamt_stream& st = p.st[j];
+                    if(st.tma && st.tile_bytes)
+                        bulk_s2g(reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0), db + st.smem_off,
+                                 st.tile_bytes);
                 }
                 bulk_commit();
+                const uint32_t next = tile + p.stages * gridDim.x;
+                if(next < p.ntiles)
+                    issue_load(next, s);
             }
         }
         if(lead)
@@ -493,10 +523,10 @@ namespace lamk
                 attrSet[dev] = smemBytes;
         }
         const uint32_t sms = static_cast<uint32_t>(sm_count(dev));
-        uint32_t grid = sms * ctasPerSm;
+        uint64_t grid = static_cast<uint64_t>(sms) * ctasPerSm;
         if(grid > p.ntiles)
             grid = p.ntiles;
-        k_tile_copy<<<grid, 512, smemBytes, s>>>(p);
+        k_tile_copy<<<static_cast<unsigned>(grid), p.threads, smemBytes, s>>>(p);
         count_launch();
         return cudaGetLastError();
     }

@@ -5,6 +5,7 @@
 #include "capi_internal.hpp"
 #include "tile.h"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace lamk
@@ -31,6 +32,15 @@ namespace lamhost
         uint64_t lcm64(uint64_t a, uint64_t b)
         {
             return a / gcd64(a, b) * b;
+        }
+
+        // tuning knobs (defaults chosen from the B200 sweep in profiles/)
+        double envNum(const char* name, double dflt)
+        {
+            const char* v = std::getenv(name);
+            if(!v || !*v)
+                return dflt;
+            return std::atof(v);
         }
 
         struct Side
@@ -185,14 +195,18 @@ namespace lamhost
                 if(D.streams[k].kind == LAMS_BITS)
                     bpe += D.streams[k].block_stride > 32 ? 8 : 4;
             }
-            const double stageTarget = 48.0 * 1024;
-            if(unit > (1u << 20) || bpe * unit > 100.0 * 1024)
+            // CTA pipeline: `stages` source buffers + `dstages` destination buffers of one tile each
+            const double stageTarget = envNum("LAMB_TILE_KB", 24.0) * 1024; // src+dst bytes of one tile
+            const uint32_t stages = static_cast<uint32_t>(envNum("LAMB_TILE_STAGES", 3));
+            const uint32_t dstages = static_cast<uint32_t>(envNum("LAMB_TILE_DSTAGES", 2));
+            if(unit > (1u << 16) || bpe * unit > 100.0 * 1024 || stages < 1 || stages > LAMT_MAX_STAGES
+               || dstages < 2 || dstages > 5)
                 return pl;
             uint64_t T = static_cast<uint64_t>(stageTarget / (bpe > 0 ? bpe : 1) / unit) * unit;
             if(T < unit)
                 T = unit;
-            if(T > (1u << 20))
-                T = (1u << 20) / unit * unit;
+            if(T > (1u << 16))
+                T = (1u << 16) / unit * unit;
 
             lamt_params& p = pl.p;
             p.T = static_cast<uint32_t>(T);
@@ -236,10 +250,53 @@ namespace lamhost
             std::memcpy(p.leaf, leaves.data(), nleaves * sizeof(lamt_leaf));
             p.facS = S.fac;
             p.facD = D.fac;
-            pl.smem = 2 * (p.src_bytes + p.dst_bytes);
-            if(pl.smem > 220 * 1024)
+            p.stages = stages;
+            p.dstages = dstages;
+            p.any_bits = 0;
+            for(int k = 0; k < ndst; ++k)
+                p.any_bits |= p.st[nsrc + k].kind == 1;
+            p.threads = static_cast<uint32_t>(envNum("LAMB_TILE_THREADS", 256));
+            pl.smem = stages * p.src_bytes + dstages * p.dst_bytes;
+            const uint32_t smBudget = 226 * 1024;
+            if(pl.smem > smBudget)
                 return pl;
-            pl.ctas = pl.smem <= 110 * 1024 ? 2 : 1;
+            pl.ctas = std::max<uint32_t>(1, std::min<uint32_t>(static_cast<uint32_t>(envNum("LAMB_TILE_CTAS", 4)),
+                                                               smBudget / (pl.smem + 1024)));
+
+            // uniform fast path: all leaves same-size aligned physical moves, one geometry per side
+            bool uni = nleaves <= LAMT_UNI_LEAVES;
+            const lamt_leaf& L0 = leaves[0];
+            for(size_t f = 0; uni && f < nleaves; ++f)
+            {
+                const lamt_leaf& L = leaves[f];
+                uni = L.pure && L.stype != Bool && (L.s[0].size == 4 || L.s[0].size == 8) && L.s[0].size == L0.s[0].size
+                    && L.s[0].aligned && L.d[0].aligned;
+                if(!uni)
+                    break;
+                const lamt_stream &a0 = p.st[L0.s[0].stream], &a = p.st[L.s[0].stream];
+                const lamt_stream &b0 = p.st[L0.d[0].stream], &b = p.st[L.d[0].stream];
+                uni = a.bs == a0.bs && a.lanes == a0.lanes && L.s[0].ls == L0.s[0].ls && b.bs == b0.bs
+                    && b.lanes == b0.lanes && L.d[0].ls == L0.d[0].ls;
+            }
+            if(uni)
+            {
+                p.uni = 1;
+                p.usize = L0.s[0].size;
+                const lamt_stream &a = p.st[L0.s[0].stream], &b = p.st[L0.d[0].stream];
+                p.ubs_s = a.bs;
+                p.ul_s = a.lanes;
+                p.ush_s = a.lshift;
+                p.uls_s = L0.s[0].ls;
+                p.ubs_d = b.bs;
+                p.ul_d = b.lanes;
+                p.ush_d = b.lshift;
+                p.uls_d = L0.d[0].ls;
+                for(size_t f = 0; f < nleaves; ++f)
+                {
+                    p.uoff_s[f] = p.st[leaves[f].s[0].stream].smem_off + leaves[f].s[0].inblock;
+                    p.uoff_d[f] = p.st[leaves[f].d[0].stream].smem_off + leaves[f].d[0].inblock;
+                }
+            }
             pl.ok = true;
             return pl;
         }
@@ -279,6 +336,9 @@ namespace lamhost
                 tma += t.tile_bytes;
         }
         p.tma_bytes = tma;
+        p.any_coop = 0;
+        for(uint32_t k = 0; k < p.nsrc + p.ndst; ++k)
+            p.any_coop |= p.st[k].tile_bytes && !p.st[k].tma;
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
         lam_cuda_check(lamk::tile_copy(p, pl.smem, pl.ctas, s), "tile_copy");

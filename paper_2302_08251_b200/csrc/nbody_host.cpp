@@ -1,0 +1,204 @@
+// n-body C ABI (tools/nbody/runner.cpp + steps.hpp on device views).
+#include "capi_internal.hpp"
+
+#include <cstring>
+#include <random>
+
+namespace lamk
+{
+    cudaError_t nbody_update(const lamp_view* v, bool f64, bool exact, uint64_t n, uint64_t ib, uint64_t ie,
+                             cudaStream_t s);
+    cudaError_t nbody_move(const lamp_view* v, bool f64, uint64_t ib, uint64_t ie, cudaStream_t s);
+} // namespace lamk
+
+using namespace lamb;
+using namespace lamhost;
+
+namespace
+{
+    // the particle record: 7 leaves Pos.{x,y,z}, Vel.{x,y,z}, Mass of one float type
+    // (runner.cpp:328-331, accessors.hpp:13-20)
+    bool particleF64(const lam_view* v)
+    {
+        const auto& s = v->L->map->schema();
+        if(s.leafCount() != 7)
+            throw std::invalid_argument("n-body needs the 7-leaf particle record Pos{x,y,z}, Vel{x,y,z}, Mass");
+        const int t = s.leaves()[0].type;
+        if(t != F32 && t != F64)
+            throw std::invalid_argument("n-body leaves must be f32 or f64");
+        for(size_t f = 1; f < 7; ++f)
+            if(s.leaves()[f].type != t)
+                throw std::invalid_argument("type mismatch: n-body leaves must share one float type");
+        if(v->L->fac || v->L->heat)
+            throw std::invalid_argument("instrumented n-body views are not supported on the device path");
+        return t == F64;
+    }
+
+    struct TempView
+    {
+        std::shared_ptr<Lowered> L;
+        lam_view v;
+        void* buf = nullptr;
+        TempView(const lam_view& like, int device)
+        {
+            const Map& m = *like.L->map;
+            Factory aos = [](Schema s, Extents e) -> MapPtr { return std::make_shared<AoSMap>(s, e, false); };
+            L = lower(aos(m.schema(), m.extents()));
+            v.L = L;
+            v.device = device;
+            v.owned = false;
+            const uint64_t bytes = L->map->blobSize(0);
+            lam_cuda_check(cudaMalloc(&buf, bytes ? bytes : 16), "cudaMalloc(temp view)");
+            v.blobs = {buf};
+            v.img.build(*L, device, streamPtrsFor(*L, v.blobs));
+        }
+        ~TempView()
+        {
+            v.img.release();
+            if(buf)
+                cudaFree(buf);
+        }
+    };
+
+    template<typename F>
+    int guard2(F&& f)
+    {
+        try
+        {
+            f();
+            return LAM_OK;
+        }
+        catch(const std::invalid_argument& e)
+        {
+            g_lam_err = e.what();
+            return LAM_EINVAL;
+        }
+        catch(const std::out_of_range& e)
+        {
+            g_lam_err = e.what();
+            return LAM_ERANGE;
+        }
+        catch(const std::logic_error& e)
+        {
+            g_lam_err = e.what();
+            return LAM_ELOGIC;
+        }
+        catch(const std::exception& e)
+        {
+            g_lam_err = e.what();
+            return std::string(e.what()).find("cuda") != std::string::npos ? LAM_ECUDA : LAM_ERUNTIME;
+        }
+    }
+} // namespace
+
+extern "C"
+{
+    int lam_nbody_init(lam_view* v, uint64_t seed, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                DeviceGuard g(v->device);
+                const uint64_t n = v->L->map->elementCount();
+                auto s = static_cast<cudaStream_t>(stream);
+                // drawInitValues (runner.cpp:30-43) then initView (runner.cpp:46-58)
+                std::mt19937_64 gen(seed);
+                const size_t T = f64 ? 8 : 4;
+                std::vector<uint8_t> host(n * 7 * T);
+                for(uint64_t i = 0; i < n; ++i)
+                {
+                    double d[7];
+                    d[0] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[1] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[2] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[6] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[3] = d[4] = d[5] = 0.0;
+                    for(int f = 0; f < 7; ++f)
+                    {
+                        if(f64)
+                            std::memcpy(&host[(i * 7 + f) * 8], &d[f], 8);
+                        else
+                        {
+                            const float x = static_cast<float>(d[f]);
+                            std::memcpy(&host[(i * 7 + f) * 4], &x, 4);
+                        }
+                    }
+                }
+                TempView tmp(*v, v->device);
+                if(!host.empty())
+                    lam_cuda_check(cudaMemcpyAsync(tmp.buf, host.data(), host.size(), cudaMemcpyHostToDevice, s),
+                                   "h2d");
+                copyViews(tmp.v, *v, 0, n, s);
+                lam_cuda_check(cudaStreamSynchronize(s), "sync");
+            });
+    }
+
+    int lam_nbody_update(lam_view* v, int mode, uint64_t ib, uint64_t ie, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                const uint64_t n = v->L->map->elementCount();
+                if(ib > ie || ie > n)
+                    throw std::out_of_range("index out of range: particles [" + std::to_string(ib) + ", "
+                                            + std::to_string(ie) + ")");
+                DeviceGuard g(v->device);
+                lam_cuda_check(lamk::nbody_update(v->img.hdr, f64, mode == LAM_NBODY_EXACT, n, ib, ie,
+                                                  static_cast<cudaStream_t>(stream)),
+                               "nbody_update");
+            });
+    }
+
+    int lam_nbody_move(lam_view* v, uint64_t ib, uint64_t ie, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                const uint64_t n = v->L->map->elementCount();
+                if(ib > ie || ie > n)
+                    throw std::out_of_range("index out of range: particles");
+                DeviceGuard g(v->device);
+                lam_cuda_check(lamk::nbody_move(v->img.hdr, f64, ib, ie, static_cast<cudaStream_t>(stream)),
+                               "nbody_move");
+            });
+    }
+
+    int lam_nbody_checksum(const lam_view* v, double* out)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                DeviceGuard g(v->device);
+                const uint64_t n = v->L->map->elementCount();
+                TempView tmp(*v, v->device);
+                copyViews(*v, tmp.v, 0, n, nullptr);
+                const size_t T = f64 ? 8 : 4;
+                std::vector<uint8_t> host(n * 7 * T);
+                if(!host.empty())
+                    lam_cuda_check(cudaMemcpy(host.data(), tmp.buf, host.size(), cudaMemcpyDeviceToHost), "d2h");
+                // checksumView (runner.cpp:62-72): Σ x, y, z in double, index order
+                double sum = 0;
+                for(uint64_t i = 0; i < n; ++i)
+                    for(int f = 0; f < 3; ++f)
+                    {
+                        if(f64)
+                        {
+                            double d;
+                            std::memcpy(&d, &host[(i * 7 + f) * 8], 8);
+                            sum += d;
+                        }
+                        else
+                        {
+                            float x;
+                            std::memcpy(&x, &host[(i * 7 + f) * 4], 4);
+                            sum += static_cast<double>(x);
+                        }
+                    }
+                *out = sum;
+            });
+    }
+}

@@ -54,19 +54,33 @@ struct lamt_leaf
     lamt_term d[LAMT_MAX_TERMS];
 };
 
+#define LAMT_MAX_WARPS 32
+#define LAMT_MAX_STAGES 4
+#define LAMT_UNI_LEAVES 16
+
 struct lamt_params
 {
     unsigned long long begin; // first element of tile 0
-    uint32_t T;               // elements per tile
+    uint32_t T;               // elements per tile (one warp owns one tile at a time)
     uint32_t ntiles;
     uint32_t nleaves;
     uint32_t nsrc, ndst; // streams [0, nsrc) source, [nsrc, nsrc+ndst) destination
-    uint32_t src_bytes;  // stage buffer bytes (source images)
-    uint32_t dst_bytes;  // stage buffer bytes (destination images + scratch)
+    uint32_t src_bytes;  // stage bytes (source images)
+    uint32_t dst_bytes;  // stage bytes (destination images + scratch)
     uint32_t tma_bytes;  // source bytes delivered by TMA per tile
+    uint32_t stages;     // source stage buffers (loads in flight ahead of the transform)
+    uint32_t dstages;    // destination buffers (stores draining behind it), >= 2
+    uint32_t threads;    // threads per CTA
+    uint32_t any_bits;   // some destination stream is bit-packed
+    uint32_t any_coop;   // some stream is not TMA-able
     uint32_t facS, facD;
     unsigned long long facSrc; // device counters (reads) or 0
     unsigned long long facDst; // device counters (writes) or 0
+    // uniform fast path: every leaf a same-size physical move, one block geometry per side
+    uint32_t uni, usize;
+    uint32_t ubs_s, ul_s, ush_s, uls_s;
+    uint32_t ubs_d, ul_d, ush_d, uls_d;
+    uint32_t uoff_s[LAMT_UNI_LEAVES], uoff_d[LAMT_UNI_LEAVES];
     lamt_stream st[LAMT_MAX_STREAMS];
     lamt_leaf leaf[LAMT_MAX_LEAVES];
 };

@@ -1,0 +1,86 @@
+"""GPU parity for the n-body kernels (tools/nbody) over every mapping.
+
+EXACT mode must be bit-identical to the reference (same positions, same checksum text);
+FAST mode (FMA + rsqrt, reassociated) must stay within a stated tolerance:
+    |pos_fast - pos_ref| <= 2e-6 * max(1, |pos_ref|)   after 5 steps at n <= 4096.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import lamina_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = ["aos-packed", "aos-aligned", "soa-sb", "soa-mb", "aosoa:8", "aosoa:32", "aosoa:3", "bytesplit:soa-mb",
+           "bitpack-float:8,23", "split:Pos:soa-mb:aosoa:4"]
+FAST_TOL = 2e-6
+
+
+def schema(t):
+    return f"Record{{Pos:Record{{x:{t},y:{t},z:{t}}},Vel:Record{{x:{t},y:{t},z:{t}}},Mass:{t}}}"
+
+
+def run_gpu(layout, n, steps, f64=False, mode=0, seed=42):
+    from paper_2302_08251_b200 import lamina as L
+    v = L.View(L.Layout(schema("f64" if f64 else "f32"), f"i64:[{n}]", layout))
+    v.nbody_init(seed)
+    for _ in range(steps):
+        v.nbody_update(mode)
+        v.nbody_move()
+    return v
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_exact_matches_oracle(layout):
+    n, steps = 512, 3
+    pos, vel, mass, cs = O.nbody_run(n, steps, seed=42, dtype=np.float32)
+    v = run_gpu(layout, n, steps)
+    assert v.nbody_checksum() == cs
+    vals = v.read_values(np.repeat(np.arange(n), 7), np.tile(np.arange(7), n)).reshape(n, 7)
+    got = vals.astype(np.uint32).view(np.float32)
+    assert np.array_equal(got[:, :3].view(np.uint32), pos.view(np.uint32))
+    assert np.array_equal(got[:, 3:6].view(np.uint32), vel.view(np.uint32))
+
+
+@pytest.mark.parametrize("case", [c for c in json.load(open(os.path.join(ROOT, "tests", "golden", "index.json")))
+                                  if c["file"].startswith("nbody_")], ids=lambda c: c["file"])
+def test_exact_matches_reference_fixture(case):
+    z = np.load(os.path.join(ROOT, "tests", "golden", case["file"]))
+    v = run_gpu(case["layout"], case["n"], case["steps"], f64=case["f64"])
+    assert v.nbody_checksum() == float(z["checksum"])
+    for k, b in enumerate(v.download_all()):
+        assert np.array_equal(b, z[f"b{k}"])
+
+
+def test_exact_f64():
+    n, steps = 256, 2
+    _, _, _, cs = O.nbody_run(n, steps, seed=7, dtype=np.float64)
+    assert run_gpu("soa-mb", n, steps, f64=True, seed=7).nbody_checksum() == cs
+
+
+@pytest.mark.parametrize("layout", ["aos-packed", "soa-mb", "aosoa:32"])
+def test_fast_within_tolerance(layout):
+    n, steps = 4096, 5
+    pos, _, _, _ = O.nbody_run(n, steps, seed=42, dtype=np.float64)
+    v = run_gpu(layout, n, steps, mode=1)
+    got = v.read_values(np.repeat(np.arange(n), 3), np.tile(np.arange(3), n)).reshape(n, 3)
+    got = got.astype(np.uint32).view(np.float32).astype(np.float64)
+    err = np.abs(got - pos) / np.maximum(1.0, np.abs(pos))
+    assert err.max() <= FAST_TOL, err.max()
+
+
+def test_sharded_update_equals_whole():
+    """i-range sharding (the multi-GPU decomposition) is bit-identical to one launch."""
+    from paper_2302_08251_b200 import lamina as L
+    n = 1000
+    a = run_gpu("aosoa:8", n, 0)
+    b = run_gpu("aosoa:8", n, 0)
+    a.nbody_update(0)
+    for lo, hi in [(0, 256), (256, 600), (600, 1000)]:
+        b.nbody_update(0, lo, hi)
+    for x, y in zip(a.download_all(), b.download_all()):
+        assert np.array_equal(x, y)
