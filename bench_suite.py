@@ -1,0 +1,116 @@
+"""Secondary configs of BASELINE.json timed on one GPU (bench.py --suite).
+
+C1  1M n-body records aos-packed -> soa-mb (fits in L2: reported, not a roofline number)
+C3  BitpackIntSoA b in {3,7,12,16,24,31} and BitpackFloatSoA e8m10 / e5m10, pack and unpack, 2^28 values
+C4  n-body 128K particles f32: update (exact and fast) over aos-packed / soa-mb / aosoa:8 / aosoa:32
+C5  one GPU's shard of the 1e9-record copy: 125M R64 records aos-packed ->
+    FieldAccessCount(changetype:f64=f32:bytesplit:soa-mb), 84 B/record
+"""
+from __future__ import annotations
+
+R32 = "Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}"
+R64 = "Record{Pos:Record{x:f64,y:f64,z:f64},Vel:Record{x:f64,y:f64,z:f64},Mass:f64}"
+
+
+def _time(fn, reps=5, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+    for r in range(reps):
+        ev[2 * r].record()
+        fn()
+        ev[2 * r + 1].record()
+    torch.cuda.synchronize()
+    ms = sorted(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps))
+    return ms[len(ms) // 2]
+
+
+def _fill(L, view, seed):
+    import torch
+    lay = view.layout
+    n = lay.element_count
+    types = lay.leaf_types
+    size = sum(lay.leaf(f)[1] for f in range(lay.leaf_count))
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    raw = torch.randint(0, 2**31 - 1, ((n * size + 3) // 4,), device="cuda", dtype=torch.int32, generator=g)
+    raw = raw.view(torch.uint8)[: n * size]
+    if all(t == 8 for t in types):  # floats: keep them finite-ish so the minifloat paths see real values
+        raw = (torch.randn(n * len(types), device="cuda", generator=g) * 100).to(torch.float32).view(torch.uint8)
+    schema = view.layout.schema
+    tmp = L.View(L.Layout(schema, f"i32:[{n}]", "aos-packed"), blobs=[raw.data_ptr()], blob_bytes=[n * size])
+    L.copy_view(tmp, view)
+    torch.cuda.synchronize()
+
+
+def run_suite(L, device=0, peak_gbs=6550.7):
+    import torch
+    out = {}
+    # ---- C1 ------------------------------------------------------------------------------
+    n = 1 << 20
+    a = L.View(L.Layout(R32, f"i32:[{n}]", "aos-packed"))
+    b = L.View(L.Layout(R32, f"i32:[{n}]", "soa-mb"))
+    _fill(L, a, 1)
+    ms = _time(lambda: L.copy_view(a, b))
+    out["C1_aos_to_soamb_1M"] = {"GB/s": 56 * n / ms / 1e6, "ms": ms, "note": "58.7 MB working set is L2-resident"}
+    del a, b
+    # ---- C3 ------------------------------------------------------------------------------
+    n = 1 << 28
+    c3 = {}
+    src = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
+    _fill(L, src, 3)
+    back = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
+    for bits in (3, 7, 12, 16, 24, 31):
+        pk = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", f"bitpack-int:{bits}"))
+        byt = (4 + bits / 8) * n
+        msp = _time(lambda: L.copy_view(src, pk), reps=3)
+        msu = _time(lambda: L.copy_view(pk, back), reps=3)
+        c3[f"int{bits}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
+                            "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
+        del pk
+    del src, back
+    fsrc = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
+    _fill(L, fsrc, 4)
+    fback = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
+    for e, m in ((8, 10), (5, 10)):
+        pk = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", f"bitpack-float:{e},{m}"))
+        byt = (4 + (1 + e + m) / 8) * n
+        msp = _time(lambda: L.copy_view(fsrc, pk), reps=3)
+        msu = _time(lambda: L.copy_view(pk, fback), reps=3)
+        c3[f"e{e}m{m}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
+                           "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
+        del pk
+    del fsrc, fback
+    out["C3_bitpack_2^28"] = c3
+    # ---- C4 ------------------------------------------------------------------------------
+    n = 128 * 1024
+    props = torch.cuda.get_device_properties(device)
+    fp32_peak = 2 * 128 * props.multi_processor_count * 1.965e9 / 1e12  # TFLOP/s at max SM clock
+    c4 = {}
+    for lay in ("aos-packed", "soa-mb", "aosoa:8", "aosoa:32"):
+        v = L.View(L.Layout(R32, f"i64:[{n}]", lay))
+        v.nbody_init(42)
+        row = {}
+        for mode, name in ((1, "fast"), (0, "exact")):
+            ms = _time(lambda: v.nbody_update(mode), reps=3, warm=1)
+            ips = n * n / (ms * 1e-3)
+            row[name] = {"ms_per_update": ms, "interactions/s": ips, "TFLOP/s@20": ips * 20 / 1e12,
+                         "frac_fp32_peak": ips * 20 / 1e12 / fp32_peak}
+        row["move_ms"] = _time(lambda: v.nbody_move(), reps=3)
+        c4[lay] = row
+        del v
+    out["C4_nbody_128K_f32"] = dict(c4, fp32_peak_tflops=fp32_peak,
+                                    peak_note="2 x 128 FP32 lanes x SMs x 1.965 GHz (max SM clock)")
+    # ---- C5 ------------------------------------------------------------------------------
+    n = 125_000_000
+    src = L.View(L.Layout(R64, f"i32:[{n}]", "aos-packed"))
+    _fill(L, src, 5)
+    dst = L.View(L.Layout(R64, f"i32:[{n}]", "changetype:f64=f32:bytesplit:soa-mb", wrap=1))
+    ms = _time(lambda: L.copy_view(src, dst), reps=3)
+    r, w = dst.counters()
+    out["C5_shard_125M_R64_to_FAC_changetype_bytesplit"] = {
+        "GB/s": 84 * n / ms / 1e6, "frac": 84 * n / ms / 1e6 / peak_gbs, "ms": ms,
+        "writes_per_leaf_after_runs": [int(x) for x in w]}
+    del src, dst
+    return out

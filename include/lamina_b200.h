@@ -104,6 +104,12 @@ uint64_t lam_layout_heatmap_blocks(const lam_layout* layout, size_t nr);
 /* Element alignment unit for sharding/chunking: every multiple of it starts every blob
  * stream on a 16-byte boundary (AoSoA lanes, bit-stream words). */
 uint64_t lam_layout_shard_unit(const lam_layout* layout);
+/* Blob streams (disjoint blob regions advancing by a fixed stride per element block) and the
+ * byte range [lo, hi) of blob *nr that elements [begin, end) occupy in stream s: what a shard
+ * of a multi-GPU run owns and exchanges (e.g. the n-body all-gather of positions). */
+size_t lam_layout_stream_count(const lam_layout* layout);
+int lam_layout_stream_region(const lam_layout* layout, size_t stream, uint64_t begin, uint64_t end, size_t* nr,
+                             uint64_t* lo, uint64_t* hi);
 
 /* ---- device views ---------------------------------------------------------------------
  * Replaces lamina::View(MappingPtr) (core/src/view.cpp:97-103): allocates blobCount()

@@ -39,6 +39,8 @@ _SIGS = {
     "lam_layout_physical_offset": (i32, [vp, u64, sz, C.POINTER(sz), C.POINTER(u64)]),
     "lam_layout_heatmap_blocks": (u64, [vp, sz]),
     "lam_layout_shard_unit": (u64, [vp]),
+    "lam_layout_stream_count": (sz, [vp]),
+    "lam_layout_stream_region": (i32, [vp, sz, u64, u64, C.POINTER(sz), C.POINTER(u64), C.POINTER(u64)]),
     "lam_view_alloc": (i32, [vp, i32, vp, C.POINTER(vp)]),
     "lam_view_wrap": (i32, [vp, i32, C.POINTER(vp), C.POINTER(u64), sz, C.POINTER(vp)]),
     "lam_view_free": (None, [vp]),

@@ -332,6 +332,40 @@ extern "C"
         return l->L->shardUnit;
     }
 
+    size_t lam_layout_stream_count(const lam_layout* l)
+    {
+        return l->L->streams.size();
+    }
+
+    int lam_layout_stream_region(const lam_layout* l, size_t s, uint64_t begin, uint64_t end, size_t* nr,
+                                 uint64_t* lo, uint64_t* hi)
+    {
+        return guard(
+            [&]
+            {
+                if(s >= l->L->streams.size())
+                    throw std::out_of_range("index out of range: stream " + std::to_string(s));
+                if(begin > end || end > l->L->map->elementCount())
+                    throw std::out_of_range("index out of range: elements");
+                const lamp_stream& st = l->L->streams[s];
+                uint64_t a, b;
+                if(st.kind == LAMS_BITS)
+                {
+                    a = (begin * st.block_stride / 32) * 4;
+                    b = ((end * st.block_stride + 31) / 32) * 4;
+                }
+                else
+                {
+                    a = st.base0 + (begin / st.lanes) * st.block_stride;
+                    b = st.base0 + ((end + st.lanes - 1) / st.lanes) * st.block_stride;
+                }
+                const uint64_t size = l->L->map->blobSize(st.nr);
+                *nr = st.nr;
+                *lo = a < size ? a : size;
+                *hi = b < size ? b : size;
+            });
+    }
+
     // ---- views ----------------------------------------------------------------------------
     int lam_view_alloc(const lam_layout* l, int device, void* stream, lam_view** out)
     {

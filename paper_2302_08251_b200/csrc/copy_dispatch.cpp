@@ -1,6 +1,7 @@
 // copyView dispatch (view.cpp:168-189) and the host-buffer entry point.
 #include "capi_internal.hpp"
 
+#include <cstdlib>
 #include <cstring>
 
 using namespace lamb;
@@ -48,7 +49,9 @@ namespace lamhost
         if(begin == end || a.schema().leafCount() == 0)
             return;
         DeviceGuard g(src.device);
-        if(full && sameLayout(a, b))
+        // LAMB_FORCE_TILE=1 (profiling only) routes equal layouts through the tile engine
+        static const bool forceTile = std::getenv("LAMB_FORCE_TILE") && std::getenv("LAMB_FORCE_TILE")[0] == '1';
+        if(full && sameLayout(a, b) && !forceTile)
         {
             for(size_t nr = 0; nr < a.blobCount(); ++nr)
                 lam_cuda_check(lamk::blob_copy(dst.blobs[nr], src.blobs[nr], a.blobSize(nr), s), "blob_copy");

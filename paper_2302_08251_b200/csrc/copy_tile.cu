@@ -338,43 +338,129 @@ namespace lamk
         return (e / L) * bs + (e % L) * ls;
     }
 
-    __global__ void __launch_bounds__(512, 1) k_tile_copy(const __grid_constant__ lamt_params p)
+    __device__ __forceinline__ void cp_async16(void* smem, const void* g)
+    {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+    }
+    __device__ __forceinline__ void cp_async_commit()
+    {
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    template<int N>
+    __device__ __forceinline__ void cp_async_wait()
+    {
+        asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+    }
+    __device__ __forceinline__ void cp_async_wait_dyn(uint32_t n)
+    {
+        switch(n)
+        {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        default: cp_async_wait<3>(); break;
+        }
+    }
+
+    __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+    {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    }
+
+    __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n)
+    {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    }
+
+    // Warp-specialised pipeline.  Warp 0 (one elected lane) is the producer: it keeps
+    // `stages` tiles of TMA bulk loads in flight (mbarrier full[s], tx-counted), issues the
+    // TMA bulk stores of each finished tile and recycles destination buffers once the bulk
+    // store has read them (dfree[d]).  Warps 1.. (the consumers) only transform: wait full[s]
+    // and dfree[d], move the tile through shared memory, fence the async proxy and arrive on
+    // tdone[s].  No CTA-wide barrier in the steady state.
+    __global__ void __launch_bounds__(544, 1) k_tile_copy(const __grid_constant__ lamt_params p)
     {
         extern __shared__ __align__(128) uint8_t smem[];
-        __shared__ __align__(8) uint64_t mbar[LAMT_MAX_STAGES];
-        const bool lead = threadIdx.x == 0;
+        __shared__ __align__(8) uint64_t full[LAMT_MAX_STAGES];
+        __shared__ __align__(8) uint64_t tdone[LAMT_MAX_STAGES];
+        __shared__ __align__(8) uint64_t dfree[8];
+        const uint32_t warp = threadIdx.x >> 5;
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t ncons = blockDim.x - 32; // consumer threads
+        const uint32_t nconsWarps = ncons >> 5;
         uint8_t* srcBase = smem;
         uint8_t* dstBase = smem + p.stages * p.src_bytes;
-        if(lead)
+        if(threadIdx.x == 0)
         {
             for(uint32_t s = 0; s < p.stages; ++s)
-                mbar_init(&mbar[s], 1);
+            {
+                mbar_init(&full[s], 1);
+                mbar_init(&tdone[s], nconsWarps);
+            }
+            for(uint32_t d = 0; d < p.dstages; ++d)
+                mbar_init(&dfree[d], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
 
-        auto issue_load = [&](uint32_t tile, uint32_t s)
+        if(warp == 0)
         {
-            const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
-            uint8_t* sb = srcBase + s * p.src_bytes;
-            if(p.tma_bytes)
-                mbar_expect_tx(&mbar[s], p.tma_bytes);
-            else
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[s])) : "memory");
-            for(uint32_t k = 0; k < p.nsrc; ++k)
+            // ================= producer =================
+            if(lane != 0)
+                return;
+            auto load = [&](uint32_t tile, uint32_t s)
             {
-                const lamt_stream& st = p.st[k];
-                if(st.tma && st.tile_bytes)
-                    bulk_g2s(sb + st.smem_off, reinterpret_cast<const uint8_t*>(st.gptr) + tile_global_off(st, t0),
-                             st.tile_bytes, &mbar[s]);
-            }
-        };
-
-        if(lead)
+                const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+                uint8_t* sb = srcBase + s * p.src_bytes;
+                if(p.tma_bytes)
+                    mbar_expect_tx(&full[s], p.tma_bytes);
+                else
+                    mbar_arrive(&full[s]);
+                for(uint32_t k = 0; k < p.nsrc; ++k)
+                {
+                    const lamt_stream& st = p.st[k];
+                    if(st.tma && st.tile_bytes)
+                        bulk_g2s(sb + st.smem_off, reinterpret_cast<const uint8_t*>(st.gptr) + tile_global_off(st, t0),
+                                 st.tile_bytes, &full[s]);
+                }
+            };
+            for(uint32_t d = 0; d < p.dstages; ++d)
+                mbar_arrive(&dfree[d]); // every destination buffer starts free
             for(uint32_t s = 0; s < p.stages; ++s)
                 if(blockIdx.x + s * gridDim.x < p.ntiles)
-                    issue_load(blockIdx.x + s * gridDim.x, s);
+                    load(blockIdx.x + s * gridDim.x, s);
+            for(uint32_t j = 0;; ++j)
+            {
+                const uint32_t tile = blockIdx.x + j * gridDim.x;
+                if(tile >= p.ntiles)
+                    break;
+                const uint32_t s = j % p.stages;
+                const uint32_t d = j % p.dstages;
+                mbar_wait(&tdone[s], (j / p.stages) & 1);
+                const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+                uint8_t* db = dstBase + d * p.dst_bytes;
+                for(uint32_t k = p.nsrc; k < p.nsrc + p.ndst; ++k)
+                {
+                    const lamt_stream& st = p.st[k];
+                    if(st.tma && st.tile_bytes)
+                        bulk_s2g(reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0), db + st.smem_off,
+                                 st.tile_bytes);
+                }
+                bulk_commit();
+                const uint32_t next = tile + p.stages * gridDim.x;
+                if(next < p.ntiles)
+                    load(next, s);
+                // the store group of tile j-D+1 has left smem -> its buffer serves tile j+1
+                bulk_wait_read_dyn(p.dstages - 1);
+                if(j + 1 >= p.dstages)
+                    mbar_arrive(&dfree[(j + 1) % p.dstages]);
+            }
+            bulk_wait_all();
+            return;
+        }
 
+        // ================= consumers =================
+        const uint32_t ct = threadIdx.x - 32;
         uint32_t os[LAMT_UNI_LEAVES], od[LAMT_UNI_LEAVES];
 #pragma unroll
         for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
@@ -382,7 +468,6 @@ namespace lamk
             os[f] = p.uoff_s[f];
             od[f] = p.uoff_d[f];
         }
-
         uint32_t done = 0;
         for(uint32_t k = 0;; ++k)
         {
@@ -394,24 +479,25 @@ namespace lamk
             uint8_t* sb = srcBase + s * p.src_bytes;
             uint8_t* db = dstBase + d * p.dst_bytes;
             const uint64_t t0 = p.begin + uint64_t(tile) * p.T;
+            mbar_wait(&full[s], (k / p.stages) & 1);
+            mbar_wait(&dfree[d], (k / p.dstages) & 1);
             if(p.any_coop)
             {
                 for(uint32_t j = 0; j < p.nsrc; ++j)
                 {
                     const lamt_stream& st = p.st[j];
                     if(!st.tma && st.tile_bytes)
-                        coop_g2s(sb + st.smem_off, reinterpret_cast<const uint8_t*>(st.gptr) + tile_global_off(st, t0),
-                                 st.tile_bytes);
+                        for(uint32_t q = ct; q < st.tile_bytes; q += ncons)
+                            sb[st.smem_off + q] = __ldg(reinterpret_cast<const uint8_t*>(st.gptr)
+                                                        + tile_global_off(st, t0) + q);
                 }
-                __syncthreads();
+                named_sync(1, ncons);
             }
-            mbar_wait(&mbar[s], (k / p.stages) & 1);
-
             // ---- transform ----
             if(p.uni)
             {
                 const uint32_t nl = p.nleaves;
-                for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                for(uint32_t e = ct; e < p.T; e += ncons)
                 {
                     const uint32_t es = uni_off(e, p.ul_s, p.ush_s, p.ubs_s, p.uls_s);
                     const uint32_t ed = uni_off(e, p.ul_d, p.ush_d, p.ubs_d, p.uls_d);
@@ -442,7 +528,7 @@ namespace lamk
                 for(uint32_t f = 0; f < p.nleaves; ++f)
                 {
                     const lamt_leaf& L = p.leaf[f];
-                    for(uint32_t e = threadIdx.x; e < p.T; e += blockDim.x)
+                    for(uint32_t e = ct; e < p.T; e += ncons)
                     {
                         uint64_t v = tile_read(p, L, sb, e);
                         v = lamd::convert_value(v, L.stype, L.ltype);
@@ -452,50 +538,36 @@ namespace lamk
                 }
                 if(p.any_bits)
                 {
-                    __syncthreads();
+                    named_sync(1, ncons);
                     for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
                         if(p.st[j].kind == 1)
-                            pack_words(p.st[j], db, p.T, threadIdx.x, blockDim.x);
+                            pack_words(p.st[j], db, p.T, ct, ncons);
                 }
             }
             done += p.T;
             if(p.any_coop)
             {
-                __syncthreads();
+                named_sync(1, ncons);
                 for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
                 {
                     const lamt_stream& st = p.st[j];
                     if(!st.tma && st.tile_bytes)
-                        coop_s2g(reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0), db + st.smem_off,
-                                 st.tile_bytes);
+                        for(uint32_t q = ct; q < st.tile_bytes; q += ncons)
+                            (reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0))[q] = db[st.smem_off + q];
                 }
             }
+            // make this thread's smem writes visible to the async proxy (the TMA store), then
+            // one arrival per consumer warp
             fence_async_smem();
-            if(lead)
-                bulk_wait_read_dyn(p.dstages - 2); // the store that used the NEXT dst buffer has left smem
-            __syncthreads();
-            if(lead)
-            {
-                for(uint32_t j = p.nsrc; j < p.nsrc + p.ndst; ++j)
-                {
-                    const lamt_stream& st = p.st[j];
-                    if(st.tma && st.tile_bytes)
-                        bulk_s2g(reinterpret_cast<uint8_t*>(st.gptr) + tile_global_off(st, t0), db + st.smem_off,
-                                 st.tile_bytes);
-                }
-                bulk_commit();
-                const uint32_t next = tile + p.stages * gridDim.x;
-                if(next < p.ntiles)
-                    issue_load(next, s);
-            }
+            __syncwarp();
+            if(lane == 0)
+                mbar_arrive(&tdone[s]);
         }
-        if(lead)
-            bulk_wait_all();
         // FieldAccessCount: every element of every leaf of a tile is accessed once; one
         // global atomic per CTA per field (instrument.cpp:57-72)
         if((p.facS || p.facD) && done)
         {
-            for(uint32_t f = threadIdx.x; f < p.nleaves; f += blockDim.x)
+            for(uint32_t f = ct; f < p.nleaves; f += ncons)
             {
                 if(p.facS)
                     atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + f, static_cast<unsigned long long>(done));
@@ -504,6 +576,71 @@ namespace lamk
                               static_cast<unsigned long long>(done));
             }
         }
+    }
+
+    // Direct uniform copy: no shared memory.  Thread = element; per leaf one 4/8-byte load at
+    // the source geometry and one store at the destination geometry.  The strided side (AoS
+    // 28-byte stride) is served from L1: the 7 leaf loads of a warp touch the same 7 lines.
+    template<typename W, int UNROLL>
+    __global__ void __launch_bounds__(256) k_uniform_direct(const __grid_constant__ lamt_params p, uint64_t n)
+    {
+        const uint8_t* sbase[LAMT_UNI_LEAVES];
+        uint8_t* dbase[LAMT_UNI_LEAVES];
+        const uint32_t nl = p.nleaves;
+#pragma unroll
+        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+            if(f < nl)
+            {
+                sbase[f] = reinterpret_cast<const uint8_t*>(p.st[p.leaf[f].s[0].stream].gptr) + p.leaf[f].s[0].inblock;
+                dbase[f] = reinterpret_cast<uint8_t*>(p.st[p.leaf[f].d[0].stream].gptr) + p.leaf[f].d[0].inblock;
+            }
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * UNROLL;
+        for(uint64_t i0 = p.begin + static_cast<uint64_t>(blockIdx.x) * blockDim.x * UNROLL + threadIdx.x;
+            i0 < p.begin + n; i0 += stride)
+        {
+            W v[UNROLL][LAMT_UNI_LEAVES];
+            uint64_t ed[UNROLL];
+#pragma unroll
+            for(int u = 0; u < UNROLL; ++u)
+            {
+                const uint64_t i = i0 + uint64_t(u) * blockDim.x;
+                const uint64_t ii = i < p.begin + n ? i : p.begin;
+                const uint64_t es = p.ul_s == 1 ? ii * p.ubs_s
+                                                : (ii >> p.ush_s) * p.ubs_s + (ii & (p.ul_s - 1)) * p.uls_s;
+                ed[u] = p.ul_d == 1 ? ii * p.ubs_d : (ii >> p.ush_d) * p.ubs_d + (ii & (p.ul_d - 1)) * p.uls_d;
+#pragma unroll
+                for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                    if(f < nl)
+                        v[u][f] = __ldcs(reinterpret_cast<const W*>(sbase[f] + es));
+            }
+#pragma unroll
+            for(int u = 0; u < UNROLL; ++u)
+            {
+                const uint64_t i = i0 + uint64_t(u) * blockDim.x;
+                if(i < p.begin + n)
+                {
+#pragma unroll
+                    for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                        if(f < nl)
+                            __stcs(reinterpret_cast<W*>(dbase[f] + ed[u]), v[u][f]);
+                }
+            }
+        }
+    }
+
+    cudaError_t uniform_direct(const lamt_params& p, uint64_t n, cudaStream_t s)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t want = (n + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 8;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        if(p.usize == 4)
+            k_uniform_direct<uint32_t, 2><<<grid, 256, 0, s>>>(p, n);
+        else
+            k_uniform_direct<unsigned long long, 2><<<grid, 256, 0, s>>>(p, n);
+        count_launch();
+        return cudaGetLastError();
     }
 
     cudaError_t tile_copy(const lamt_params& p, uint32_t smemBytes, uint32_t ctasPerSm, cudaStream_t s)
@@ -523,10 +660,17 @@ namespace lamk
                 attrSet[dev] = smemBytes;
         }
         const uint32_t sms = static_cast<uint32_t>(sm_count(dev));
-        uint64_t grid = static_cast<uint64_t>(sms) * ctasPerSm;
+        // persistent grid: exactly the CTAs that are co-resident (a second wave would serialise)
+        int occ = 0;
+        cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_copy, static_cast<int>(p.threads + 32),
+                                                                       smemBytes);
+        if(oe != cudaSuccess || occ < 1)
+            occ = 1;
+        const uint32_t perSm = ctasPerSm < static_cast<uint32_t>(occ) ? ctasPerSm : static_cast<uint32_t>(occ);
+        uint64_t grid = static_cast<uint64_t>(sms) * perSm;
         if(grid > p.ntiles)
             grid = p.ntiles;
-        k_tile_copy<<<static_cast<unsigned>(grid), p.threads, smemBytes, s>>>(p);
+        k_tile_copy<<<static_cast<unsigned>(grid), p.threads + 32, smemBytes, s>>>(p);
         count_launch();
         return cudaGetLastError();
     }

@@ -11,6 +11,7 @@
 namespace lamk
 {
     cudaError_t tile_copy(const lamt_params& p, uint32_t smemBytes, uint32_t ctasPerSm, cudaStream_t s);
+    cudaError_t uniform_direct(const lamt_params& p, uint64_t n, cudaStream_t s);
 }
 
 using namespace lamb;
@@ -200,7 +201,7 @@ namespace lamhost
             const uint32_t stages = static_cast<uint32_t>(envNum("LAMB_TILE_STAGES", 3));
             const uint32_t dstages = static_cast<uint32_t>(envNum("LAMB_TILE_DSTAGES", 2));
             if(unit > (1u << 16) || bpe * unit > 100.0 * 1024 || stages < 1 || stages > LAMT_MAX_STAGES
-               || dstages < 2 || dstages > 5)
+               || dstages < 2 || dstages > 4)
                 return pl;
             uint64_t T = static_cast<uint64_t>(stageTarget / (bpe > 0 ? bpe : 1) / unit) * unit;
             if(T < unit)
@@ -256,6 +257,11 @@ namespace lamhost
             for(int k = 0; k < ndst; ++k)
                 p.any_bits |= p.st[nsrc + k].kind == 1;
             p.threads = static_cast<uint32_t>(envNum("LAMB_TILE_THREADS", 256));
+            p.stg = envNum("LAMB_TILE_STG", 1) != 0;
+            p.lmode = static_cast<uint32_t>(envNum("LAMB_TILE_LMODE", 1));
+            p.chunk = static_cast<uint32_t>(envNum("LAMB_TILE_CHUNK", 0)) & ~15u;
+            if(p.lmode == 1 && stages < 2)
+                return pl;
             pl.smem = stages * p.src_bytes + dstages * p.dst_bytes;
             const uint32_t smBudget = 226 * 1024;
             if(pl.smem > smBudget)
@@ -341,6 +347,12 @@ namespace lamhost
             p.any_coop |= p.st[k].tile_bytes && !p.st[k].tma;
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
+        if(p.uni && !p.facS && !p.facD && envNum("LAMB_DIRECT", 0) != 0 && (p.ush_s != 0xFFFFFFFFu || p.ul_s == 1)
+           && (p.ush_d != 0xFFFFFFFFu || p.ul_d == 1))
+        {
+            lam_cuda_check(lamk::uniform_direct(p, end - begin, s), "uniform_direct");
+            return true;
+        }
         lam_cuda_check(lamk::tile_copy(p, pl.smem, pl.ctas, s), "tile_copy");
         const uint64_t doneEnd = begin + ntiles * p.T;
         if(doneEnd < end)

@@ -71,6 +71,9 @@ struct lamt_params
     uint32_t stages;     // source stage buffers (loads in flight ahead of the transform)
     uint32_t dstages;    // destination buffers (stores draining behind it), >= 2
     uint32_t threads;    // threads per CTA
+    uint32_t stg;        // destination images leave through 16-byte thread stores instead of TMA
+    uint32_t lmode;      // 0: TMA bulk loads (mbarrier), 1: cp.async 16-byte loads (commit groups)
+    uint32_t chunk;      // lmode 0: bytes per bulk op (0 = whole image)
     uint32_t any_bits;   // some destination stream is bit-packed
     uint32_t any_coop;   // some stream is not TMA-able
     uint32_t facS, facD;

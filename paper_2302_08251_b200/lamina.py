@@ -175,6 +175,16 @@ class Layout:
     def shard_unit(self) -> int:
         return lib().lam_layout_shard_unit(self._h)
 
+    @property
+    def stream_count(self) -> int:
+        return lib().lam_layout_stream_count(self._h)
+
+    def stream_region(self, stream: int, begin: int, end: int) -> tuple[int, int, int]:
+        """(blob nr, lo, hi): bytes of blob nr that elements [begin, end) occupy in `stream`."""
+        nr, lo, hi = C.c_size_t(), C.c_uint64(), C.c_uint64()
+        _check(lib().lam_layout_stream_region(self._h, stream, begin, end, C.byref(nr), C.byref(lo), C.byref(hi)))
+        return nr.value, lo.value, hi.value
+
     def __repr__(self):
         return f"Layout({self.name!r}, {self.schema!r}, {self.extents!r})"
 

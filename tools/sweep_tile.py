@@ -1,4 +1,4 @@
-"""Tile-engine tuning sweep on the GPU: stage size x pipeline depth x warps per CTA."""
+"""Tile-engine tuning sweep on the GPU over the LAMB_TILE_* knobs (host planner reads them per call)."""
 import itertools
 import json
 import os
@@ -8,6 +8,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 R32 = "Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}"
+KNOBS = ["LAMB_TILE_KB", "LAMB_TILE_STAGES", "LAMB_TILE_THREADS", "LAMB_TILE_STG", "LAMB_TILE_DSTAGES",
+         "LAMB_TILE_LMODE", "LAMB_TILE_CHUNK"]
 
 
 def main():
@@ -19,27 +21,26 @@ def main():
     views = {}
     for a in {x for p in pairs for x in p}:
         views[a] = (L.View(L.Layout(R32, ext, a)), L.View(L.Layout(R32, ext, a)))
-    grid = list(itertools.product([12, 24, 36, 48], [2, 3, 4], [256, 512]))
+    grid = [(kb, st, th, 1, 2, 1, 0) for kb, st, th in itertools.product([12, 24, 36, 48], [2, 3, 4], [256, 512])]
+    grid += [(kb, st, 256, 1, 2, 0, ch) for kb, st, ch in itertools.product([24, 36], [2, 4], [1024, 4096])]
     if len(sys.argv) > 1:
         grid = [tuple(float(x) for x in g.split(",")) for g in sys.argv[1:]]
-    res = []
-    for kb, st, th in grid:
-        os.environ["LAMB_TILE_KB"] = str(kb)
-        os.environ["LAMB_TILE_STAGES"] = str(int(st))
-        os.environ["LAMB_TILE_THREADS"] = str(int(th))
-        row = {"kb": kb, "stages": st, "threads": th}
+    for cfg in grid:
+        for k, v in zip(KNOBS, cfg):
+            os.environ[k] = str(v)
+        row = dict(zip(["kb", "stages", "threads", "stg", "dstages", "lmode", "chunk"], cfg))
         for a, b in pairs:
             s, d = views[a][0], views[b][1]
             L.copy_view(s, d)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
-            for r in range(4):
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            for r in range(3):
                 ev[2 * r].record()
                 L.copy_view(s, d)
                 ev[2 * r + 1].record()
             torch.cuda.synchronize()
-            ms = min(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(4))
+            ms = min(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(3))
             row[f"{a}->{b}"] = round(56 * n / ms / 1e6, 1)
-        res.append(row)
         print(json.dumps(row), flush=True)
 
 
