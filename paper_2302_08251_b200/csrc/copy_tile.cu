@@ -628,6 +628,139 @@ namespace lamk
         }
     }
 
+    // Warp-tile transpose for uniform physical pairs: every warp owns a private smem slice and
+    // streams warp tiles of WT elements: 16-byte coalesced loads of the source images
+    // (registers -> smem), the per-leaf transpose in smem, 16-byte coalesced stores of the
+    // destination images.  Only __syncwarp; images of one side all have the same size
+    // (one stream per leaf for SoA, one stream for AoS/AoSoA).
+    template<typename W, int CH>
+    __global__ void __launch_bounds__(256) k_uniform_warp(const __grid_constant__ lamt_params p, uint32_t ntiles)
+    {
+        extern __shared__ __align__(16) uint8_t wsm[];
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t warp = threadIdx.x >> 5;
+        const uint32_t WT = p.T;
+        uint8_t* sbuf = wsm + warp * (p.src_bytes + p.dst_bytes);
+        uint8_t* dbuf = sbuf + p.src_bytes;
+        const uint32_t ns = p.nsrc, nd = p.ndst;
+        const uint32_t imgS = p.st[0].tile_bytes, imgD = p.st[ns].tile_bytes;
+        const uint32_t cpsS = imgS >> 4, cpsD = imgD >> 4; // 16-byte chunks per image
+        const uint32_t chS = ns * cpsS, chD = nd * cpsD;
+        uint32_t os[LAMT_UNI_LEAVES], od[LAMT_UNI_LEAVES];
+        const uint32_t nl = p.nleaves;
+#pragma unroll
+        for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+        {
+            os[f] = p.uoff_s[f];
+            od[f] = p.uoff_d[f];
+        }
+        const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp;
+        const uint32_t tw = gridDim.x * (blockDim.x >> 5);
+        __shared__ unsigned long long s_done;
+        if(threadIdx.x == 0)
+            s_done = 0;
+        __syncthreads();
+        uint32_t done = 0;
+        for(uint32_t wt = gw; wt < ntiles; wt += tw)
+        {
+            done += WT;
+            const uint64_t t0 = p.begin + uint64_t(wt) * WT;
+            // ---- load: CH chunks per lane in flight ----
+            for(uint32_t c0 = 0; c0 < chS; c0 += 32 * CH)
+            {
+                uint4 v[CH];
+#pragma unroll
+                for(int u = 0; u < CH; ++u)
+                {
+                    const uint32_t c = c0 + u * 32 + lane;
+                    if(c < chS)
+                    {
+                        const uint32_t j = c / cpsS, o = c - j * cpsS;
+                        const uint4* g = reinterpret_cast<const uint4*>(
+                            reinterpret_cast<const uint8_t*>(p.st[j].gptr) + tile_global_off(p.st[j], t0));
+                        v[u] = __ldcs(g + o);
+                    }
+                }
+#pragma unroll
+                for(int u = 0; u < CH; ++u)
+                {
+                    const uint32_t c = c0 + u * 32 + lane;
+                    if(c < chS)
+                        reinterpret_cast<uint4*>(sbuf)[c] = v[u];
+                }
+            }
+            __syncwarp();
+            // ---- transpose in smem ----
+            for(uint32_t e = lane; e < WT; e += 32)
+            {
+                const uint32_t es = uni_off(e, p.ul_s, p.ush_s, p.ubs_s, p.uls_s);
+                const uint32_t ed = uni_off(e, p.ul_d, p.ush_d, p.ubs_d, p.uls_d);
+                W v[LAMT_UNI_LEAVES];
+#pragma unroll
+                for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                    if(f < nl)
+                        v[f] = *reinterpret_cast<const W*>(sbuf + os[f] + es);
+#pragma unroll
+                for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
+                    if(f < nl)
+                        *reinterpret_cast<W*>(dbuf + od[f] + ed) = v[f];
+            }
+            __syncwarp();
+            // ---- store ----
+            for(uint32_t c = lane; c < chD; c += 32)
+            {
+                const uint32_t j = c / cpsD, o = c - j * cpsD;
+                uint4* g = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.st[ns + j].gptr)
+                                                    + tile_global_off(p.st[ns + j], t0));
+                __stcs(g + o, reinterpret_cast<const uint4*>(dbuf)[c]);
+            }
+            __syncwarp();
+        }
+        // FieldAccessCount: per-warp totals -> shared counter -> one global atomic per CTA per field
+        if(p.facS || p.facD)
+        {
+            if(lane == 0 && done)
+                atomicAdd(&s_done, static_cast<unsigned long long>(done));
+            __syncthreads();
+            for(uint32_t f = threadIdx.x; f < nl && s_done; f += blockDim.x)
+            {
+                if(p.facS)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + f, s_done);
+                if(p.facD)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(p.facDst) + nl + f, s_done);
+            }
+        }
+    }
+
+    cudaError_t uniform_warp(const lamt_params& p, uint32_t ntiles, cudaStream_t s)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint32_t perWarp = p.src_bytes + p.dst_bytes;
+        const uint32_t warps = 8;
+        const size_t smem = static_cast<size_t>(warps) * perWarp;
+        static size_t attr[64] = {0};
+        auto kern = p.usize == 4 ? k_uniform_warp<uint32_t, 4> : k_uniform_warp<unsigned long long, 4>;
+        if(dev < 64 && attr[dev] < smem)
+        {
+            cudaFuncSetAttribute(k_uniform_warp<uint32_t, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            cudaFuncSetAttribute(k_uniform_warp<unsigned long long, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            attr[dev] = smem;
+        }
+        int occ = 0;
+        if(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+        uint64_t grid = static_cast<uint64_t>(sm_count(dev)) * occ;
+        const uint64_t need = (ntiles + warps - 1) / warps;
+        if(grid > need)
+            grid = need;
+        kern<<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p, ntiles);
+        count_launch();
+        return cudaGetLastError();
+    }
+
     cudaError_t uniform_direct(const lamt_params& p, uint64_t n, cudaStream_t s)
     {
         int dev = 0;

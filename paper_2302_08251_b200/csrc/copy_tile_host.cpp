@@ -12,6 +12,44 @@ namespace lamk
 {
     cudaError_t tile_copy(const lamt_params& p, uint32_t smemBytes, uint32_t ctasPerSm, cudaStream_t s);
     cudaError_t uniform_direct(const lamt_params& p, uint64_t n, cudaStream_t s);
+    cudaError_t uniform_warp(const lamt_params& p, uint32_t ntiles, cudaStream_t s);
+
+    struct VecSide
+    {
+        unsigned long long leafBase[LAMT_UNI_LEAVES];
+        unsigned long long recBase;
+        uint32_t recordContig;
+        uint32_t bs, lanes, lshift;
+    };
+    struct VecParams
+    {
+        VecSide s, d;
+        unsigned long long begin;
+        unsigned long long groups;
+        unsigned long long facSrc, facDst;
+        uint32_t nl, facS, facD;
+    };
+    bool vec_transpose(const VecParams& p, uint32_t leafSize, cudaStream_t s);
+
+    struct PackParams
+    {
+        unsigned long long vals, bits, begin, groups;
+        uint32_t w, kind, sgn, E, M, valType;
+        unsigned long long facSrc, facDst;
+        uint32_t facS, facD, leaf, nleaves;
+        uint32_t vbs, vl, vsh, vinb;
+    };
+    bool pack32(const PackParams& p, bool pack, cudaStream_t s);
+
+    struct SplitParams
+    {
+        unsigned long long rec;
+        unsigned long long plane[8][4];
+        unsigned long long begin, groups;
+        unsigned long long facSrc, facDst;
+        uint32_t nl, facS, facD;
+    };
+    bool f64_to_f32_planes(const SplitParams& p, cudaStream_t s);
 }
 
 using namespace lamb;
@@ -315,6 +353,202 @@ namespace lamhost
         }
     } // namespace
 
+    // register-transpose path (vec_transpose.cu) for uniform 4/8-byte-leaf pairs whose sides are
+    // leaf-contiguous in groups of V elements (SoA, AoSoA with V | L) or record-contiguous (AoS)
+    static bool tryVec(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
+                       const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        if(p.usize != 4 && p.usize != 8)
+            return false;
+        const uint32_t V = 16 / p.usize;
+        const uint32_t nl = p.nleaves;
+        if(nl < 1 || nl > 8 || begin % V)
+            return false;
+        lamk::VecParams vp{};
+        auto side = [&](bool src, lamk::VecSide& sd) -> bool
+        {
+            const uint32_t L = src ? p.ul_s : p.ul_d;
+            const uint32_t bs = src ? p.ubs_s : p.ubs_d;
+            const uint32_t ls = src ? p.uls_s : p.uls_d;
+            const uint32_t sh = src ? p.ush_s : p.ush_d;
+            const uint32_t S = p.usize;
+            bool recordContig = L == 1 && bs == nl * S;
+            bool leafContig = (L == 1 && bs == S) || (L > 1 && L % V == 0 && sh != 0xFFFFFFFFu && ls == S);
+            if(recordContig)
+            {
+                // one stream, leaves packed in leaf order
+                const lamt_leaf& L0 = p.leaf[0];
+                const lamt_term& t0 = src ? L0.s[0] : L0.d[0];
+                for(uint32_t f = 0; f < nl && recordContig; ++f)
+                {
+                    const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                    recordContig = t.stream == t0.stream && t.inblock == f * S;
+                }
+                if(recordContig)
+                {
+                    sd.recordContig = 1;
+                    sd.recBase = p.st[t0.stream].gptr;
+                    return (sd.recBase % 16) == 0;
+                }
+            }
+            if(!leafContig)
+                return false;
+            sd.recordContig = 0;
+            sd.bs = bs;
+            sd.lanes = L;
+            sd.lshift = L == 1 ? 0 : sh;
+            for(uint32_t f = 0; f < nl; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                sd.leafBase[f] = p.st[t.stream].gptr + t.inblock;
+                if(sd.leafBase[f] % 16)
+                    return false;
+            }
+            return bs % 16 == 0 || L == 1;
+        };
+        if(!side(true, vp.s) || !side(false, vp.d))
+            return false;
+        vp.begin = begin;
+        vp.groups = (end - begin) / V;
+        vp.nl = nl;
+        vp.facS = p.facS;
+        vp.facD = p.facD;
+        vp.facSrc = p.facSrc;
+        vp.facDst = p.facDst;
+        if(vp.groups == 0)
+            return false;
+        if(!lamk::vec_transpose(vp, p.usize, s))
+            return false;
+        const uint64_t doneEnd = begin + vp.groups * V;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s),
+                           "generic_copy(tail)");
+        (void)D;
+        return true;
+    }
+
+    // K3/K4: every leaf 4-byte physical (SoA or AoSoA with 32 | L) <-> bit stream of width <= 32
+    static bool tryPack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
+                        const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        if(begin % 32 || envNum("LAMB_PACK", 1) == 0)
+            return false;
+        const uint64_t groups = (end - begin) / 32;
+        if(groups == 0)
+            return false;
+        std::vector<lamk::PackParams> jobs;
+        bool packDir = false;
+        for(uint32_t f = 0; f < p.nleaves; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            const bool pk = L.skind == LAMT_K_PHYS && (L.dkind == LAMT_K_BITS_INT || L.dkind == LAMT_K_BITS_FLT);
+            const bool up = L.dkind == LAMT_K_PHYS && (L.skind == LAMT_K_BITS_INT || L.skind == LAMT_K_BITS_FLT);
+            if(!(pk || up) || (f && pk != packDir))
+                return false;
+            packDir = pk;
+            const lamt_term& vt = pk ? L.s[0] : L.d[0];
+            const lamt_stream& vs = p.st[vt.stream];
+            const lamt_stream& bs = p.st[pk ? L.d[0].stream : L.s[0].stream];
+            if(vt.size != 4 || L.stype != L.ltype || L.dtype != L.ltype || L.ltype == Bool)
+                return false;
+            const bool soa = vs.lanes == 1 && vs.bs == 4;
+            const bool aosoa = vs.lanes % 32 == 0 && vs.lshift != 0xFFFFFFFFu && vt.ls == 4;
+            if(!(soa || aosoa))
+                return false;
+            lamk::PackParams j{};
+            const uint8_t kind = pk ? L.dkind : L.skind;
+            j.kind = kind == LAMT_K_BITS_FLT ? 1 : 0;
+            j.E = pk ? L.dE : L.sE;
+            j.M = pk ? L.dM : L.sM;
+            j.w = j.kind ? 1 + j.E + j.M : j.E;
+            if(j.w < 1 || j.w > 32 || bs.bs != j.w)
+                return false;
+            if(j.kind == 1 && L.ltype != F32)
+                return false;
+            j.sgn = pk ? 0 : L.ssigned;
+            j.valType = L.ltype;
+            j.vals = vs.gptr + (soa ? 0 : 0);
+            j.vinb = soa ? 0 : vt.inblock;
+            j.vbs = vs.bs;
+            j.vl = vs.lanes;
+            j.vsh = soa ? 0 : vs.lshift;
+            if(soa)
+                j.vals += vt.inblock;
+            j.bits = bs.gptr;
+            if((j.vals + (soa ? 0 : j.vinb)) % 16 || j.bits % 16)
+                return false;
+            j.begin = begin;
+            j.groups = groups;
+            j.facS = p.facS;
+            j.facD = p.facD;
+            j.facSrc = p.facSrc;
+            j.facDst = p.facDst;
+            j.leaf = f;
+            j.nleaves = p.nleaves;
+            jobs.push_back(j);
+        }
+        for(const auto& j : jobs)
+            if(!lamk::pack32(j, packDir, s))
+                throw std::runtime_error(std::string("pack32 launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        const uint64_t doneEnd = begin + groups * 32;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s),
+                           "generic_copy(tail)");
+        return true;
+    }
+
+    // K5: record-contiguous f64 -> changetype f32 -> bytesplit into 1-byte SoA planes
+    static bool trySplit(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
+                         const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        if(begin % 4 || p.nleaves > 8 || envNum("LAMB_SPLITK", 1) == 0)
+            return false;
+        const uint32_t nl = p.nleaves;
+        lamk::SplitParams sp{};
+        const lamt_term& s0 = p.leaf[0].s[0];
+        for(uint32_t f = 0; f < nl; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            if(L.skind != LAMT_K_PHYS || L.stype != F64 || L.ltype != F64 || L.dkind != LAMT_K_SPLIT || L.dtype != F32
+               || L.dn != 4)
+                return false;
+            const lamt_term& t = L.s[0];
+            const lamt_stream& st = p.st[t.stream];
+            if(t.stream != s0.stream || t.inblock != f * 8 || st.lanes != 1 || st.bs != nl * 8)
+                return false;
+            for(uint32_t k = 0; k < 4; ++k)
+            {
+                const lamt_term& d = L.d[k];
+                const lamt_stream& ds = p.st[d.stream];
+                if(ds.lanes != 1 || ds.bs != 1)
+                    return false;
+                sp.plane[f][k] = ds.gptr + d.inblock;
+                if((sp.plane[f][k] + begin) % 4)
+                    return false;
+            }
+        }
+        sp.rec = p.st[s0.stream].gptr;
+        if((sp.rec + begin * nl * 8) % 16)
+            return false;
+        sp.begin = begin;
+        sp.groups = (end - begin) / 4;
+        sp.nl = nl;
+        sp.facS = p.facS;
+        sp.facD = p.facD;
+        sp.facSrc = p.facSrc;
+        sp.facDst = p.facDst;
+        if(sp.groups == 0 || !lamk::f64_to_f32_planes(sp, s))
+            return false;
+        const uint64_t doneEnd = begin + sp.groups * 4;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s),
+                           "generic_copy(tail)");
+        return true;
+    }
+
     static bool launchTile(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr, const Lowered& D,
                            DeviceImage& di, const std::vector<uint8_t*>& dptr, uint64_t begin, uint64_t end,
                            cudaStream_t s)
@@ -347,11 +581,60 @@ namespace lamhost
             p.any_coop |= p.st[k].tile_bytes && !p.st[k].tma;
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
+        if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
+            return true;
+        if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
+            return true;
+        if(!p.uni && trySplit(p, begin, end, si, di, S, D, s))
+            return true;
         if(p.uni && !p.facS && !p.facD && envNum("LAMB_DIRECT", 0) != 0 && (p.ush_s != 0xFFFFFFFFu || p.ul_s == 1)
            && (p.ush_d != 0xFFFFFFFFu || p.ul_d == 1))
         {
             lam_cuda_check(lamk::uniform_direct(p, end - begin, s), "uniform_direct");
             return true;
+        }
+        if(p.uni && !p.any_coop && envNum("LAMB_UNI_WARP", 1) != 0)
+        {
+            // warp-tile transpose: WT elements per warp tile, equal-size images per side
+            const uint64_t unit = lcm64(lcm64(S.shardUnit, D.shardUnit), 32);
+            uint64_t wt = static_cast<uint64_t>(envNum("LAMB_WT", 64));
+            wt = std::max<uint64_t>(unit, wt / unit * unit);
+            lamt_params q = p;
+            q.T = static_cast<uint32_t>(wt);
+            bool ok = true;
+            uint32_t imgS = 0, imgD = 0;
+            for(uint32_t k = 0; k < q.nsrc + q.ndst && ok; ++k)
+            {
+                lamt_stream& t = q.st[k];
+                const uint64_t bytes = wt / t.lanes * t.bs;
+                uint32_t& img = k < q.nsrc ? imgS : imgD;
+                if(img == 0)
+                    img = static_cast<uint32_t>(bytes);
+                ok = bytes == img && bytes % 16 == 0 && bytes <= 16384;
+                t.tile_bytes = static_cast<uint32_t>(bytes);
+                t.smem_off = (k < q.nsrc ? k : k - q.nsrc) * img;
+            }
+            const uint64_t ntw = (end - begin) / wt;
+            if(ok && ntw > 0 && ntw <= 0xFFFFFFFFull)
+            {
+                q.src_bytes = q.nsrc * imgS;
+                q.dst_bytes = q.ndst * imgD;
+                for(uint32_t f = 0; f < q.nleaves; ++f)
+                {
+                    q.uoff_s[f] = q.st[q.leaf[f].s[0].stream].smem_off + q.leaf[f].s[0].inblock;
+                    q.uoff_d[f] = q.st[q.leaf[f].d[0].stream].smem_off + q.leaf[f].d[0].inblock;
+                }
+                if(8ull * (q.src_bytes + q.dst_bytes) <= 200 * 1024)
+                {
+                    lam_cuda_check(lamk::uniform_warp(q, static_cast<uint32_t>(ntw), s), "uniform_warp");
+                    const uint64_t doneEnd = begin + ntw * wt;
+                    if(doneEnd < end)
+                        lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end,
+                                                          static_cast<uint32_t>(S.roots.size()), S.fac, D.fac, s),
+                                       "generic_copy(tail)");
+                    return true;
+                }
+            }
         }
         lam_cuda_check(lamk::tile_copy(p, pl.smem, pl.ctas, s), "tile_copy");
         const uint64_t doneEnd = begin + ntiles * p.T;

@@ -6,9 +6,9 @@
 
 namespace lamk
 {
-    cudaError_t nbody_update(const lamp_view* v, bool f64, bool exact, uint64_t n, uint64_t ib, uint64_t ie,
+    cudaError_t nbody_update(const lamp_view* v, bool f64, bool exact, bool phys, uint64_t n, uint64_t ib, uint64_t ie,
                              cudaStream_t s);
-    cudaError_t nbody_move(const lamp_view* v, bool f64, uint64_t ib, uint64_t ie, cudaStream_t s);
+    cudaError_t nbody_move(const lamp_view* v, bool f64, bool phys, uint64_t ib, uint64_t ie, cudaStream_t s);
 } // namespace lamk
 
 using namespace lamb;
@@ -32,6 +32,18 @@ namespace
         if(v->L->fac || v->L->heat)
             throw std::invalid_argument("instrumented n-body views are not supported on the device path");
         return t == F64;
+    }
+
+    // every particle leaf an aligned physical leaf: the kernels take the direct-load path
+    bool particlePhys(const lam_view* v)
+    {
+        for(size_t f = 0; f < 7; ++f)
+        {
+            const lamp_node& nd = v->L->nodes[v->L->roots[f]];
+            if(nd.kind != LAMP_PHYS || !(nd.flags & LAMP_FLAG_ALIGNED))
+                return false;
+        }
+        return true;
     }
 
     struct TempView
@@ -145,7 +157,7 @@ extern "C"
                     throw std::out_of_range("index out of range: particles [" + std::to_string(ib) + ", "
                                             + std::to_string(ie) + ")");
                 DeviceGuard g(v->device);
-                lam_cuda_check(lamk::nbody_update(v->img.hdr, f64, mode == LAM_NBODY_EXACT, n, ib, ie,
+                lam_cuda_check(lamk::nbody_update(v->img.hdr, f64, mode == LAM_NBODY_EXACT, particlePhys(v), n, ib, ie,
                                                   static_cast<cudaStream_t>(stream)),
                                "nbody_update");
             });
@@ -161,7 +173,7 @@ extern "C"
                 if(ib > ie || ie > n)
                     throw std::out_of_range("index out of range: particles");
                 DeviceGuard g(v->device);
-                lam_cuda_check(lamk::nbody_move(v->img.hdr, f64, ib, ie, static_cast<cudaStream_t>(stream)),
+                lam_cuda_check(lamk::nbody_move(v->img.hdr, f64, particlePhys(v), ib, ie, static_cast<cudaStream_t>(stream)),
                                "nbody_move");
             });
     }

@@ -1,0 +1,299 @@
+// Register-direct kernels for the computed mappings on the benchmark configs.
+//
+// K3/K4  bit packing (BitpackIntSoA / BitpackFloatSoA, computed.cpp:48-222): a thread owns
+//        32 consecutive values = `w` whole 32-bit words of the bit stream (w = field width),
+//        so words are never shared between threads (no RMW, bitpack.hpp:16-17).  Values move
+//        as 16-byte vectors; the word spans of a warp are staged in a warp-private smem slice
+//        (lane stride w words) so global stream traffic is coalesced 128-byte lines.
+//        f32 e8m10 / e5m10 use the exact integer/half fast encoders (device_common.cuh),
+//        every other (E, M) the integer-exact floatEncode restatement.
+// K5     convert-on-access + byte split (ChangeType f64->f32 then Bytesplit into plane
+//        streams, computed.cpp:363-378, 473-490): a thread owns 4 records, loads them as
+//        16-byte vectors, converts with x86 NaN rules and writes one 32-bit word per plane.
+#include "device_common.cuh"
+#include "launch.h"
+
+namespace lamk
+{
+    struct PackParams
+    {
+        unsigned long long vals;   // value stream (leaf-contiguous, 4-byte values, element 0)
+        unsigned long long bits;   // bit stream (word 0 = element 0)
+        unsigned long long begin;  // first element (multiple of 32)
+        unsigned long long groups; // groups of 32 elements
+        uint32_t w;                // field width (bits), 1..32
+        uint32_t kind;             // 0 int, 1 float
+        uint32_t sgn;              // int: sign-extend on unpack
+        uint32_t E, M;             // float format
+        uint32_t valType;          // LAM_I32/U32/F32 ... of the values
+        unsigned long long facSrc, facDst;
+        uint32_t facS, facD, leaf, nleaves;
+        uint32_t vbs, vl, vsh, vinb; // value-stream geometry: AoSoA lanes (vl % 32 == 0) or SoA (vl == 1)
+    };
+
+    __device__ __forceinline__ uint64_t val_addr(const PackParams& p, uint64_t e0)
+    {
+        if(p.vl == 1)
+            return p.vals + e0 * 4;
+        return p.vals + (e0 >> p.vsh) * p.vbs + p.vinb + (e0 & (p.vl - 1)) * 4;
+    }
+
+    __device__ __forceinline__ uint32_t encode_value(const PackParams& p, uint32_t v)
+    {
+        if(p.kind == 0)
+            return p.w >= 32 ? v : (v & ((1u << p.w) - 1u));
+        if(p.E == 8 && p.M == 10)
+            return lamd::encode_e8m10_f32(v);
+        if(p.E == 5 && p.M == 10)
+            return lamd::encode_e5m10_f32(v);
+        return static_cast<uint32_t>(lamd::float_encode(lamd::f32_to_f64_bits(v), p.E, p.M));
+    }
+
+    __device__ __forceinline__ uint32_t decode_value(const PackParams& p, uint32_t pat)
+    {
+        if(p.kind == 0)
+        {
+            if(p.sgn && p.w < 32)
+            {
+                const uint32_t s = 1u << (p.w - 1);
+                return (pat ^ s) - s;
+            }
+            return pat;
+        }
+        if(p.E == 8 && p.M == 10)
+        {
+            const uint32_t sign = (pat >> 18) << 31;
+            if((pat & 0x3FC00u) == 0x3FC00u && (pat & 0x3FFu))
+                return sign | 0x7FC00000u;
+            return sign | ((pat & 0x3FFFFu) << 13);
+        }
+        if(p.E == 5 && p.M == 10)
+        {
+            if((pat & 0x7C00u) == 0x7C00u && (pat & 0x3FFu))
+                return ((pat >> 15) << 31) | 0x7FC00000u;
+            return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
+        }
+        return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
+    }
+
+    __device__ __forceinline__ void fac_flush(const PackParams& p, unsigned long long cnt)
+    {
+        if(!(p.facS || p.facD))
+            return;
+        for(int o = 16; o > 0; o >>= 1)
+            cnt += __shfl_down_sync(0xFFFFFFFFu, cnt, o);
+        if((threadIdx.x & 31) == 0 && cnt)
+        {
+            if(p.facS)
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + p.leaf, cnt);
+            if(p.facD)
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.facDst) + p.nleaves + p.leaf, cnt);
+        }
+    }
+
+    // pack: 32 values -> w words per thread
+    __global__ void __launch_bounds__(256) k_pack32(const __grid_constant__ PackParams p)
+    {
+        extern __shared__ __align__(16) uint32_t psm[]; // 8 warps x 32 lanes x w words
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t* slice = psm + (threadIdx.x >> 5) * 32 * p.w;
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        unsigned long long cnt = 0;
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32; // whole warps iterate together
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const bool live = g < p.groups;
+            const uint64_t e0 = p.begin + g * 32;
+            if(live)
+            {
+                const uint4* src = reinterpret_cast<const uint4*>(val_addr(p, e0));
+                uint32_t v[32];
+#pragma unroll
+                for(int q = 0; q < 8; ++q)
+                {
+                    const uint4 x = __ldcs(src + q);
+                    v[4 * q] = x.x;
+                    v[4 * q + 1] = x.y;
+                    v[4 * q + 2] = x.z;
+                    v[4 * q + 3] = x.w;
+                }
+                unsigned long long acc = 0;
+                uint32_t nb = 0, k = 0;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    acc |= static_cast<unsigned long long>(encode_value(p, v[i])) << nb;
+                    nb += p.w;
+                    if(nb >= 32)
+                    {
+                        slice[lane * p.w + k++] = static_cast<uint32_t>(acc);
+                        acc >>= 32;
+                        nb -= 32;
+                    }
+                }
+                cnt += 32;
+            }
+            __syncwarp();
+            // coalesced stream write of the warp's span (32 * w words)
+            const uint64_t warpG = g - lane;
+            const uint64_t liveLanes = p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * p.w;
+            const uint32_t words = static_cast<uint32_t>(liveLanes) * p.w;
+            for(uint32_t q = lane; q < words; q += 32)
+                __stcs(dst + q, slice[q]);
+            __syncwarp();
+        }
+        fac_flush(p, cnt);
+    }
+
+    // unpack: w words -> 32 values per thread
+    __global__ void __launch_bounds__(256) k_unpack32(const __grid_constant__ PackParams p)
+    {
+        extern __shared__ __align__(16) uint32_t psm[];
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t* slice = psm + (threadIdx.x >> 5) * (32 * p.w + 1);
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        unsigned long long cnt = 0;
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32;
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const uint64_t warpG = g - lane;
+            const uint64_t liveLanes = p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0;
+            const uint32_t* srcw = reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * p.w;
+            const uint32_t words = static_cast<uint32_t>(liveLanes) * p.w;
+            for(uint32_t q = lane; q < words; q += 32)
+                slice[q] = __ldcs(srcw + q);
+            __syncwarp();
+            if(g < p.groups)
+            {
+                const uint64_t e0 = p.begin + g * 32;
+                uint32_t v[32];
+                const uint32_t* my = slice + lane * p.w;
+                unsigned long long acc = my[0];
+                uint32_t nb = 32, k = 1;
+                const uint32_t mask = p.w >= 32 ? 0xFFFFFFFFu : ((1u << p.w) - 1u);
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    if(nb < p.w)
+                    {
+                        acc |= static_cast<unsigned long long>(my[k < p.w ? k : p.w - 1]) << nb;
+                        ++k;
+                        nb += 32;
+                    }
+                    v[i] = decode_value(p, static_cast<uint32_t>(acc) & mask);
+                    acc >>= p.w;
+                    nb -= p.w;
+                }
+                uint4* dst = reinterpret_cast<uint4*>(val_addr(p, e0));
+#pragma unroll
+                for(int q = 0; q < 8; ++q)
+                    __stcs(dst + q, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                cnt += 32;
+            }
+            __syncwarp();
+        }
+        fac_flush(p, cnt);
+    }
+
+    bool pack32(const PackParams& p, bool pack, cudaStream_t s)
+    {
+        if(p.groups == 0 || p.w < 1 || p.w > 32)
+            return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t want = (p.groups + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 8;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        const size_t smem = 8 * (32 * p.w + 1) * sizeof(uint32_t);
+        if(pack)
+            k_pack32<<<grid, 256, smem, s>>>(p);
+        else
+            k_unpack32<<<grid, 256, smem, s>>>(p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess;
+    }
+
+    // ---- K5: f64 record-contiguous -> f32 -> 4 byte planes per leaf ------------------------
+    struct SplitParams
+    {
+        unsigned long long rec;           // source records (NL x f64, packed), element 0
+        unsigned long long plane[8][4];   // plane[f][k]: byte k of leaf f, element 0
+        unsigned long long begin, groups; // groups of 4 records
+        unsigned long long facSrc, facDst;
+        uint32_t nl, facS, facD;
+    };
+
+    template<int NL>
+    __global__ void __launch_bounds__(256) k_f64_to_f32_planes(const __grid_constant__ SplitParams p)
+    {
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        unsigned long long cnt = 0;
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < p.groups; g += stride)
+        {
+            const uint64_t e0 = p.begin + g * 4;
+            const uint4* src = reinterpret_cast<const uint4*>(p.rec + e0 * (NL * 8));
+            uint32_t f32[4][NL];
+#pragma unroll
+            for(int q = 0; q < 2 * NL; ++q)
+            {
+                const uint4 x = __ldcs(src + q);
+                // vector q holds doubles 2q, 2q+1 of the 4*NL record-major doubles
+                const int d0 = 2 * q, d1 = 2 * q + 1;
+                f32[d0 / NL][d0 % NL] = lamd::f64_to_f32_bits((uint64_t(x.y) << 32) | x.x);
+                f32[d1 / NL][d1 % NL] = lamd::f64_to_f32_bits((uint64_t(x.w) << 32) | x.z);
+            }
+#pragma unroll
+            for(int f = 0; f < NL; ++f)
+            {
+#pragma unroll
+                for(int k = 0; k < 4; ++k)
+                {
+                    // byte k of the 4 consecutive elements -> one 32-bit word of plane (f, k)
+                    const uint32_t w = ((f32[0][f] >> (8 * k)) & 0xFF) | (((f32[1][f] >> (8 * k)) & 0xFF) << 8)
+                        | (((f32[2][f] >> (8 * k)) & 0xFF) << 16) | (((f32[3][f] >> (8 * k)) & 0xFF) << 24);
+                    __stcs(reinterpret_cast<uint32_t*>(p.plane[f][k] + e0), w);
+                }
+            }
+            cnt += 4;
+        }
+        if(p.facS || p.facD)
+        {
+            for(int o = 16; o > 0; o >>= 1)
+                cnt += __shfl_down_sync(0xFFFFFFFFu, cnt, o);
+            if((threadIdx.x & 31) == 0 && cnt)
+                for(uint32_t f = 0; f < p.nl; ++f)
+                {
+                    if(p.facS)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + f, cnt);
+                    if(p.facD)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(p.facDst) + p.nl + f, cnt);
+                }
+        }
+    }
+
+    bool f64_to_f32_planes(const SplitParams& p, cudaStream_t s)
+    {
+        if(p.groups == 0)
+            return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t want = (p.groups + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 8;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        switch(p.nl)
+        {
+        case 1: k_f64_to_f32_planes<1><<<grid, 256, 0, s>>>(p); break;
+        case 2: k_f64_to_f32_planes<2><<<grid, 256, 0, s>>>(p); break;
+        case 3: k_f64_to_f32_planes<3><<<grid, 256, 0, s>>>(p); break;
+        case 4: k_f64_to_f32_planes<4><<<grid, 256, 0, s>>>(p); break;
+        case 5: k_f64_to_f32_planes<5><<<grid, 256, 0, s>>>(p); break;
+        case 6: k_f64_to_f32_planes<6><<<grid, 256, 0, s>>>(p); break;
+        case 7: k_f64_to_f32_planes<7><<<grid, 256, 0, s>>>(p); break;
+        case 8: k_f64_to_f32_planes<8><<<grid, 256, 0, s>>>(p); break;
+        default: return false;
+        }
+        count_launch();
+        return cudaGetLastError() == cudaSuccess;
+    }
+} // namespace lamk

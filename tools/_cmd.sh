@@ -1,3 +1,3 @@
 python -m pytest tests/test_gpu_copy.py -x -q 2>&1 | tail -3
-python tools/sweep_tile.py 16,2,256,0,2,0,0 16,3,256,0,3,0,0 16,4,256,0,4,0,0 24,2,256,0,2,0,0 24,3,256,0,3,0,0 24,4,256,0,3,0,0 36,3,256,0,3,0,0 36,2,256,0,2,0,0 48,3,256,0,3,0,0 48,2,256,0,2,0,0 16,4,128,0,4,0,0 24,3,128,0,3,0,0 32,4,256,0,4,0,0 64,2,256,0,2,0,0 > gpurun_out/sweep7.log 2>&1
-cat gpurun_out/sweep7.log
+python tools/sweep_env.py LAMB_VEC=1 LAMB_VEC=0,LAMB_UNI_WARP=0,LAMB_DIRECT=1 > gpurun_out/sweep9.log 2>&1
+cat gpurun_out/sweep9.log
