@@ -130,5 +130,16 @@ namespace lamhost
         void* slot_[kSlots]{};
         size_t slotBytes_ = 0;
         void* pinnedPtrs_ = nullptr; // per slot stream-pointer tables (pinned)
+        size_t pinnedBytes_ = 0;
+        // per-slot chunk-view images, cached per (src, dst) layout pair
+        struct Images
+        {
+            std::shared_ptr<lamb::Lowered> S, D;
+            std::unique_ptr<DeviceImage> simg[kSlots], dimg[kSlots];
+            void* sheat = nullptr;
+            void* dheat = nullptr;
+        };
+        std::vector<std::unique_ptr<Images>> cache_;
+        Images& images(const std::shared_ptr<lamb::Lowered>& S, const std::shared_ptr<lamb::Lowered>& D);
     };
 } // namespace lamhost

@@ -102,6 +102,42 @@ namespace lamhost
 
     HostPipeline::~HostPipeline() = default; // process-lifetime singleton
 
+    HostPipeline::Images& HostPipeline::images(const std::shared_ptr<Lowered>& S, const std::shared_ptr<Lowered>& D)
+    {
+        for(auto& c : cache_)
+            if(c->S == S && c->D == D)
+                return *c;
+        if(cache_.size() >= 16)
+        {
+            lam_cuda_check(cudaDeviceSynchronize(), "sync");
+            for(auto& c : cache_)
+            {
+                if(c->sheat)
+                    cudaFree(c->sheat);
+                if(c->dheat)
+                    cudaFree(c->dheat);
+            }
+            cache_.clear();
+        }
+        auto im = std::make_unique<Images>();
+        im->S = S;
+        im->D = D;
+        if(S->heat && S->heatTotal)
+            lam_cuda_check(cudaMalloc(&im->sheat, S->heatTotal * 8), "cudaMalloc(heat)");
+        if(D->heat && D->heatTotal)
+            lam_cuda_check(cudaMalloc(&im->dheat, D->heatTotal * 8), "cudaMalloc(heat)");
+        std::vector<uint8_t*> zeroS(S->streams.size(), nullptr), zeroD(D->streams.size(), nullptr);
+        for(int k = 0; k < kSlots; ++k)
+        {
+            im->simg[k] = std::make_unique<DeviceImage>();
+            im->dimg[k] = std::make_unique<DeviceImage>();
+            im->simg[k]->build(*S, device_, zeroS, im->sheat);
+            im->dimg[k]->build(*D, device_, zeroD, im->dheat);
+        }
+        cache_.push_back(std::move(im));
+        return *cache_.back();
+    }
+
     void HostPipeline::ensure(size_t bytes)
     {
         if(bytes <= slotBytes_)
@@ -191,48 +227,36 @@ namespace lamhost
         }
         ensure(used);
 
-        // shared heatmaps (global block indices), per-slot images
-        void* sheat = nullptr;
-        void* dheat = nullptr;
-        if(S.heat && S.heatTotal)
-        {
-            lam_cuda_check(cudaMalloc(&sheat, S.heatTotal * 8), "cudaMalloc(heat)");
-            lam_cuda_check(cudaMemset(sheat, 0, S.heatTotal * 8), "memset");
-        }
-        if(D.heat && D.heatTotal)
-        {
-            lam_cuda_check(cudaMalloc(&dheat, D.heatTotal * 8), "cudaMalloc(heat)");
-            lam_cuda_check(cudaMemset(dheat, 0, D.heatTotal * 8), "memset");
-        }
-        struct HeatFree
-        {
-            void* p;
-            ~HeatFree()
-            {
-                if(p)
-                    cudaFree(p);
-            }
-        } hf1{sheat}, hf2{dheat};
-
-        std::vector<uint8_t*> zeroS(S.streams.size(), nullptr), zeroD(D.streams.size(), nullptr);
-        DeviceImage simg[kSlots], dimg[kSlots];
+        // per-slot chunk-view images (cached per layout pair) sharing one heatmap per side
+        Images& im = images(sl.L, dl.L);
+        void* sheat = im.sheat;
+        void* dheat = im.dheat;
+        lam_cuda_check(cudaStreamSynchronize(comp_), "sync");
+        if(sheat)
+            lam_cuda_check(cudaMemsetAsync(sheat, 0, S.heatTotal * 8, comp_), "memset");
+        if(dheat)
+            lam_cuda_check(cudaMemsetAsync(dheat, 0, D.heatTotal * 8, comp_), "memset");
+        DeviceImage* simg[kSlots];
+        DeviceImage* dimg[kSlots];
         for(int k = 0; k < kSlots; ++k)
         {
-            simg[k].build(S, device_, zeroS, sheat);
-            dimg[k].build(D, device_, zeroD, dheat);
+            simg[k] = im.simg[k].get();
+            dimg[k] = im.dimg[k].get();
+            if(S.fac)
+                lam_cuda_check(cudaMemsetAsync(simg[k]->facDev, 0, 2 * leaves * 8, comp_), "memset");
+            if(D.fac)
+                lam_cuda_check(cudaMemsetAsync(dimg[k]->facDev, 0, 2 * leaves * 8, comp_), "memset");
         }
         const size_t ptrBytes = (S.streams.size() + D.streams.size()) * sizeof(uint8_t*);
-        std::vector<uint8_t*> pinned; // per slot table lives in pinned host memory
-        void* ptab = nullptr;
-        lam_cuda_check(cudaMallocHost(&ptab, std::max<size_t>(ptrBytes, 8) * kSlots), "cudaMallocHost");
-        struct HostFree
+        const size_t tabBytes = std::max<size_t>(ptrBytes, 8) * kSlots;
+        if(tabBytes > pinnedBytes_)
         {
-            void* p;
-            ~HostFree()
-            {
-                cudaFreeHost(p);
-            }
-        } hfree{ptab};
+            if(pinnedPtrs_)
+                cudaFreeHost(pinnedPtrs_);
+            lam_cuda_check(cudaMallocHost(&pinnedPtrs_, tabBytes), "cudaMallocHost");
+            pinnedBytes_ = tabBytes;
+        }
+        void* ptab = pinnedPtrs_;
 
         const uint64_t nchunks = (n + C - 1) / C;
         for(uint64_t k = 0; k < nchunks; ++k)
@@ -270,17 +294,17 @@ namespace lamhost
 
             lam_cuda_check(cudaStreamWaitEvent(comp_, evIn_[s], 0), "wait");
             if(!S.streams.empty())
-                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(simg[s].mem) + simg[s].offPtrs, tab,
+                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(simg[s]->mem) + simg[s]->offPtrs, tab,
                                                S.streams.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice, comp_),
                                "ptr table");
             if(!D.streams.empty())
-                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dimg[s].mem) + dimg[s].offPtrs,
+                lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dimg[s]->mem) + dimg[s]->offPtrs,
                                                tab + S.streams.size(), D.streams.size() * sizeof(uint8_t*),
                                                cudaMemcpyHostToDevice, comp_),
                                "ptr table");
-            if(!tileCopyPtrs(S, simg[s], tab, D, dimg[s], tab + S.streams.size(), lo, hi, comp_))
-                lam_cuda_check(lamk::generic_copy(simg[s].hdr, dimg[s].hdr, lo, hi, static_cast<uint32_t>(leaves), S.fac,
-                                                  D.fac, comp_),
+            if(!tileCopyPtrs(S, *simg[s], tab, D, *dimg[s], tab + S.streams.size(), lo, hi, comp_))
+                lam_cuda_check(lamk::generic_copy(simg[s]->hdr, dimg[s]->hdr, lo, hi, static_cast<uint32_t>(leaves),
+                                                  S.fac, D.fac, comp_),
                                "generic_copy");
             lam_cuda_check(cudaEventRecord(evDone_[s], comp_), "record");
 
@@ -299,7 +323,7 @@ namespace lamhost
         lam_cuda_check(cudaStreamSynchronize(comp_), "sync");
 
         // counters: FieldAccessCount summed over slots, then the heatmap blocks
-        auto gather = [&](const Lowered& L, DeviceImage* imgs, void* heat, uint64_t* out)
+        auto gather = [&](const Lowered& L, DeviceImage* const* imgs, void* heat, uint64_t* out)
         {
             if(!out)
                 return;
@@ -309,7 +333,7 @@ namespace lamhost
                 std::vector<uint64_t> sum(2 * leaves, 0), part(2 * leaves);
                 for(int k = 0; k < kSlots; ++k)
                 {
-                    lam_cuda_check(cudaMemcpy(part.data(), imgs[k].facDev, 2 * leaves * 8, cudaMemcpyDeviceToHost),
+                    lam_cuda_check(cudaMemcpy(part.data(), imgs[k]->facDev, 2 * leaves * 8, cudaMemcpyDeviceToHost),
                                    "counters");
                     for(size_t j = 0; j < 2 * leaves; ++j)
                         sum[j] += part[j];
