@@ -235,8 +235,42 @@ def run_c2_e2e(L, n, steps, local):
         for a, b in pairs:
             L.copy_view_host(lays[a], [x for _, x in src[a]], lays[b], [x for _, x in dst[b]], device=local)
     dt = (time.perf_counter() - t0) / steps
+    link = pcie_bandwidth(local)
+    moved = (h2d + d2h) / dt / 1e9
     return {"value": 56 * n * len(pairs) / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "s_per_step": dt, "api": "lam_copy_host (pinned host blobs)"}
+            "d2h_bytes_per_step": int(d2h), "s_per_step": dt, "api": "lam_copy_host (pinned host blobs)",
+            "host_link_GBps": link, "transfer_GBps": moved,
+            "frac_of_link": moved / link["bidirectional"] if link.get("bidirectional") else None}
+
+
+def pcie_bandwidth(local, nbytes=1 << 30):
+    """Host link roofline of the e2e number: pinned H2D, D2H and both at once (copy engines)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    t_h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    t_d2h = timed(lambda: h2.copy_(d2, non_blocking=True))
+    t_bi = timed(both)
+    return {"h2d": nbytes / t_h2d / 1e9, "d2h": nbytes / t_d2h / 1e9, "bidirectional": 2 * nbytes / t_bi / 1e9}
 
 
 def cpu_reference_c2(n, nthreads, repeats=1):

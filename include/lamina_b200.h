@@ -178,6 +178,9 @@ int lam_nbody_checksum(const lam_view* view, double* out);
 /* ---- misc ------------------------------------------------------------------------------- */
 /* Number of kernels this library launched on the calling process (all devices). */
 uint64_t lam_launch_count(void);
+/* Measurement helper (n-body roofline denominator): sustained FP32 FFMA throughput of the
+ * device over about `seconds`, in TFLOP/s (2 flops per FMA). */
+int lam_bench_fma_peak(int device, double seconds, double* tflops);
 int lam_device_sync(int device);
 
 #ifdef __cplusplus

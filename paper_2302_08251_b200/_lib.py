@@ -61,6 +61,7 @@ _SIGS = {
     "lam_nbody_move": (i32, [vp, u64, u64, vp]),
     "lam_nbody_checksum": (i32, [vp, C.POINTER(C.c_double)]),
     "lam_launch_count": (u64, []),
+    "lam_bench_fma_peak": (i32, [i32, C.c_double, C.POINTER(C.c_double)]),
     "lam_device_sync": (i32, [i32]),
 }
 

@@ -57,7 +57,10 @@ namespace lamhost
                 lam_cuda_check(lamk::blob_copy(dst.blobs[nr], src.blobs[nr], a.blobSize(nr), s), "blob_copy");
             return;
         }
-        if(tileCopy(src, dst, begin, end, s))
+        // LAMB_FORCE_GENERIC=1 (tests only): cross-check the specialised kernels against the
+        // plan interpreter on identical inputs
+        const char* fg = std::getenv("LAMB_FORCE_GENERIC");
+        if(!(fg && fg[0] == '1') && tileCopy(src, dst, begin, end, s))
             return;
         lam_cuda_check(lamk::generic_copy(src.img.hdr, dst.img.hdr, begin, end,
                                           static_cast<uint32_t>(a.schema().leafCount()), src.L->fac, dst.L->fac, s),

@@ -7,6 +7,9 @@
 #include <stddef.h>
 #include <stdint.h>
 
+// throws (mapped to LAM_ECUDA at the C ABI) on a CUDA error; defined in capi.cpp
+void lam_cuda_check(cudaError_t e, const char* what);
+
 namespace lamk
 {
     // counts every kernel this library launches (reported as gpu_launches)

@@ -91,109 +91,283 @@ namespace lamk
         }
     }
 
-    // pack: 32 values -> w words per thread
+    // Compile-time field width: the 32 values of a thread map to exactly W words, and the
+    // word boundaries fall at compile-time positions, so packing is pure shift/or chains.
+    // FMT: 0 integer, 1 f32 e8m10 (W=19), 2 f32 e5m10 (W=16), 3 any float (runtime E, M).
+    template<int FMT>
+    __device__ __forceinline__ uint32_t enc_t(const PackParams& p, uint32_t v, uint32_t mask)
+    {
+        if constexpr(FMT == 0)
+            return v & mask;
+        else if constexpr(FMT == 1)
+            return lamd::encode_e8m10_f32(v);
+        else if constexpr(FMT == 2)
+            return lamd::encode_e5m10_f32(v);
+        else
+            return static_cast<uint32_t>(lamd::float_encode(lamd::f32_to_f64_bits(v), p.E, p.M));
+    }
+
+    template<int FMT>
+    __device__ __forceinline__ uint32_t dec_t(const PackParams& p, uint32_t pat, uint32_t w)
+    {
+        if constexpr(FMT == 0)
+        {
+            if(p.sgn && w < 32)
+            {
+                const uint32_t s = 1u << (w - 1);
+                return (pat ^ s) - s;
+            }
+            return pat;
+        }
+        else if constexpr(FMT == 1)
+        {
+            const uint32_t sign = (pat >> 18) << 31;
+            if((pat & 0x3FC00u) == 0x3FC00u && (pat & 0x3FFu))
+                return sign | 0x7FC00000u;
+            return sign | ((pat & 0x3FFFFu) << 13);
+        }
+        else if constexpr(FMT == 2)
+        {
+            if((pat & 0x7C00u) == 0x7C00u && (pat & 0x3FFu))
+                return ((pat >> 15) << 31) | 0x7FC00000u;
+            return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
+        }
+        else
+            return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
+    }
+
+    // Warp smem slice: [32 lanes x VSTRIDE words of values][32 lanes x wstride words of the
+    // bit stream].  VSTRIDE = 36 keeps 16-byte value accesses conflict-free both in lane order
+    // and in coalesced (global) order; wstride = w rounded up to odd keeps the per-lane word
+    // accesses conflict-free.
+    constexpr uint32_t VSTRIDE = 36;
+    __host__ __device__ constexpr uint32_t wstride_of(uint32_t w)
+    {
+        return w | 1u;
+    }
+    __host__ __device__ constexpr uint32_t slice_words(uint32_t w)
+    {
+        return 32 * VSTRIDE + 32 * wstride_of(w) + 4;
+    }
+
+    // value side, coalesced: chunk c (16 B) of the warp's 32 x 32 values <-> lane c/8, quad c%8
+    __device__ __forceinline__ void values_g2s(const PackParams& p, uint32_t* vs, uint64_t warpE0, uint32_t lane,
+                                               uint32_t liveLanes)
+    {
+        const uint32_t chunks = liveLanes * 8;
+        for(uint32_t c = lane; c < chunks; c += 32)
+        {
+            const uint64_t e = warpE0 + 4ull * c;
+            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(val_addr(p, e)));
+            *reinterpret_cast<uint4*>(vs + (c >> 3) * VSTRIDE + (c & 7) * 4) = x;
+        }
+    }
+
+    __device__ __forceinline__ void values_s2g(const PackParams& p, const uint32_t* vs, uint64_t warpE0, uint32_t lane,
+                                               uint32_t liveLanes)
+    {
+        const uint32_t chunks = liveLanes * 8;
+        for(uint32_t c = lane; c < chunks; c += 32)
+        {
+            const uint64_t e = warpE0 + 4ull * c;
+            __stcs(reinterpret_cast<uint4*>(val_addr(p, e)),
+                   *reinterpret_cast<const uint4*>(vs + (c >> 3) * VSTRIDE + (c & 7) * 4));
+        }
+    }
+
+    // pack: 32 values -> W words per thread (W = 0: runtime width p.w)
+    template<int W, int FMT>
     __global__ void __launch_bounds__(256) k_pack32(const __grid_constant__ PackParams p)
     {
-        extern __shared__ __align__(16) uint32_t psm[]; // 8 warps x 32 lanes x w words
+        extern __shared__ __align__(16) uint32_t psm[];
+        const uint32_t w = W ? W : p.w;
+        const uint32_t ws = wstride_of(w);
         const uint32_t lane = threadIdx.x & 31;
-        uint32_t* slice = psm + (threadIdx.x >> 5) * 32 * p.w;
+        uint32_t* vs = psm + (threadIdx.x >> 5) * slice_words(w);
+        uint32_t* slice = vs + 32 * VSTRIDE;
+        const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32; // whole warps iterate together
         for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
         {
-            const bool live = g < p.groups;
-            const uint64_t e0 = p.begin + g * 32;
-            if(live)
+            const uint64_t warpG = g - lane;
+            const uint32_t liveLanes =
+                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            values_g2s(p, vs, p.begin + warpG * 32, lane, liveLanes);
+            __syncwarp();
+            if(g < p.groups)
             {
-                const uint4* src = reinterpret_cast<const uint4*>(val_addr(p, e0));
                 uint32_t v[32];
 #pragma unroll
                 for(int q = 0; q < 8; ++q)
                 {
-                    const uint4 x = __ldcs(src + q);
+                    const uint4 x = *reinterpret_cast<const uint4*>(vs + lane * VSTRIDE + 4 * q);
                     v[4 * q] = x.x;
                     v[4 * q + 1] = x.y;
                     v[4 * q + 2] = x.z;
                     v[4 * q + 3] = x.w;
                 }
-                unsigned long long acc = 0;
-                uint32_t nb = 0, k = 0;
-#pragma unroll
-                for(int i = 0; i < 32; ++i)
+                uint32_t* my = slice + lane * ws;
+                if constexpr(W != 0)
                 {
-                    acc |= static_cast<unsigned long long>(encode_value(p, v[i])) << nb;
-                    nb += p.w;
-                    if(nb >= 32)
+                    // word k = bits [32k, 32k+32): values floor(32k/W) .. floor((32k+31)/W)
+#pragma unroll
+                    for(int k = 0; k < W; ++k)
                     {
-                        slice[lane * p.w + k++] = static_cast<uint32_t>(acc);
-                        acc >>= 32;
-                        nb -= 32;
+                        uint32_t word = 0;
+#pragma unroll
+                        for(int i = (32 * k) / W; i <= (32 * k + 31) / W && i < 32; ++i)
+                        {
+                            const int pos = i * W - 32 * k; // bit position of value i inside word k
+                            const uint32_t e = enc_t<FMT>(p, v[i], mask);
+                            if(pos >= 0)
+                                word |= e << pos;
+                            else
+                                word |= e >> (-pos);
+                        }
+                        my[k] = word;
+                    }
+                }
+                else
+                {
+                    unsigned long long acc = 0;
+                    uint32_t nb = 0, k = 0;
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
+                    {
+                        acc |= static_cast<unsigned long long>(enc_t<FMT>(p, v[i], mask)) << nb;
+                        nb += w;
+                        if(nb >= 32)
+                        {
+                            my[k++] = static_cast<uint32_t>(acc);
+                            acc >>= 32;
+                            nb -= 32;
+                        }
                     }
                 }
                 cnt += 32;
             }
             __syncwarp();
             // coalesced stream write of the warp's span (32 * w words)
-            const uint64_t warpG = g - lane;
-            const uint64_t liveLanes = p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0;
-            uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * p.w;
-            const uint32_t words = static_cast<uint32_t>(liveLanes) * p.w;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w;
+            const uint32_t words = liveLanes * w;
             for(uint32_t q = lane; q < words; q += 32)
-                __stcs(dst + q, slice[q]);
+                __stcs(dst + q, slice[(q / w) * ws + (q % w)]);
             __syncwarp();
         }
         fac_flush(p, cnt);
     }
 
-    // unpack: w words -> 32 values per thread
+    // unpack: W words -> 32 values per thread
+    template<int W, int FMT>
     __global__ void __launch_bounds__(256) k_unpack32(const __grid_constant__ PackParams p)
     {
         extern __shared__ __align__(16) uint32_t psm[];
+        const uint32_t w = W ? W : p.w;
+        const uint32_t ws = wstride_of(w);
         const uint32_t lane = threadIdx.x & 31;
-        uint32_t* slice = psm + (threadIdx.x >> 5) * (32 * p.w + 1);
+        uint32_t* vs = psm + (threadIdx.x >> 5) * slice_words(w);
+        uint32_t* slice = vs + 32 * VSTRIDE;
+        const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
         for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
         {
             const uint64_t warpG = g - lane;
-            const uint64_t liveLanes = p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0;
-            const uint32_t* srcw = reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * p.w;
-            const uint32_t words = static_cast<uint32_t>(liveLanes) * p.w;
+            const uint32_t liveLanes =
+                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint32_t* srcw = reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w;
+            const uint32_t words = liveLanes * w;
             for(uint32_t q = lane; q < words; q += 32)
-                slice[q] = __ldcs(srcw + q);
+                slice[(q / w) * ws + (q % w)] = __ldcs(srcw + q);
             __syncwarp();
             if(g < p.groups)
             {
-                const uint64_t e0 = p.begin + g * 32;
                 uint32_t v[32];
-                const uint32_t* my = slice + lane * p.w;
-                unsigned long long acc = my[0];
-                uint32_t nb = 32, k = 1;
-                const uint32_t mask = p.w >= 32 ? 0xFFFFFFFFu : ((1u << p.w) - 1u);
-#pragma unroll
-                for(int i = 0; i < 32; ++i)
+                const uint32_t* my = slice + lane * ws;
+                if constexpr(W != 0)
                 {
-                    if(nb < p.w)
+                    uint32_t wd[W];
+#pragma unroll
+                    for(int k = 0; k < W; ++k)
+                        wd[k] = my[k];
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
                     {
-                        acc |= static_cast<unsigned long long>(my[k < p.w ? k : p.w - 1]) << nb;
-                        ++k;
-                        nb += 32;
+                        const int bit = i * W, k = bit >> 5, sh = bit & 31;
+                        uint32_t pat = wd[k] >> sh;
+                        if(sh + W > 32)
+                            pat |= wd[k + 1] << (32 - sh);
+                        v[i] = dec_t<FMT>(p, pat & mask, w);
                     }
-                    v[i] = decode_value(p, static_cast<uint32_t>(acc) & mask);
-                    acc >>= p.w;
-                    nb -= p.w;
                 }
-                uint4* dst = reinterpret_cast<uint4*>(val_addr(p, e0));
+                else
+                {
+                    unsigned long long acc = my[0];
+                    uint32_t nb = 32, k = 1;
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
+                    {
+                        if(nb < w)
+                        {
+                            acc |= static_cast<unsigned long long>(my[k < w ? k : w - 1]) << nb;
+                            ++k;
+                            nb += 32;
+                        }
+                        v[i] = dec_t<FMT>(p, static_cast<uint32_t>(acc) & mask, w);
+                        acc >>= w;
+                        nb -= w;
+                    }
+                }
 #pragma unroll
                 for(int q = 0; q < 8; ++q)
-                    __stcs(dst + q, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                    *reinterpret_cast<uint4*>(vs + lane * VSTRIDE + 4 * q)
+                        = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                 cnt += 32;
             }
             __syncwarp();
+            values_s2g(p, vs, p.begin + warpG * 32, lane, liveLanes);
+            __syncwarp();
         }
         fac_flush(p, cnt);
+    }
+
+    template<int W, int FMT>
+    static void launch_pack(const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s)
+    {
+        // opt in to > 48 KB of dynamic shared memory once per instantiation and size
+        static size_t setPack = 0, setUnpack = 0;
+        if(pack)
+        {
+            if(setPack < smem)
+            {
+                cudaFuncSetAttribute(k_pack32<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+                setPack = smem;
+            }
+            k_pack32<W, FMT><<<grid, 256, smem, s>>>(p);
+        }
+        else
+        {
+            if(setUnpack < smem)
+            {
+                cudaFuncSetAttribute(k_unpack32<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+                setUnpack = smem;
+            }
+            k_unpack32<W, FMT><<<grid, 256, smem, s>>>(p);
+        }
+    }
+
+    template<int... Ws>
+    static bool dispatch_int(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+                             std::integer_sequence<int, Ws...>)
+    {
+        bool hit = false;
+        ((w == Ws + 1 ? (launch_pack<Ws + 1, 0>(p, pack, grid, smem, s), hit = true) : false), ...);
+        return hit;
     }
 
     bool pack32(const PackParams& p, bool pack, cudaStream_t s)
@@ -205,13 +379,18 @@ namespace lamk
         const uint64_t want = (p.groups + 255) / 256;
         const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 8;
         const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-        const size_t smem = 8 * (32 * p.w + 1) * sizeof(uint32_t);
-        if(pack)
-            k_pack32<<<grid, 256, smem, s>>>(p);
+        const size_t smem = 8 * slice_words(p.w) * sizeof(uint32_t);
+        if(p.kind == 0)
+            dispatch_int(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
+        else if(p.E == 8 && p.M == 10)
+            launch_pack<19, 1>(p, pack, grid, smem, s);
+        else if(p.E == 5 && p.M == 10)
+            launch_pack<16, 2>(p, pack, grid, smem, s);
         else
-            k_unpack32<<<grid, 256, smem, s>>>(p);
+            launch_pack<0, 3>(p, pack, grid, smem, s);
         count_launch();
-        return cudaGetLastError() == cudaSuccess;
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
     }
 
     // ---- K5: f64 record-contiguous -> f32 -> 4 byte planes per leaf ------------------------
@@ -294,6 +473,7 @@ namespace lamk
         default: return false;
         }
         count_launch();
-        return cudaGetLastError() == cudaSuccess;
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
     }
 } // namespace lamk

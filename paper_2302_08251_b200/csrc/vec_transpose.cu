@@ -221,6 +221,7 @@ namespace lamk
         else
             return false;
         count_launch();
-        return cudaGetLastError() == cudaSuccess;
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
     }
 } // namespace lamk

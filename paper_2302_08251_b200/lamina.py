@@ -363,6 +363,13 @@ def launch_count() -> int:
     return lib().lam_launch_count()
 
 
+def fp32_peak_tflops(device: int = 0, seconds: float = 1.0) -> float:
+    """Measured sustained FP32 FFMA throughput (the n-body roofline denominator)."""
+    out = C.c_double()
+    _check(lib().lam_bench_fma_peak(device, seconds, C.byref(out)))
+    return out.value
+
+
 # ---- reports (instrument.cpp:235-257) ------------------------------------------------------------
 def field_access_csv(layout: Layout, reads, writes) -> str:
     rows = ["field,reads,writes,total"]
