@@ -1,3 +1,1 @@
-python -m pytest tests/test_gpu_nbody.py tests/test_gpu_copy.py -x -q 2>&1 | tail -3
-python bench.py --warmup 3 --suite > gpurun_out/bench5.json 2> gpurun_out/bench5.err; tail -3 gpurun_out/bench5.err
-python tools/summarize_bench.py gpurun_out/bench5.json
+for sh in 0 1 2 3 4 5; do echo "shape=$sh"; LAMB_NB_SHAPE=$sh python tools/nb_sweep.py 131072 auto 2>&1; done
