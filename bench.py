@@ -227,8 +227,8 @@ def run_c2_e2e(L, n, steps, local):
     pairs = [(a, b) for a in C2_LAYOUTS for b in C2_LAYOUTS]
     h2d = sum(sum(lays[a].blob_sizes) for a, b in pairs)
     d2h = sum(sum(lays[b].blob_sizes) for a, b in pairs)
-    # warm-up: one pass (allocates the pipeline slots)
-    for a, b in pairs[:6]:
+    # warm-up: one untimed pass over every pair (pipeline slots, per-pair device images)
+    for a, b in pairs:
         L.copy_view_host(lays[a], [x for _, x in src[a]], lays[b], [x for _, x in dst[b]], device=local)
     t0 = time.perf_counter()
     for _ in range(steps):

@@ -44,81 +44,93 @@ def _fill(L, view, seed):
     torch.cuda.synchronize()
 
 
-def run_suite(L, device=0, peak_gbs=6550.7):
+def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5")):
     import torch
     out = {}
     # ---- C1 ------------------------------------------------------------------------------
-    n = 1 << 20
-    a = L.View(L.Layout(R32, f"i32:[{n}]", "aos-packed"))
-    b = L.View(L.Layout(R32, f"i32:[{n}]", "soa-mb"))
-    _fill(L, a, 1)
-    ms = _time(lambda: L.copy_view(a, b))
-    out["C1_aos_to_soamb_1M"] = {"GB/s": 56 * n / ms / 1e6, "ms": ms, "note": "58.7 MB working set is L2-resident"}
-    del a, b
+    if "C1" in parts:
+        n = 1 << 20
+        a = L.View(L.Layout(R32, f"i32:[{n}]", "aos-packed"))
+        b = L.View(L.Layout(R32, f"i32:[{n}]", "soa-mb"))
+        _fill(L, a, 1)
+        ms = _time(lambda: L.copy_view(a, b))
+        out["C1_aos_to_soamb_1M"] = {"GB/s": 56 * n / ms / 1e6, "ms": ms, "note": "58.7 MB working set is L2-resident"}
+        del a, b
     # ---- C3 ------------------------------------------------------------------------------
-    n = 1 << 28
-    c3 = {}
-    src = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
-    _fill(L, src, 3)
-    back = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
-    for bits in (3, 7, 12, 16, 24, 31):
-        pk = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", f"bitpack-int:{bits}"))
-        byt = (4 + bits / 8) * n
-        msp = _time(lambda: L.copy_view(src, pk), reps=3)
-        msu = _time(lambda: L.copy_view(pk, back), reps=3)
-        c3[f"int{bits}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
-                            "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
-        del pk
-    del src, back
-    fsrc = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
-    _fill(L, fsrc, 4)
-    fback = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
-    for e, m in ((8, 10), (5, 10)):
-        pk = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", f"bitpack-float:{e},{m}"))
-        byt = (4 + (1 + e + m) / 8) * n
-        msp = _time(lambda: L.copy_view(fsrc, pk), reps=3)
-        msu = _time(lambda: L.copy_view(pk, fback), reps=3)
-        c3[f"e{e}m{m}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
-                           "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
-        del pk
-    del fsrc, fback
-    out["C3_bitpack_2^28"] = c3
+    if "C3" in parts:
+        n = 1 << 28
+        c3 = {}
+        src = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
+        _fill(L, src, 3)
+        back = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", "soa-mb"))
+        for bits in (3, 7, 12, 16, 24, 31):
+            pk = L.View(L.Layout("Record{v:u32}", f"i32:[{n}]", f"bitpack-int:{bits}"))
+            byt = (4 + bits / 8) * n
+            msp = _time(lambda: L.copy_view(src, pk), reps=3)
+            msu = _time(lambda: L.copy_view(pk, back), reps=3)
+            c3[f"int{bits}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
+                                "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
+            del pk
+        del src, back
+        fsrc = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
+        _fill(L, fsrc, 4)
+        fback = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", "soa-mb"))
+        for e, m in ((8, 10), (5, 10)):
+            pk = L.View(L.Layout("Record{v:f32}", f"i32:[{n}]", f"bitpack-float:{e},{m}"))
+            byt = (4 + (1 + e + m) / 8) * n
+            msp = _time(lambda: L.copy_view(fsrc, pk), reps=3)
+            msu = _time(lambda: L.copy_view(pk, fback), reps=3)
+            c3[f"e{e}m{m}"] = {"pack_GB/s": byt / msp / 1e6, "unpack_GB/s": byt / msu / 1e6,
+                               "pack_frac": byt / msp / 1e6 / peak_gbs, "unpack_frac": byt / msu / 1e6 / peak_gbs}
+            del pk
+        del fsrc, fback
+        out["C3_bitpack_2^28"] = c3
     # ---- C4 ------------------------------------------------------------------------------
-    n = 128 * 1024
-    from bench import ClockSampler
-    props = torch.cuda.get_device_properties(device)
-    nominal = 2 * 128 * props.multi_processor_count * 1.965e9 / 1e12  # TFLOP/s at max SM clock
-    with ClockSampler(device) as clk_peak:
-        measured = L.fp32_peak_tflops(device, 2.0)  # sustained FFMA chains, same power regime
-    c4 = {}
-    with ClockSampler(device) as clk:
-        for lay in ("aos-packed", "soa-mb", "aosoa:8", "aosoa:32"):
-            v = L.View(L.Layout(R32, f"i64:[{n}]", lay))
-            v.nbody_init(42)
-            row = {}
-            for mode, name in ((1, "fast"), (0, "exact")):
-                ms = _time(lambda: v.nbody_update(mode), reps=5, warm=2)
-                ips = n * n / (ms * 1e-3)
-                row[name] = {"ms_per_update": ms, "interactions/s": ips, "TFLOP/s@20": ips * 20 / 1e12,
-                             "frac_measured_fp32_peak": ips * 20 / 1e12 / measured,
-                             "frac_nominal_fp32_peak": ips * 20 / 1e12 / nominal}
-            row["move_ms"] = _time(lambda: v.nbody_move(), reps=3)
-            c4[lay] = row
-            del v
-    out["C4_nbody_128K_f32"] = dict(
-        c4, fp32_peak_measured_tflops=measured, fp32_peak_nominal_tflops=nominal,
-        clocks_during_peak=clk_peak.summary(), clocks_during_nbody=clk.summary(),
-        peak_note="measured: lam_bench_fma_peak (independent FFMA chains, 2 s sustained); "
-                  "nominal: 2 x 128 lanes x SMs x 1.965 GHz; flop convention 20 per interaction")
+    if "C4" in parts:
+        n = 128 * 1024
+        from bench import ClockSampler
+        props = torch.cuda.get_device_properties(device)
+        nominal = 2 * 128 * props.multi_processor_count * 1.965e9 / 1e12  # TFLOP/s at max SM clock
+        with ClockSampler(device) as clk_peak:
+            measured = L.fp32_peak_tflops(device, 2.0)  # sustained FFMA chains, same power regime
+        c4 = {}
+        with ClockSampler(device) as clk:
+            for lay in ("aos-packed", "soa-mb", "aosoa:8", "aosoa:32"):
+                v = L.View(L.Layout(R32, f"i64:[{n}]", lay))
+                v.nbody_init(42)
+                row = {}
+                for mode, name in ((1, "fast"), (0, "exact")):
+                    ms = _time(lambda: v.nbody_update(mode), reps=5, warm=2)
+                    ips = n * n / (ms * 1e-3)
+                    row[name] = {"ms_per_update": ms, "interactions/s": ips, "TFLOP/s@20": ips * 20 / 1e12,
+                                 "frac_measured_fp32_peak": ips * 20 / 1e12 / measured,
+                                 "frac_nominal_fp32_peak": ips * 20 / 1e12 / nominal}
+                row["move_ms"] = _time(lambda: v.nbody_move(), reps=3)
+                c4[lay] = row
+                del v
+        out["C4_nbody_128K_f32"] = dict(
+            c4, fp32_peak_measured_tflops=measured, fp32_peak_nominal_tflops=nominal,
+            clocks_during_peak=clk_peak.summary(), clocks_during_nbody=clk.summary(),
+            peak_note="measured: lam_bench_fma_peak (independent FFMA chains, 2 s sustained); "
+                      "nominal: 2 x 128 lanes x SMs x 1.965 GHz; flop convention 20 per interaction")
     # ---- C5 ------------------------------------------------------------------------------
-    n = 125_000_000
-    src = L.View(L.Layout(R64, f"i32:[{n}]", "aos-packed"))
-    _fill(L, src, 5)
-    dst = L.View(L.Layout(R64, f"i32:[{n}]", "changetype:f64=f32:bytesplit:soa-mb", wrap=1))
-    ms = _time(lambda: L.copy_view(src, dst), reps=3)
-    r, w = dst.counters()
-    out["C5_shard_125M_R64_to_FAC_changetype_bytesplit"] = {
-        "GB/s": 84 * n / ms / 1e6, "frac": 84 * n / ms / 1e6 / peak_gbs, "ms": ms,
-        "writes_per_leaf_after_runs": [int(x) for x in w]}
-    del src, dst
+    if "C5" in parts:
+        n = 125_000_000
+        src = L.View(L.Layout(R64, f"i32:[{n}]", "aos-packed"))
+        _fill(L, src, 5)
+        dst = L.View(L.Layout(R64, f"i32:[{n}]", "changetype:f64=f32:bytesplit:soa-mb", wrap=1))
+        ms = _time(lambda: L.copy_view(src, dst), reps=3)
+        r, w = dst.counters()
+        out["C5_shard_125M_R64_to_FAC_changetype_bytesplit"] = {
+            "GB/s": 84 * n / ms / 1e6, "frac": 84 * n / ms / 1e6 / peak_gbs, "ms": ms,
+            "writes_per_leaf_after_runs": [int(x) for x in w]}
+        del src, dst
     return out
+
+
+if __name__ == "__main__":
+    import json
+    import sys
+    sys.path.insert(0, ".")
+    from paper_2302_08251_b200 import lamina
+    print(json.dumps(run_suite(lamina, 0, parts=tuple(sys.argv[1:]) or ("C1", "C3", "C4", "C5")), indent=1))

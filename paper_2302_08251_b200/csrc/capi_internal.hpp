@@ -126,7 +126,9 @@ namespace lamhost
         int device_;
         static constexpr int kSlots = 3;
         cudaStream_t h2d_ = nullptr, comp_ = nullptr, d2h_ = nullptr;
+        cudaStream_t h2dB_ = nullptr, d2hB_ = nullptr; // second copy queue per direction
         cudaEvent_t evIn_[kSlots]{}, evDone_[kSlots]{}, evFree_[kSlots]{};
+        cudaEvent_t evInB_[kSlots]{}, evFreeB_[kSlots]{};
         void* slot_[kSlots]{};
         size_t slotBytes_ = 0;
         void* pinnedPtrs_ = nullptr; // per slot stream-pointer tables (pinned)

@@ -12,6 +12,7 @@
 // heatmap blocks and counters stay exact.
 #include "capi_internal.hpp"
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -75,7 +76,38 @@ namespace lamhost
                 && b.isFullyPhysical();
         }
 
-        constexpr uint64_t kSlotTarget = uint64_t{192} << 20; // bytes of src+dst per chunk
+        // bytes of src+dst per chunk (LAMB_PIPE_MB overrides, for link experiments)
+        // copy queues per direction (LAMB_PIPE_CE=2: stream regions alternate over two
+        // queues, so consecutive DMA transfers overlap their start-up)
+        int copyQueues()
+        {
+            static const int v = []
+            {
+                const char* e = getenv("LAMB_PIPE_CE");
+                return e && atoi(e) == 2 ? 2 : 1;
+            }();
+            return v;
+        }
+
+        // bytes of the last chunk's region that the copy does not write (partial AoSoA block,
+        // partial final bit-stream word): only then must the host's bytes be pre-uploaded
+        bool tailHole(const lamp_stream& st, uint64_t n)
+        {
+            if(st.kind == LAMS_BITS)
+                return (n * st.block_stride) % 32 != 0;
+            return st.lanes > 1 && n % st.lanes != 0;
+        }
+
+        uint64_t slotTarget()
+        {
+            static const uint64_t v = []
+            {
+                const char* e = getenv("LAMB_PIPE_MB");
+                const long mb = e ? atol(e) : 0;
+                return mb > 0 ? static_cast<uint64_t>(mb) << 20 : uint64_t{192} << 20;
+            }();
+            return v;
+        }
     } // namespace
 
     HostPipeline& HostPipeline::get(int device)
@@ -92,11 +124,15 @@ namespace lamhost
         lam_cuda_check(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "stream");
         lam_cuda_check(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking), "stream");
         lam_cuda_check(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "stream");
+        lam_cuda_check(cudaStreamCreateWithFlags(&h2dB_, cudaStreamNonBlocking), "stream");
+        lam_cuda_check(cudaStreamCreateWithFlags(&d2hB_, cudaStreamNonBlocking), "stream");
         for(int k = 0; k < kSlots; ++k)
         {
             lam_cuda_check(cudaEventCreateWithFlags(&evIn_[k], cudaEventDisableTiming), "event");
             lam_cuda_check(cudaEventCreateWithFlags(&evDone_[k], cudaEventDisableTiming), "event");
             lam_cuda_check(cudaEventCreateWithFlags(&evFree_[k], cudaEventDisableTiming), "event");
+            lam_cuda_check(cudaEventCreateWithFlags(&evInB_[k], cudaEventDisableTiming), "event");
+            lam_cuda_check(cudaEventCreateWithFlags(&evFreeB_[k], cudaEventDisableTiming), "event");
         }
     }
 
@@ -107,7 +143,7 @@ namespace lamhost
         for(auto& c : cache_)
             if(c->S == S && c->D == D)
                 return *c;
-        if(cache_.size() >= 16)
+        if(cache_.size() >= 64)
         {
             lam_cuda_check(cudaDeviceSynchronize(), "sync");
             for(auto& c : cache_)
@@ -168,7 +204,7 @@ namespace lamhost
         // ---- copyView fast path: blob bytes streamed through the device blob copy ----------
         if(sameLayout(a, b))
         {
-            const uint64_t cb = (kSlotTarget / 2) & ~uint64_t{15};
+            const uint64_t cb = (slotTarget() / 2) & ~uint64_t{15};
             ensure(2 * cb);
             int k = 0;
             for(size_t nr = 0; nr < a.blobCount(); ++nr)
@@ -207,7 +243,16 @@ namespace lamhost
             bpe += st.kind == LAMS_BITS ? st.block_stride / 8.0 : double(st.block_stride) / st.lanes;
         for(const auto& st : D.streams)
             bpe += st.kind == LAMS_BITS ? st.block_stride / 8.0 : double(st.block_stride) / st.lanes;
-        uint64_t C = bpe > 0 ? static_cast<uint64_t>(kSlotTarget / bpe) : n;
+        uint64_t C = bpe > 0 ? static_cast<uint64_t>(slotTarget() / bpe) : n;
+        // chunk boundaries on a multiple of 4096 elements too (when that keeps >= 2 chunks): every
+        // stream region then starts on a host page boundary, which the DMA engines need
+        // to run at full link rate
+        {
+            const char* e = getenv("LAMB_PIPE_PAGEALIGN");
+            const uint64_t pageUnit = unit / gcd64(unit, 4096) * 4096;
+            if((!e || atoi(e) != 0) && C >= 2 * pageUnit)
+                C = C / pageUnit * pageUnit;
+        }
         C = std::max<uint64_t>(unit, C / unit * unit);
         if(C > n)
             C = (n + unit - 1) / unit * unit;
@@ -269,7 +314,17 @@ namespace lamhost
             uint8_t* slot = static_cast<uint8_t*>(slot_[s]);
             auto* tab = reinterpret_cast<uint8_t**>(static_cast<uint8_t*>(ptab) + s * std::max<size_t>(ptrBytes, 8));
 
+            const int nq = copyQueues();
+            cudaStream_t hq[2] = {h2d_, h2dB_};
+            int qi = 0;
             lam_cuda_check(cudaStreamWaitEvent(h2d_, evFree_[s], 0), "wait");
+            if(nq == 2)
+                lam_cuda_check(cudaStreamWaitEvent(h2dB_, evFree_[s], 0), "wait");
+            auto up = [&](void* dev, const void* host, uint64_t bytes)
+            {
+                lam_cuda_check(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, hq[qi]), "h2d");
+                qi = (qi + 1) % nq;
+            };
             for(size_t t = 0; t < S.streams.size(); ++t)
             {
                 const auto& st = S.streams[t];
@@ -277,8 +332,7 @@ namespace lamhost
                 uint8_t* dev = slot + soff[t] + (r.lo & 15);
                 tab[t] = dev - (r.lo - st.base0);
                 if(r.hi > r.lo)
-                    lam_cuda_check(cudaMemcpyAsync(dev, static_cast<const uint8_t*>(sb[st.nr]) + r.lo, r.hi - r.lo,
-                                                   cudaMemcpyHostToDevice, h2d_), "h2d");
+                    up(dev, static_cast<const uint8_t*>(sb[st.nr]) + r.lo, r.hi - r.lo);
             }
             for(size_t t = 0; t < D.streams.size(); ++t)
             {
@@ -286,36 +340,55 @@ namespace lamhost
                 const Region r = regionOf(st, lo, hi, b.blobSize(st.nr));
                 uint8_t* dev = slot + doff[t] + (r.lo & 15);
                 tab[S.streams.size() + t] = dev - (r.lo - st.base0);
-                if((!st.holefree || last) && r.hi > r.lo)
-                    lam_cuda_check(cudaMemcpyAsync(dev, static_cast<const uint8_t*>(db[st.nr]) + r.lo, r.hi - r.lo,
-                                                   cudaMemcpyHostToDevice, h2d_), "h2d");
+                if((!st.holefree || (last && tailHole(st, n))) && r.hi > r.lo)
+                    up(dev, static_cast<const uint8_t*>(db[st.nr]) + r.lo, r.hi - r.lo);
             }
-            lam_cuda_check(cudaEventRecord(evIn_[s], h2d_), "record");
-
-            lam_cuda_check(cudaStreamWaitEvent(comp_, evIn_[s], 0), "wait");
+            // the chunk views' stream-pointer tables ride on the h2d stream too: a small copy
+            // queued on the compute stream would wait behind the next chunk's bulk H2D on the
+            // copy engine and serialise the pipeline
             if(!S.streams.empty())
                 lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(simg[s]->mem) + simg[s]->offPtrs, tab,
-                                               S.streams.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice, comp_),
+                                               S.streams.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice, h2d_),
                                "ptr table");
             if(!D.streams.empty())
                 lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dimg[s]->mem) + dimg[s]->offPtrs,
                                                tab + S.streams.size(), D.streams.size() * sizeof(uint8_t*),
-                                               cudaMemcpyHostToDevice, comp_),
+                                               cudaMemcpyHostToDevice, h2d_),
                                "ptr table");
+            if(nq == 2)
+            {
+                lam_cuda_check(cudaEventRecord(evInB_[s], h2dB_), "record");
+                lam_cuda_check(cudaStreamWaitEvent(h2d_, evInB_[s], 0), "wait");
+            }
+            lam_cuda_check(cudaEventRecord(evIn_[s], h2d_), "record");
+
+            lam_cuda_check(cudaStreamWaitEvent(comp_, evIn_[s], 0), "wait");
             if(!tileCopyPtrs(S, *simg[s], tab, D, *dimg[s], tab + S.streams.size(), lo, hi, comp_))
                 lam_cuda_check(lamk::generic_copy(simg[s]->hdr, dimg[s]->hdr, lo, hi, static_cast<uint32_t>(leaves),
                                                   S.fac, D.fac, comp_),
                                "generic_copy");
             lam_cuda_check(cudaEventRecord(evDone_[s], comp_), "record");
 
+            cudaStream_t dq[2] = {d2h_, d2hB_};
             lam_cuda_check(cudaStreamWaitEvent(d2h_, evDone_[s], 0), "wait");
+            if(nq == 2)
+                lam_cuda_check(cudaStreamWaitEvent(d2hB_, evDone_[s], 0), "wait");
+            qi = 0;
             for(size_t t = 0; t < D.streams.size(); ++t)
             {
                 const auto& st = D.streams[t];
                 const Region r = regionOf(st, lo, hi, b.blobSize(st.nr));
                 if(r.hi > r.lo)
+                {
                     lam_cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(db[st.nr]) + r.lo, slot + doff[t] + (r.lo & 15),
-                                                   r.hi - r.lo, cudaMemcpyDeviceToHost, d2h_), "d2h");
+                                                   r.hi - r.lo, cudaMemcpyDeviceToHost, dq[qi]), "d2h");
+                    qi = (qi + 1) % nq;
+                }
+            }
+            if(nq == 2)
+            {
+                lam_cuda_check(cudaEventRecord(evFreeB_[s], d2hB_), "record");
+                lam_cuda_check(cudaStreamWaitEvent(d2h_, evFreeB_[s], 0), "wait");
             }
             lam_cuda_check(cudaEventRecord(evFree_[s], d2h_), "record");
         }

@@ -154,6 +154,22 @@ namespace lamk
     __device__ __forceinline__ void values_g2s(const PackParams& p, uint32_t* vs, uint64_t warpE0, uint32_t lane,
                                                uint32_t liveLanes)
     {
+        if(liveLanes == 32)
+        {
+            // full warp: all 8 loads in flight before the first shared-memory store (4 KB per
+            // warp outstanding; a load->store loop would expose the HBM latency 8 times)
+            uint4 x[8];
+#pragma unroll
+            for(int k = 0; k < 8; ++k)
+                x[k] = __ldcs(reinterpret_cast<const uint4*>(val_addr(p, warpE0 + 4ull * (lane + 32 * k))));
+#pragma unroll
+            for(int k = 0; k < 8; ++k)
+            {
+                const uint32_t c = lane + 32 * k;
+                *reinterpret_cast<uint4*>(vs + (c >> 3) * VSTRIDE + (c & 7) * 4) = x[k];
+            }
+            return;
+        }
         const uint32_t chunks = liveLanes * 8;
         for(uint32_t c = lane; c < chunks; c += 32)
         {
@@ -166,6 +182,17 @@ namespace lamk
     __device__ __forceinline__ void values_s2g(const PackParams& p, const uint32_t* vs, uint64_t warpE0, uint32_t lane,
                                                uint32_t liveLanes)
     {
+        if(liveLanes == 32)
+        {
+#pragma unroll
+            for(int k = 0; k < 8; ++k)
+            {
+                const uint32_t c = lane + 32 * k;
+                __stcs(reinterpret_cast<uint4*>(val_addr(p, warpE0 + 4ull * c)),
+                       *reinterpret_cast<const uint4*>(vs + (c >> 3) * VSTRIDE + (c & 7) * 4));
+            }
+            return;
+        }
         const uint32_t chunks = liveLanes * 8;
         for(uint32_t c = lane; c < chunks; c += 32)
         {
@@ -211,6 +238,10 @@ namespace lamk
                 uint32_t* my = slice + lane * ws;
                 if constexpr(W != 0)
                 {
+                    // encode once per value (a value can straddle two words)
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
+                        v[i] = enc_t<FMT>(p, v[i], mask);
                     // word k = bits [32k, 32k+32): values floor(32k/W) .. floor((32k+31)/W)
 #pragma unroll
                     for(int k = 0; k < W; ++k)
@@ -220,7 +251,7 @@ namespace lamk
                         for(int i = (32 * k) / W; i <= (32 * k + 31) / W && i < 32; ++i)
                         {
                             const int pos = i * W - 32 * k; // bit position of value i inside word k
-                            const uint32_t e = enc_t<FMT>(p, v[i], mask);
+                            const uint32_t e = v[i];
                             if(pos >= 0)
                                 word |= e << pos;
                             else
@@ -252,8 +283,18 @@ namespace lamk
             // coalesced stream write of the warp's span (32 * w words)
             uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w;
             const uint32_t words = liveLanes * w;
-            for(uint32_t q = lane; q < words; q += 32)
-                __stcs(dst + q, slice[(q / w) * ws + (q % w)]);
+            if(W != 0 && liveLanes == 32)
+            {
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t q = lane + 32 * k;
+                    __stcs(dst + q, slice[(q / w) * ws + (q % w)]);
+                }
+            }
+            else
+                for(uint32_t q = lane; q < words; q += 32)
+                    __stcs(dst + q, slice[(q / w) * ws + (q % w)]);
             __syncwarp();
         }
         fac_flush(p, cnt);
@@ -280,8 +321,23 @@ namespace lamk
                 static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
             const uint32_t* srcw = reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w;
             const uint32_t words = liveLanes * w;
-            for(uint32_t q = lane; q < words; q += 32)
-                slice[(q / w) * ws + (q % w)] = __ldcs(srcw + q);
+            if(W != 0 && liveLanes == 32)
+            {
+                // full warp: the W coalesced word loads are all in flight before any smem store
+                uint32_t t[W ? W : 1];
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                    t[k] = __ldcs(srcw + lane + 32 * k);
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t q = lane + 32 * k;
+                    slice[(q / w) * ws + (q % w)] = t[k];
+                }
+            }
+            else
+                for(uint32_t q = lane; q < words; q += 32)
+                    slice[(q / w) * ws + (q % w)] = __ldcs(srcw + q);
             __syncwarp();
             if(g < p.groups)
             {
@@ -334,6 +390,18 @@ namespace lamk
         fac_flush(p, cnt);
     }
 
+    // grid-stride kernels: never launch more CTAs than can be resident at once (a partial
+    // second wave would run a full share of the work late)
+    template<typename K>
+    static unsigned resident_grid(K kernel, unsigned want, size_t smem)
+    {
+        int dev = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem);
+        const unsigned cap = static_cast<unsigned>((occ > 0 ? occ : 1) * sm_count(dev));
+        return want < cap ? want : cap;
+    }
+
     template<int W, int FMT>
     static void launch_pack(const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s)
     {
@@ -347,7 +415,7 @@ namespace lamk
                                      static_cast<int>(smem));
                 setPack = smem;
             }
-            k_pack32<W, FMT><<<grid, 256, smem, s>>>(p);
+            k_pack32<W, FMT><<<resident_grid(k_pack32<W, FMT>, grid, smem), 256, smem, s>>>(p);
         }
         else
         {
@@ -357,7 +425,7 @@ namespace lamk
                                      static_cast<int>(smem));
                 setUnpack = smem;
             }
-            k_unpack32<W, FMT><<<grid, 256, smem, s>>>(p);
+            k_unpack32<W, FMT><<<resident_grid(k_unpack32<W, FMT>, grid, smem), 256, smem, s>>>(p);
         }
     }
 

@@ -102,7 +102,10 @@ class Layout:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().lam_layout_destroy(h)
+            try:
+                lib().lam_layout_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     @property
@@ -222,7 +225,10 @@ class View:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().lam_view_free(h)
+            try:
+                lib().lam_view_free(h)
+            except TypeError:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     @property

@@ -1,1 +1,3 @@
-for sh in 0 1 2 3 4 5; do echo "shape=$sh"; LAMB_NB_SHAPE=$sh python tools/nb_sweep.py 131072 auto 2>&1; done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python bench.py --warmup 3 --suite > gpurun_out/bench_suite.json 2> gpurun_out/bench_suite.err; echo rc=$?
+python tools/summarize_bench.py gpurun_out/bench_suite.json

@@ -6,4 +6,4 @@ from paper_2302_08251_b200 import lamina as L
 from bench_suite import run_suite
 print(json.dumps(run_suite(L,0), indent=0)[:6000])
 " 2>&1 | tail -120
-python tools/nbody_prof.py && ncu --set full --clock-control none --import-source on -k regex:k_nbody_update -s 1 -c 1 -o gpurun_out/prof_nbody python tools/nbody_prof.py > gpurun_out/ncu_nb.log 2>&1; tail -2 gpurun_out/ncu_nb.log
+python tools/nbody_prof.py && ncu --set full --clock-control none --import-source on -k regex:k_nbody -s 1 -c 1 -o gpurun_out/prof_nbody python tools/nbody_prof.py > gpurun_out/ncu_nb.log 2>&1; tail -2 gpurun_out/ncu_nb.log
