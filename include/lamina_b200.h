@@ -169,7 +169,11 @@ int lam_view_write_values(lam_view* view, const uint64_t* linear, const uint32_t
  * lam_nbody_update = updateStep   (tools/nbody/steps.hpp:13-42, kernel.hpp:15-41); updates
  *                    Vel of elements [i_begin, i_end) against ALL j in index order.
  * lam_nbody_move   = moveStep     (tools/nbody/steps.hpp:97-118) over [i_begin, i_end).
- * lam_nbody_checksum = checksumView (runner.cpp:62-72): Σ pos in double, index order. */
+ * lam_nbody_checksum = checksumView (runner.cpp:62-72): Σ pos in double, index order.
+ * On an instrumented view (FieldAccessCount and/or Heatmap) update and move also add the
+ * counts the reference runner's funnel accessor produces (runner.cpp:344-436): update reads
+ * Pos/Mass of every j once per i in the range and reads 7 / writes 3 leaves of each i; move
+ * reads Pos+Vel and writes Pos of each i.  Counts are exact (not sampled). */
 int lam_nbody_init(lam_view* view, uint64_t seed, void* stream);
 int lam_nbody_update(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_move(lam_view* view, uint64_t i_begin, uint64_t i_end, void* stream);

@@ -1142,3 +1142,71 @@ def nbody_run(n, steps, seed=42, dtype=np.float32):
 def checksum(pos):
     """checksumView: Σ x,y,z in double, index order (sequential accumulate, not pairwise)."""
     return float(np.cumsum(pos.astype(np.float64).reshape(-1))[-1]) if pos.size else 0.0
+
+
+# ---- instrumented n-body: the runner's traced counters (runner.cpp:344-436) -------------------
+NBODY_SCHEMA = {
+    False: "Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}",
+    True: "Record{Pos:Record{x:f64,y:f64,z:f64},Vel:Record{x:f64,y:f64,z:f64},Mass:f64}",
+}
+
+
+def nbody_access_multiplicity(n: int, phase: str, ib: int = 0, ie: int | None = None):
+    """Accesses per (element, leaf) of one step through the funnel accessor (steps.hpp:13-118).
+
+    update, for i in [ib, ie): read the 7 leaves of i (loadLeafSimd), read Pos.{x,y,z} and Mass
+    of every j (acc.get<>), write Vel.{x,y,z} of i (storeLeafSimd).  move, for i: read Pos and
+    Vel, write Pos.  Returns (reads[7][n], writes[7][n]) as uint64 arrays.
+    """
+    ie = n if ie is None else ie
+    own = np.zeros(n, U)
+    own[ib:ie] = 1
+    cnt = U(ie - ib)
+    reads = np.zeros((7, n), U)
+    writes = np.zeros((7, n), U)
+    if phase == "update":
+        for f in (0, 1, 2, 6):
+            reads[f] = cnt + own
+        for f in (3, 4, 5):
+            reads[f] = own
+            writes[f] = own
+    else:
+        for f in (0, 1, 2):
+            reads[f] = own
+            writes[f] = own
+        for f in (3, 4, 5):
+            reads[f] = own
+    return reads, writes
+
+
+def nbody_trace(layout: str, n: int, steps: int, f64: bool = False, gran: int = 0):
+    """fields_{update,move} and heatmap_{update,move} of `lamina-nbody --trace-fields --heatmap g`.
+
+    Counters are sums over accesses, so each phase is the per-(element, leaf) multiplicity of
+    nbody_access_multiplicity times the leaf's access ranges (Mapping::accessRanges), summed
+    over the steps.  Returns {"update": (reads[7], writes[7], blocks or None), "move": ...}.
+    """
+    base = parse_layout(layout, Schema.parse(NBODY_SCHEMA[f64]), n)
+    out = {}
+    for phase in ("update", "move"):
+        reads, writes = nbody_access_multiplicity(n, phase)
+        r = reads.sum(axis=1) * U(steps)
+        w = writes.sum(axis=1) * U(steps)
+        blocks = None
+        if gran:
+            blocks = [np.zeros((s + gran - 1) // gran, U) for s in base.blob_sizes()]
+            for f in range(7):
+                m = (reads[f] + writes[f]) * U(steps)
+                for nr, lo, hi in base.ranges(f):
+                    lo = np.asarray(lo, U)
+                    hi = np.asarray(hi, U)
+                    live = (lo < hi) & (m > 0)
+                    first = (lo[live] // U(gran)).astype(np.int64)
+                    last = ((hi[live] - U(1)) // U(gran)).astype(np.int64)
+                    wt = m[live]
+                    span = int((last - first).max()) + 1 if first.size else 0
+                    for d in range(span):
+                        k = first + d <= last
+                        np.add.at(blocks[nr], first[k] + d, wt[k])
+        out[phase] = (r, w, blocks)
+    return out

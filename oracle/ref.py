@@ -60,6 +60,7 @@ def lib():
         L.ref_f32_to_f64_array.argtypes = [P(C.c_uint32), P(u64), sz]
         L.ref_nbody.argtypes = [cp, u64, u64, i32, u64, i32, i32, P(vp), P(dbl), P(dbl), P(dbl)]
         L.ref_nbody_cli.argtypes = [cp, u64, u64, i32, u64, i32]
+        L.ref_nbody_trace.argtypes = [cp, u64, u64, i32, u64, i32, u64, cp, cp]
         _lib = L
     return _lib
 
@@ -187,3 +188,13 @@ def nbody(layout, n, steps, f64=False, seed=42, width=1, nthreads=1, with_blobs=
     _check(L.ref_nbody(layout.encode(), n, steps, 1 if f64 else 0, seed, width, nthreads,
                        _ptrs(blobs) if with_blobs else None, C.byref(cs), C.byref(us), C.byref(ms)))
     return cs.value, blobs, us.value, ms.value
+
+
+def nbody_trace(layout, n, steps, report_dir, trace=True, heat_gran=0, f64=False, seed=42, csv_path=None):
+    """The reference runner with field tracing / heatmap: report CSVs land in report_dir."""
+    import os
+    os.makedirs(report_dir, exist_ok=True)
+    rc = lib().ref_nbody_trace(layout.encode(), n, steps, 1 if f64 else 0, seed, 1 if trace else 0, heat_gran,
+                               str(report_dir).encode(), csv_path.encode() if csv_path else None)
+    if rc != 0:
+        raise RefError(5, f"ref_nbody_trace exit code {rc}")

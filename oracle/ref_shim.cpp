@@ -20,9 +20,14 @@
 #include "support/oracles.hpp"
 
 #include <chrono>
+#include <iostream>
 #include <cstring>
 #include <memory>
 #include <random>
+
+// this toolchain links libstdc++ statically into the .so; make sure the standard streams
+// the reference runner writes to are constructed before it runs
+static std::ios_base::Init g_iosInit;
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -576,6 +581,24 @@ extern "C"
         cfg.precision = f64 ? "f64" : "f32";
         cfg.seed = seed;
         cfg.simdWidth = static_cast<std::size_t>(width);
+        return nbody::runBenchmark(cfg);
+    }
+
+    // the runner with --trace-fields / --heatmap <g>: writes fields_{update,move}.csv and
+    // heatmap_{update,move}.csv into reportDir (runner.cpp:344-436)
+    int ref_nbody_trace(const char* layout, std::uint64_t n, std::uint64_t steps, int f64, std::uint64_t seed,
+                        int traceFields, std::uint64_t heatGran, const char* reportDir, const char* csvPath)
+    {
+        nbody::BenchConfig cfg;
+        cfg.layout = layout;
+        cfg.n = n;
+        cfg.steps = steps;
+        cfg.precision = f64 ? "f64" : "f32";
+        cfg.seed = seed;
+        cfg.traceFields = traceFields != 0;
+        cfg.heatmapGranularity = static_cast<std::size_t>(heatGran);
+        cfg.reportDir = reportDir;
+        cfg.csvPath = csvPath ? csvPath : "";
         return nbody::runBenchmark(cfg);
     }
 }

@@ -290,6 +290,7 @@ namespace lamd
         unsigned long long* heat;
         const uint64_t* heatOff;
         uint64_t gran;
+        unsigned long long heatMul; // accesses one touch stands for (1 except in n-body accounting)
     };
 
     LAM_DEV ViewCtx make_ctx(const lamp_view* v)
@@ -301,6 +302,7 @@ namespace lamd
         c.heat = v->heat ? v->heat_counters : nullptr;
         c.heatOff = v->heat_offset;
         c.gran = v->heat_gran;
+        c.heatMul = 1;
         return c;
     }
 
@@ -328,7 +330,7 @@ namespace lamd
             return;
         const uint64_t first = begin / v.gran, last = (end - 1) / v.gran;
         for(uint64_t b = first; b <= last; ++b)
-            atomicAdd(&v.heat[v.heatOff[nr] + b], 1ull);
+            atomicAdd(&v.heat[v.heatOff[nr] + b], v.heatMul);
     }
 
     template<int D>

@@ -9,6 +9,7 @@ namespace lamk
     cudaError_t nbody_update(const lamp_view* v, bool f64, bool exact, bool phys, uint64_t n, uint64_t ib, uint64_t ie,
                              cudaStream_t s);
     cudaError_t nbody_move(const lamp_view* v, bool f64, bool phys, uint64_t ib, uint64_t ie, cudaStream_t s);
+    cudaError_t nbody_account(const lamp_view* v, bool move, uint64_t n, uint64_t ib, uint64_t ie, cudaStream_t s);
 } // namespace lamk
 
 using namespace lamb;
@@ -29,8 +30,6 @@ namespace
         for(size_t f = 1; f < 7; ++f)
             if(s.leaves()[f].type != t)
                 throw std::invalid_argument("type mismatch: n-body leaves must share one float type");
-        if(v->L->fac || v->L->heat)
-            throw std::invalid_argument("instrumented n-body views are not supported on the device path");
         return t == F64;
     }
 
@@ -160,6 +159,9 @@ extern "C"
                 lam_cuda_check(lamk::nbody_update(v->img.hdr, f64, mode == LAM_NBODY_EXACT, particlePhys(v), n, ib, ie,
                                                   static_cast<cudaStream_t>(stream)),
                                "nbody_update");
+                if(v->L->fac || v->L->heat)
+                    lam_cuda_check(lamk::nbody_account(v->img.hdr, false, n, ib, ie, static_cast<cudaStream_t>(stream)),
+                                   "nbody_account");
             });
     }
 
@@ -175,6 +177,9 @@ extern "C"
                 DeviceGuard g(v->device);
                 lam_cuda_check(lamk::nbody_move(v->img.hdr, f64, particlePhys(v), ib, ie, static_cast<cudaStream_t>(stream)),
                                "nbody_move");
+                if(v->L->fac || v->L->heat)
+                    lam_cuda_check(lamk::nbody_account(v->img.hdr, true, n, ib, ie, static_cast<cudaStream_t>(stream)),
+                                   "nbody_account");
             });
     }
 

@@ -84,3 +84,53 @@ def test_sharded_update_equals_whole():
         b.nbody_update(0, lo, hi)
     for x, y in zip(a.download_all(), b.download_all()):
         assert np.array_equal(x, y)
+
+
+# ---- instrumented n-body: the device runner vs the reference runner's reports ------------------
+TRACE_DIR = os.path.join(ROOT, "tests", "golden", "nbody_trace")
+
+
+def _trace_cases():
+    with open(os.path.join(TRACE_DIR, "index.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _trace_cases(), ids=lambda c: c["dir"])
+def test_instrumented_runner_matches_reference_reports(case, tmp_path, capsys):
+    from paper_2302_08251_b200 import nbody
+    cfg = nbody.BenchConfig(layout=case["layout"], n=case["n"], steps=case["steps"],
+                            precision="f64" if case["f64"] else "f32", seed=42, trace_fields=case["trace"],
+                            heatmap_granularity=case["gran"], report_dir=str(tmp_path))
+    assert nbody.run_benchmark(cfg) == 0
+    out = capsys.readouterr().out.strip().split("\n")
+    d = os.path.join(TRACE_DIR, case["dir"])
+    with open(os.path.join(d, "stdout.csv")) as f:
+        want = f.read().strip().split("\n")
+    # same header, same layout/phase/width, same checksum text (exact mode is bit-identical)
+    assert out[0] == want[0]
+    for a, b in zip(out[1:], want[1:]):
+        ra, rb = a.split(","), b.split(",")
+        assert ra[:3] == rb[:3] and ra[-1] == rb[-1], (a, b)
+    names = (["fields_update.csv", "fields_move.csv"] if case["trace"] else []) + \
+        (["heatmap_update.csv", "heatmap_move.csv"] if case["gran"] else [])
+    for name in names:
+        with open(os.path.join(d, name)) as f, open(tmp_path / name) as g:
+            assert g.read() == f.read(), name
+
+
+def test_instrumented_sharded_update_counts():
+    """Counts of an update over two i-shards add up to the whole-range update."""
+    from paper_2302_08251_b200 import lamina as L
+    n = 96
+    lay = L.Layout(schema("f32"), f"i64:[{n}]", "aosoa:8", wrap=L.WRAP_FIELD_ACCESS_COUNT | L.WRAP_HEATMAP,
+                   granularity=16)
+    a, b = L.View(lay), L.View(lay)
+    for v in (a, b):
+        v.nbody_init(42)
+        v.reset_counters()
+    a.nbody_update(0)
+    b.nbody_update(0, 0, 40)
+    b.nbody_update(0, 40, n)
+    assert all(np.array_equal(x, y) for x, y in zip(a.counters(), b.counters()))
+    assert np.array_equal(a.heatmap(0), b.heatmap(0))
+    assert a.nbody_checksum() == b.nbody_checksum()

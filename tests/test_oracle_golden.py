@@ -69,3 +69,43 @@ def test_nbody_fixture(case):
     O.write_all(m, bl, vals)
     for k, b in enumerate(bl):
         assert np.array_equal(b, z[f"b{k}"])
+
+
+# ---- instrumented n-body reports (runner.cpp:344-436), fixtures from the reference runner ----
+TRACE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nbody_trace")
+
+
+def _trace_cases():
+    with open(os.path.join(TRACE_DIR, "index.json")) as f:
+        return json.load(f)
+
+
+def parse_fields_csv(text):
+    rows = text.strip().split("\n")[1:]
+    return [(r.split(",")[0], int(r.split(",")[1]), int(r.split(",")[2])) for r in rows]
+
+
+def parse_heatmap_csv(text):
+    blobs = []
+    for ln in text.strip().split("\n"):
+        if ln.startswith("# blob"):
+            blobs.append([])
+        elif not ln.startswith("blockIndex"):
+            blobs[-1].append(int(ln.split(",")[2]))
+    return blobs
+
+
+@pytest.mark.parametrize("case", _trace_cases(), ids=lambda c: c["dir"])
+def test_oracle_nbody_trace_matches_reference_runner(case):
+    t = O.nbody_trace(case["layout"], case["n"], case["steps"], case["f64"], case["gran"])
+    d = os.path.join(TRACE_DIR, case["dir"])
+    for phase in ("update", "move"):
+        r, w, blocks = t[phase]
+        if case["trace"]:
+            with open(os.path.join(d, f"fields_{phase}.csv")) as f:
+                rows = parse_fields_csv(f.read())
+            assert [(x[1], x[2]) for x in rows[:7]] == list(zip(r.tolist(), w.tolist()))
+            assert rows[7] == ("TOTAL", int(r.sum()), int(w.sum()))
+        if case["gran"]:
+            with open(os.path.join(d, f"heatmap_{phase}.csv")) as f:
+                assert parse_heatmap_csv(f.read()) == [b.tolist() for b in blocks]
