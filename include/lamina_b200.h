@@ -130,6 +130,17 @@ void* lam_view_blob(const lam_view* view, size_t nr);
 int lam_view_upload(lam_view* view, size_t nr, const void* host, void* stream);
 int lam_view_download(const lam_view* view, size_t nr, void* host, void* stream);
 
+/* ---- view dump / restore (core/include/lamina/view_io.hpp; core/src/view_io.cpp:28-129) ----
+ * The reference's on-disk format: <stem>.meta (schema=, extents=, extent-values=, mapping=,
+ * blobs=, blob<nr>-size=) and <stem>.blob<nr>.bin.  lam_view_dump = writeViewDump (blobs are
+ * read back from the device), lam_view_restore = readViewDump (a new layout + device view;
+ * the caller frees both), with readViewDump's error messages ("cannot read", "malformed
+ * sidecar line", "sidecar missing field", "blob count mismatch", "blob size mismatch",
+ * "blob file truncated") as LAM_ERUNTIME.  lam_layout_dump_meta returns the .meta text. */
+size_t lam_layout_dump_meta(const lam_layout* layout, char* buf, size_t cap);
+int lam_view_dump(const lam_view* view, const char* stem);
+int lam_view_restore(const char* stem, int device, void* stream, lam_layout** layout_out, lam_view** view_out);
+
 /* ---- the hot path: layout-aware copy ---------------------------------------------------
  * Replaces lamina::copyView(const View& src, View& dst)  (core/include/lamina/view.hpp:285,
  * core/src/view.cpp:168-189).  Same contract: schema and extents must be equal

@@ -48,6 +48,9 @@ _SIGS = {
     "lam_view_blob": (vp, [vp, sz]),
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
+    "lam_layout_dump_meta": (sz, [vp, cp, sz]),
+    "lam_view_dump": (i32, [vp, cp]),
+    "lam_view_restore": (i32, [cp, i32, vp, C.POINTER(vp), C.POINTER(vp)]),
     "lam_copy": (i32, [vp, vp, vp]),
     "lam_copy_range": (i32, [vp, vp, u64, u64, vp]),
     "lam_copy_host": (i32, [vp, C.POINTER(vp), vp, C.POINTER(vp), i32, C.POINTER(u64), C.POINTER(u64)]),

@@ -6,6 +6,8 @@
 #include "capi_internal.hpp"
 
 #include <cstring>
+#include <fstream>
+#include <map>
 #include <mutex>
 
 using namespace lamb;
@@ -485,6 +487,160 @@ extern "C"
                                                    static_cast<cudaStream_t>(stream)),
                                    "cudaMemcpyAsync(download)");
             });
+    }
+
+    // ---- view dump / restore (core/src/view_io.cpp:28-129) -------------------------------------
+    // Same files as lamina::writeViewDump / readViewDump: <stem>.meta (key=value sidecar) and
+    // <stem>.blob<nr>.bin (raw blob bytes), same error messages (std::runtime_error ->
+    // LAM_ERUNTIME), so dumps move between the reference and this library in both directions.
+    size_t lam_layout_dump_meta(const lam_layout* l, char* buf, size_t cap)
+    {
+        const Map& m = *l->L->map;
+        std::string t = "schema=" + m.schema().toString() + "\nextents=" + m.extents().toString() + "\nextent-values=";
+        const auto& dv = m.extents().dynamicValues();
+        for(size_t i = 0; i < dv.size(); ++i)
+            t += (i ? "," : "") + std::to_string(dv[i]);
+        t += "\nmapping=" + m.name() + "\nblobs=" + std::to_string(m.blobCount()) + "\n";
+        for(size_t nr = 0; nr < m.blobCount(); ++nr)
+            t += "blob" + std::to_string(nr) + "-size=" + std::to_string(m.blobSize(nr)) + "\n";
+        return copyOut(t, buf, cap);
+    }
+
+    int lam_view_dump(const lam_view* v, const char* stem)
+    {
+        return guard(
+            [&]
+            {
+                if(!v || !stem)
+                    throw std::invalid_argument("null argument");
+                const std::string metaPath = std::string(stem) + ".meta";
+                std::string meta(lam_layout_dump_meta(v->layout, nullptr, 0), '\0');
+                lam_layout_dump_meta(v->layout, meta.data(), meta.size() + 1);
+                {
+                    std::ofstream out(metaPath);
+                    if(!out)
+                        throw std::runtime_error("cannot write " + metaPath);
+                    out << meta;
+                    out.close();
+                    if(!out)
+                        throw std::runtime_error("cannot write " + metaPath);
+                }
+                DeviceGuard g(v->device);
+                const Map& m = *v->L->map;
+                std::vector<char> host;
+                for(size_t nr = 0; nr < m.blobCount(); ++nr)
+                {
+                    const std::string path = std::string(stem) + ".blob" + std::to_string(nr) + ".bin";
+                    host.resize(m.blobSize(nr));
+                    if(!host.empty())
+                        lam_cuda_check(cudaMemcpy(host.data(), v->blobs[nr], host.size(), cudaMemcpyDeviceToHost),
+                                       "cudaMemcpy(dump)");
+                    std::ofstream out(path, std::ios::binary);
+                    if(!out)
+                        throw std::runtime_error("cannot write " + path);
+                    out.write(host.data(), static_cast<std::streamsize>(host.size()));
+                    out.close();
+                    if(!out)
+                        throw std::runtime_error("cannot write " + path);
+                }
+            });
+    }
+
+    int lam_view_restore(const char* stem, int device, void* stream, lam_layout** layoutOut, lam_view** viewOut)
+    {
+        lam_layout* lay = nullptr;
+        lam_view* view = nullptr;
+        const int rc = guard(
+            [&]
+            {
+                if(!stem || !layoutOut || !viewOut)
+                    throw std::invalid_argument("null argument");
+                const std::string metaPath = std::string(stem) + ".meta";
+                std::ifstream meta(metaPath);
+                if(!meta)
+                    throw std::runtime_error("cannot read " + metaPath);
+                std::map<std::string, std::string> kv;
+                std::string line;
+                while(std::getline(meta, line))
+                {
+                    if(line.empty())
+                        continue;
+                    const size_t eq = line.find('=');
+                    if(eq == std::string::npos)
+                        throw std::runtime_error("malformed sidecar line: '" + line + "'");
+                    kv[line.substr(0, eq)] = line.substr(eq + 1);
+                }
+                auto field = [&](const std::string& key) -> const std::string&
+                {
+                    const auto it = kv.find(key);
+                    if(it == kv.end())
+                        throw std::runtime_error("sidecar missing field '" + key + "'");
+                    return it->second;
+                };
+                const std::string& schemaText = field("schema");
+                std::vector<uint64_t> dyn;
+                if(const std::string& vals = field("extent-values"); !vals.empty())
+                {
+                    size_t start = 0;
+                    while(true)
+                    {
+                        const size_t comma = vals.find(',', start);
+                        dyn.push_back(std::stoull(comma == std::string::npos ? vals.substr(start)
+                                                                           : vals.substr(start, comma - start)));
+                        if(comma == std::string::npos)
+                            break;
+                        start = comma + 1;
+                    }
+                }
+                const std::string& extentsText = field("extents");
+                const std::string& mappingText = field("mapping");
+                const int rc1 = lam_layout_create(schemaText.c_str(), extentsText.c_str(), dyn.data(), dyn.size(),
+                                                  mappingText.c_str(), 0, 1, &lay);
+                if(rc1 != LAM_OK)
+                    throw std::invalid_argument(g_lam_err);
+                const Map& m = *lay->L->map;
+                const size_t blobCount = std::stoull(field("blobs"));
+                if(blobCount != m.blobCount())
+                    throw std::runtime_error("blob count mismatch: sidecar says " + std::to_string(blobCount)
+                                             + ", mapping declares " + std::to_string(m.blobCount()));
+                std::vector<std::vector<char>> host(blobCount);
+                for(size_t nr = 0; nr < blobCount; ++nr)
+                {
+                    const size_t declared = std::stoull(field("blob" + std::to_string(nr) + "-size"));
+                    if(declared != m.blobSize(nr))
+                        throw std::runtime_error("blob size mismatch: blob " + std::to_string(nr) + " sidecar says "
+                                                 + std::to_string(declared) + ", mapping declares "
+                                                 + std::to_string(m.blobSize(nr)));
+                    const std::string path = std::string(stem) + ".blob" + std::to_string(nr) + ".bin";
+                    std::ifstream in(path, std::ios::binary);
+                    if(!in)
+                        throw std::runtime_error("cannot read " + path);
+                    host[nr].resize(declared);
+                    in.read(host[nr].data(), static_cast<std::streamsize>(declared));
+                    if(static_cast<size_t>(in.gcount()) != declared)
+                        throw std::runtime_error("blob file truncated: " + path);
+                }
+                if(lam_view_alloc(lay, device, stream, &view) != LAM_OK)
+                    throw CudaError(g_lam_err);
+                for(size_t nr = 0; nr < blobCount; ++nr)
+                    if(lam_view_upload(view, nr, host[nr].data(), stream) != LAM_OK)
+                        throw CudaError(g_lam_err);
+                DeviceGuard g(device);
+                lam_cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "restore sync");
+            });
+        if(rc != LAM_OK)
+        {
+            const std::string err = g_lam_err;
+            if(view)
+                lam_view_free(view);
+            if(lay)
+                lam_layout_destroy(lay);
+            g_lam_err = err;
+            return rc;
+        }
+        *layoutOut = lay;
+        *viewOut = view;
+        return LAM_OK;
     }
 
     // ---- copy -----------------------------------------------------------------------------

@@ -158,6 +158,10 @@ namespace lamb
         }
         size_t runtimeStateBytes() const;
         std::string toString() const;
+        const std::vector<uint64_t>& dynamicValues() const
+        {
+            return dynValues_;
+        }
         bool operator==(const Extents& o) const
         {
             return it_ == o.it_ && dims_ == o.dims_ && dynValues_ == o.dynValues_;

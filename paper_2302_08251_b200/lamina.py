@@ -58,7 +58,12 @@ class CudaError(LaminaError, RuntimeError):
     pass
 
 
-_ERR = {1: InvalidArgument, 2: OutOfRange, 3: IndexTypeOverflow, 4: LogicError, 5: LaminaError, 6: CudaError}
+class ReferenceRuntimeError(LaminaError, RuntimeError):
+    """std::runtime_error in the reference (e.g. readViewDump's "cannot read")."""
+
+
+_ERR = {1: InvalidArgument, 2: OutOfRange, 3: IndexTypeOverflow, 4: LogicError, 5: ReferenceRuntimeError,
+        6: CudaError}
 
 
 def _check(rc: int) -> None:
@@ -98,6 +103,18 @@ class Layout:
         self._h = h
         self.layout_text = layout
         self.dyn = tuple(dyn)
+
+    @classmethod
+    def _adopt(cls, handle: C.c_void_p) -> "Layout":
+        self = cls.__new__(cls)
+        self._h = handle
+        self.layout_text = _str(lib().lam_layout_name, handle)
+        self.dyn = ()
+        return self
+
+    def dump_meta(self) -> str:
+        """The .meta sidecar text writeViewDump writes for a view of this layout (view_io.cpp:30-44)."""
+        return _str(lib().lam_layout_dump_meta, self._h)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -235,6 +252,10 @@ class View:
     def handle(self):
         return self._h
 
+    def dump(self, stem: str) -> None:
+        """lamina::writeViewDump (view_io.cpp:28-59): <stem>.meta + <stem>.blob<nr>.bin."""
+        _check(lib().lam_view_dump(self._h, str(stem).encode()))
+
     def blob_ptr(self, nr: int) -> int:
         return lib().lam_view_blob(self._h, nr) or 0
 
@@ -317,6 +338,22 @@ class View:
         out = C.c_double()
         _check(lib().lam_nbody_checksum(self._h, C.byref(out)))
         return out.value
+
+
+def write_view_dump(view: View, stem: str) -> None:
+    """lamina::writeViewDump (core/src/view_io.cpp:28-59)."""
+    view.dump(stem)
+
+
+def read_view_dump(stem: str, device: int = 0, stream=None) -> View:
+    """lamina::readViewDump (core/src/view_io.cpp:61-129): a new device view from a dump."""
+    lh, vh = C.c_void_p(), C.c_void_p()
+    _check(lib().lam_view_restore(str(stem).encode(), device, _stream_handle(stream), C.byref(lh), C.byref(vh)))
+    v = View.__new__(View)
+    v.layout = Layout._adopt(lh)
+    v.device = device
+    v._h = vh
+    return v
 
 
 def copy_view(src: View, dst: View, stream=None) -> None:

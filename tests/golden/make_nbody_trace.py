@@ -32,13 +32,13 @@ def case_dir(layout, n, steps, f64, trace, gran):
 
 def main():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
-    exe = os.path.join(ROOT, "oracle", "_ref", "ref_nbody")
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
     shutil.rmtree(OUT, ignore_errors=True)
     index = []
     for layout, n, steps, f64, trace, gran in CASES:
         d = os.path.join(OUT, case_dir(layout, n, steps, f64, trace, gran))
         os.makedirs(d)
-        r = subprocess.run([exe, layout, str(n), str(steps), str(int(f64)), "42", str(int(trace)), str(gran), d],
+        r = subprocess.run([exe, "nbody", layout, str(n), str(steps), str(int(f64)), "42", str(int(trace)), str(gran), d],
                            check=True, capture_output=True, text=True)
         with open(os.path.join(d, "stdout.csv"), "w") as f:
             f.write(r.stdout)

@@ -115,3 +115,62 @@ def test_dynamic_extents():
 def test_golden_fixtures_present():
     idx = os.path.join(ROOT, "tests", "golden", "index.json")
     assert os.path.exists(idx)
+
+
+# ---- view dump sidecar (core/src/view_io.cpp), fixtures written by the reference ---------------
+DUMP_DIR = os.path.join(ROOT, "tests", "golden", "view_dump")
+
+
+def _dump_cases():
+    import json
+    with open(os.path.join(DUMP_DIR, "index.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _dump_cases(), ids=lambda c: c["name"])
+def test_dump_meta_matches_reference_sidecar(case):
+    from paper_2302_08251_b200 import lamina as L
+    lay = L.Layout(case["schema"], case["extents"], case["layout"], dyn=case["dyn"])
+    with open(os.path.join(DUMP_DIR, case["name"] + ".meta")) as f:
+        assert lay.dump_meta() == f.read()
+
+
+def _damaged_dump(tmp_path, edit_meta=None, truncate=None, drop_blob=False):
+    """A copy of the io_soamb fixture, damaged like test_view_io.cpp:95-140."""
+    import shutil
+    stem = tmp_path / "dump"
+    for nr in range(4):
+        shutil.copy(os.path.join(DUMP_DIR, f"io_soamb.blob{nr}.bin"), f"{stem}.blob{nr}.bin")
+    with open(os.path.join(DUMP_DIR, "io_soamb.meta")) as f:
+        meta = f.read()
+    if edit_meta:
+        meta = edit_meta(meta)
+    with open(f"{stem}.meta", "w") as f:
+        f.write(meta)
+    if truncate is not None:
+        os.truncate(f"{stem}.blob0.bin", truncate)
+    if drop_blob:
+        os.remove(f"{stem}.blob0.bin")
+    return str(stem)
+
+
+@pytest.mark.parametrize("damage,msg", [
+    (dict(truncate=8), "truncated"),
+    (dict(drop_blob=True), "cannot read"),
+    (dict(edit_meta=lambda m: m.replace("blob0-size=48", "blob0-size=16")), "blob size mismatch"),
+    (dict(edit_meta=lambda m: m.replace("blobs=4", "blobs=3")), "blob count mismatch"),
+    (dict(edit_meta=lambda m: "schema=Record{x:f64}\n"), "missing field"),
+    (dict(edit_meta=lambda m: m + "garbage\n"), "malformed sidecar line"),
+])
+def test_restore_rejects_damaged_dumps(tmp_path, damage, msg):
+    """readViewDump's checks run before any device allocation, so they are testable here."""
+    from paper_2302_08251_b200 import lamina as L
+    stem = _damaged_dump(tmp_path, **damage)
+    with pytest.raises(L.ReferenceRuntimeError, match=msg):
+        L.read_view_dump(stem)
+
+
+def test_restore_missing_dump(tmp_path):
+    from paper_2302_08251_b200 import lamina as L
+    with pytest.raises(L.ReferenceRuntimeError, match="cannot read"):
+        L.read_view_dump(str(tmp_path / "absent"))
