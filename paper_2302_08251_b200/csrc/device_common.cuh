@@ -176,13 +176,11 @@ namespace lamd
     {
         const uint32_t s = (b >> 31) << 18;
         const uint32_t a = b & 0x7FFFFFFFu;
-        if(a > 0x7F800000u)
-            return s | 0x3FE00u; // NaN: exp all ones | quiet bit
-        if(a == 0x7F800000u)
-            return s | 0x3FC00u;
         // RNE of the low 13 mantissa bits, carry propagates into the exponent;
-        // 0x7F7FF000.. round up into 0x7F800000 = Inf, which is the overflow rule
-        return s | ((a + 0xFFFu + ((a >> 13) & 1u)) >> 13);
+        // 0x7F7FF000.. round up into 0x7F800000 = Inf, which is the overflow rule, and
+        // Inf itself (low bits 0) maps to 0x3FC00 unchanged
+        const uint32_t r = (a + 0xFFFu + ((a >> 13) & 1u)) >> 13;
+        return s | (a > 0x7F800000u ? 0x3FE00u : r); // NaN: exp all ones | quiet bit
     }
 
     LAM_DEV uint32_t encode_e5m10_f32(uint32_t b)

@@ -136,8 +136,8 @@ namespace lamk
             return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
     }
 
-    // Warp smem slice: [32 lanes x VSTRIDE words of values][32 lanes x wstride words of the
-    // bit stream].  VSTRIDE = 36 keeps 16-byte value accesses conflict-free both in lane order
+    // Warp smem slice: 32 lanes x VSTRIDE words of values, aliased by 32 lanes x wstride words
+    // of the bit stream.  VSTRIDE = 36 keeps 16-byte value accesses conflict-free both in lane order
     // and in coalesced (global) order; wstride = w rounded up to odd keeps the per-lane word
     // accesses conflict-free.
     constexpr uint32_t VSTRIDE = 36;
@@ -145,9 +145,11 @@ namespace lamk
     {
         return w | 1u;
     }
+    // the word slice and the value slice alias: each kernel moves one of them into registers
+    // (with a __syncwarp) before it writes the other
     __host__ __device__ constexpr uint32_t slice_words(uint32_t w)
     {
-        return 32 * VSTRIDE + 32 * wstride_of(w) + 4;
+        return (32 * VSTRIDE > 32 * wstride_of(w) ? 32 * VSTRIDE : 32 * wstride_of(w)) + 4;
     }
 
     // value side, coalesced: chunk c (16 B) of the warp's 32 x 32 values <-> lane c/8, quad c%8
@@ -204,14 +206,14 @@ namespace lamk
 
     // pack: 32 values -> W words per thread (W = 0: runtime width p.w)
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256) k_pack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, FMT == 1 ? 4 : 3) k_pack32(const __grid_constant__ PackParams p)
     {
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
         const uint32_t lane = threadIdx.x & 31;
         uint32_t* vs = psm + (threadIdx.x >> 5) * slice_words(w);
-        uint32_t* slice = vs + 32 * VSTRIDE;
+        uint32_t* slice = vs; // aliases the value slice (see the __syncwarp before the word writes)
         const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
@@ -223,9 +225,10 @@ namespace lamk
                 static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
             values_g2s(p, vs, p.begin + warpG * 32, lane, liveLanes);
             __syncwarp();
-            if(g < p.groups)
+            const bool live = g < p.groups;
+            uint32_t v[32];
+            if(live)
             {
-                uint32_t v[32];
 #pragma unroll
                 for(int q = 0; q < 8; ++q)
                 {
@@ -235,6 +238,12 @@ namespace lamk
                     v[4 * q + 2] = x.z;
                     v[4 * q + 3] = x.w;
                 }
+            }
+            // every lane's values are in registers: the word slice may now overwrite the value
+            // slice (they alias, which halves the smem per warp and raises occupancy)
+            __syncwarp();
+            if(live)
+            {
                 uint32_t* my = slice + lane * ws;
                 if constexpr(W != 0)
                 {
@@ -302,14 +311,14 @@ namespace lamk
 
     // unpack: W words -> 32 values per thread
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256) k_unpack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, 3) k_unpack32(const __grid_constant__ PackParams p)
     {
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
         const uint32_t lane = threadIdx.x & 31;
         uint32_t* vs = psm + (threadIdx.x >> 5) * slice_words(w);
-        uint32_t* slice = vs + 32 * VSTRIDE;
+        uint32_t* slice = vs; // aliases the value slice (see the __syncwarp before the value writes)
         const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
@@ -339,9 +348,10 @@ namespace lamk
                 for(uint32_t q = lane; q < words; q += 32)
                     slice[(q / w) * ws + (q % w)] = __ldcs(srcw + q);
             __syncwarp();
-            if(g < p.groups)
+            const bool live = g < p.groups;
+            uint32_t v[32];
+            if(live)
             {
-                uint32_t v[32];
                 const uint32_t* my = slice + lane * ws;
                 if constexpr(W != 0)
                 {
@@ -377,6 +387,11 @@ namespace lamk
                         nb -= w;
                     }
                 }
+            }
+            // every lane's words are consumed: the value slice may now overwrite the word slice
+            __syncwarp();
+            if(live)
+            {
 #pragma unroll
                 for(int q = 0; q < 8; ++q)
                     *reinterpret_cast<uint4*>(vs + lane * VSTRIDE + 4 * q)
