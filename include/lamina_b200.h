@@ -126,6 +126,10 @@ int lam_view_wrap(const lam_layout* layout, int device, void* const* device_blob
 void lam_view_free(lam_view* view);
 const lam_layout* lam_view_layout(const lam_view* view);
 void* lam_view_blob(const lam_view* view, size_t nr);
+/* Device pointer to the view's lowered plan (struct lamp_view): the argument user kernels pass
+ * to lamina_b200::DeviceView (include/lamina_b200_device.cuh) to read / write the view through
+ * its mapping from their own kernels (View::read/write/load/store, view.hpp:144-181). */
+const void* lam_view_device_plan(const lam_view* view);
 /* Stream-ordered host<->device blob transfer (pinned host memory makes them async). */
 int lam_view_upload(lam_view* view, size_t nr, const void* host, void* stream);
 int lam_view_download(const lam_view* view, size_t nr, void* host, void* stream);

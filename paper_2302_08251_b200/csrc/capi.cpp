@@ -452,6 +452,11 @@ extern "C"
         return v->layout;
     }
 
+    const void* lam_view_device_plan(const lam_view* v)
+    {
+        return v ? v->img.hdr : nullptr;
+    }
+
     void* lam_view_blob(const lam_view* v, size_t nr)
     {
         return nr < v->blobs.size() ? v->blobs[nr] : nullptr;

@@ -252,6 +252,11 @@ class View:
     def handle(self):
         return self._h
 
+    @property
+    def device_plan(self) -> int:
+        """Device pointer of the lowered plan, for user kernels on include/lamina_b200_device.cuh."""
+        return lib().lam_view_device_plan(self._h) or 0
+
     def dump(self, stem: str) -> None:
         """lamina::writeViewDump (view_io.cpp:28-59): <stem>.meta + <stem>.blob<nr>.bin."""
         _check(lib().lam_view_dump(self._h, str(stem).encode()))
