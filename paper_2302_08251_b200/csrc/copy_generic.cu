@@ -8,6 +8,8 @@
 #include "device_common.cuh"
 #include "launch.h"
 
+#include <cstdlib>
+
 #include <atomic>
 
 namespace lamk
@@ -110,18 +112,22 @@ namespace lamk
     }
 
     // ---- blob copy: vectorised 16-byte path when both sides are aligned ----------------
-    __global__ void __launch_bounds__(512) k_blob_copy16(uint4* __restrict__ d, const uint4* __restrict__ s, uint64_t n16)
+    // U 16-byte loads per thread are in flight before the first store; consecutive threads
+    // touch consecutive 16-byte words, so each warp instruction moves 512 contiguous bytes.
+    template<int U>
+    __global__ void __launch_bounds__(256) k_blob_copy16(uint4* __restrict__ d, const uint4* __restrict__ s, uint64_t n16)
     {
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        for(; i + 3 * stride < n16; i += 4 * stride)
+        for(; i + (U - 1) * stride < n16; i += U * stride)
         {
-            const uint4 a = __ldcs(s + i), b = __ldcs(s + i + stride), c = __ldcs(s + i + 2 * stride),
-                        e = __ldcs(s + i + 3 * stride);
-            __stcs(d + i, a);
-            __stcs(d + i + stride, b);
-            __stcs(d + i + 2 * stride, c);
-            __stcs(d + i + 3 * stride, e);
+            uint4 x[U];
+#pragma unroll
+            for(int k = 0; k < U; ++k)
+                x[k] = __ldcs(s + i + k * stride);
+#pragma unroll
+            for(int k = 0; k < U; ++k)
+                __stcs(d + i + k * stride, x[k]);
         }
         for(; i < n16; i += stride)
             __stcs(d + i, __ldcs(s + i));
@@ -148,9 +154,22 @@ namespace lamk
             const uint64_t n16 = bytes / 16;
             if(n16)
             {
-                const uint64_t want = (n16 + 511) / 512;
-                const unsigned grid = static_cast<unsigned>(want < sms * 4ull ? want : sms * 4ull);
-                k_blob_copy16<<<grid, 512, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+                static const int U = [] { const char* e = getenv("LAMB_BLOB_U"); return e ? atoi(e) : 2; }();
+                // measured optimum at 2^26 R32 (tools/blob_sweep.py): 2 loads x 4 CTAs of 256 per SM;
+                // more bytes in flight per SM lowers the DRAM rate
+                static const unsigned per = [] { const char* e = getenv("LAMB_BLOB_CTAS"); return e ? atoi(e) : 4; }();
+                const uint64_t want = (n16 + 255) / 256;
+                const unsigned grid = static_cast<unsigned>(want < sms * uint64_t(per) ? want : sms * uint64_t(per));
+                auto* dp = static_cast<uint4*>(dst);
+                auto* sp = static_cast<const uint4*>(src);
+                if(U == 8)
+                    k_blob_copy16<8><<<grid, 256, 0, s>>>(dp, sp, n16);
+                else if(U == 2)
+                    k_blob_copy16<2><<<grid, 256, 0, s>>>(dp, sp, n16);
+                else if(U == 1)
+                    k_blob_copy16<1><<<grid, 256, 0, s>>>(dp, sp, n16);
+                else
+                    k_blob_copy16<4><<<grid, 256, 0, s>>>(dp, sp, n16);
                 count_launch();
             }
             head = n16 * 16;

@@ -13,6 +13,8 @@
 #include "launch.h"
 #include "tile.h"
 
+#include <cstdlib>
+
 namespace lamk
 {
     struct VecSide
@@ -186,7 +188,12 @@ namespace lamk
         int dev = 0;
         cudaGetDevice(&dev);
         const uint64_t want = (p.groups + 255) / 256;
-        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * 16;
+        static const uint64_t per = []
+        {
+            const char* e = getenv("LAMB_VEC_CTAS");
+            return static_cast<uint64_t>(e ? atoi(e) : 16);
+        }();
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * per;
         const unsigned grid = static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
         if(leafSize == 4)
         {

@@ -1,4 +1,3 @@
-python -m pytest tests/test_gpu_copy.py -q -x -k "pack or bit" 2>&1 | tail -1
-for r in 1 2; do python bench_suite.py C3 2>&1 | python -c "
-import json,sys; d=json.load(sys.stdin)
-print(' '.join(f\"{k}:{v['pack_frac']:.3f}/{v['unpack_frac']:.3f}\" for k,v in d['C3_bitpack_2^28'].items()))"; done
+for c in 2 3 4 6 8 16; do echo "VEC_CTAS=$c"; LAMB_VEC_CTAS=$c python bench.py --warmup 3 --steps 5 --no-e2e --no-cpu > gpurun_out/b_$c.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/b_$c.json')); p=d['per_pair_gbs']
+print(round(d['value']), round(d['roofline']['achieved']), ' '.join(str(round(v)) for k,v in p.items()))"; done
