@@ -140,6 +140,36 @@ namespace lamk
             d[i] = s[i];
     }
 
+    __global__ void k_fac_add(unsigned long long* src, unsigned long long* dst, uint32_t nl, unsigned long long cnt)
+    {
+        for(uint32_t f = threadIdx.x; f < nl; f += blockDim.x)
+        {
+            if(src)
+                src[f] += cnt;
+            if(dst)
+                dst[nl + f] += cnt;
+        }
+    }
+
+    cudaError_t fac_add(unsigned long long* srcCounters, unsigned long long* dstCounters, uint32_t nleaves,
+                        uint64_t count, cudaStream_t s)
+    {
+        k_fac_add<<<1, 64, 0, s>>>(srcCounters, dstCounters, nleaves, count);
+        count_launch();
+        return cudaGetLastError();
+    }
+
+    unsigned stream_grid(uint64_t want, const char* env, uint64_t perSm)
+    {
+        if(const char* e = getenv(env))
+            perSm = static_cast<uint64_t>(atoll(e));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t cap = perSm ? perSm * static_cast<uint64_t>(sm_count(dev)) : want;
+        const uint64_t g = want < cap ? want : cap;
+        return static_cast<unsigned>(g == 0 ? 1 : (g > 0x7FFFFFFFull ? 0x7FFFFFFFull : g));
+    }
+
     cudaError_t blob_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s)
     {
         if(bytes == 0)
@@ -155,11 +185,7 @@ namespace lamk
             if(n16)
             {
                 static const int U = [] { const char* e = getenv("LAMB_BLOB_U"); return e ? atoi(e) : 2; }();
-                // measured optimum at 2^26 R32 (tools/blob_sweep.py): 2 loads x 4 CTAs of 256 per SM;
-                // more bytes in flight per SM lowers the DRAM rate
-                static const unsigned per = [] { const char* e = getenv("LAMB_BLOB_CTAS"); return e ? atoi(e) : 4; }();
-                const uint64_t want = (n16 + 255) / 256;
-                const unsigned grid = static_cast<unsigned>(want < sms * uint64_t(per) ? want : sms * uint64_t(per));
+                const unsigned grid = stream_grid((n16 + 256 * U - 1) / (256 * U), "LAMB_BLOB_CTAS", 0);
                 auto* dp = static_cast<uint4*>(dst);
                 auto* sp = static_cast<const uint4*>(src);
                 if(U == 8)

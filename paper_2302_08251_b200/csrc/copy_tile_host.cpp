@@ -353,6 +353,19 @@ namespace lamhost
         }
     } // namespace
 
+    // FieldAccessCount under copyView (view.cpp:186-188): every element of the range reads each
+    // source leaf once and writes each destination leaf once, so the specialised kernels add
+    // the counts in closed form (one tiny launch) instead of atomics in the streaming loop
+    static void addAccessCounts(const lamt_params& p, const Lowered& S, uint64_t count, cudaStream_t s)
+    {
+        if(!(p.facS || p.facD) || count == 0)
+            return;
+        lam_cuda_check(lamk::fac_add(p.facS ? reinterpret_cast<unsigned long long*>(p.facSrc) : nullptr,
+                                     p.facD ? reinterpret_cast<unsigned long long*>(p.facDst) : nullptr,
+                                     static_cast<uint32_t>(S.roots.size()), count, s),
+                       "fac_add");
+    }
+
     // register-transpose path (vec_transpose.cu) for uniform 4/8-byte-leaf pairs whose sides are
     // leaf-contiguous in groups of V elements (SoA, AoSoA with V | L) or record-contiguous (AoS)
     static bool tryVec(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
@@ -411,14 +424,15 @@ namespace lamhost
         vp.begin = begin;
         vp.groups = (end - begin) / V;
         vp.nl = nl;
-        vp.facS = p.facS;
-        vp.facD = p.facD;
+        vp.facS = 0; // counted in closed form below (fac_add)
+        vp.facD = 0;
         vp.facSrc = p.facSrc;
         vp.facDst = p.facDst;
         if(vp.groups == 0)
             return false;
         if(!lamk::vec_transpose(vp, p.usize, s))
             return false;
+        addAccessCounts(p, S, vp.groups * V, s);
         const uint64_t doneEnd = begin + vp.groups * V;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
@@ -480,8 +494,8 @@ namespace lamhost
                 return false;
             j.begin = begin;
             j.groups = groups;
-            j.facS = p.facS;
-            j.facD = p.facD;
+            j.facS = 0; // counted in closed form below (fac_add)
+            j.facD = 0;
             j.facSrc = p.facSrc;
             j.facDst = p.facDst;
             j.leaf = f;
@@ -491,6 +505,7 @@ namespace lamhost
         for(const auto& j : jobs)
             if(!lamk::pack32(j, packDir, s))
                 throw std::runtime_error(std::string("pack32 launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+        addAccessCounts(p, S, groups * 32, s);
         const uint64_t doneEnd = begin + groups * 32;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
@@ -535,12 +550,13 @@ namespace lamhost
         sp.begin = begin;
         sp.groups = (end - begin) / 4;
         sp.nl = nl;
-        sp.facS = p.facS;
-        sp.facD = p.facD;
+        sp.facS = 0; // counted in closed form below (fac_add)
+        sp.facD = 0;
         sp.facSrc = p.facSrc;
         sp.facDst = p.facDst;
         if(sp.groups == 0 || !lamk::f64_to_f32_planes(sp, s))
             return false;
+        addAccessCounts(p, S, sp.groups * 4, s);
         const uint64_t doneEnd = begin + sp.groups * 4;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,

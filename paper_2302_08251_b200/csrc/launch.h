@@ -18,6 +18,17 @@ namespace lamk
 
     int sm_count(int device);
 
+    // Grid for a grid-stride streaming kernel: `want` CTAs (one pass of the data), capped at
+    // `perSm` x SMs, with the cap overridable by the environment variable `env`; a cap of 0
+    // means uncapped.  Uncapped one-pass grids measured best for streaming copies on B200: the
+    // hardware block scheduler keeps the active CTAs on a compact, advancing address window
+    // (k_vec_transpose 6.24 -> 6.70 TB/s at 2^26 records).
+    unsigned stream_grid(uint64_t want, const char* env, uint64_t perSm);
+
+    // FieldAccessCount closed form: reads[f] += count (src), writes[f] += count (dst), f < nleaves
+    cudaError_t fac_add(unsigned long long* srcCounters, unsigned long long* dstCounters, uint32_t nleaves,
+                        uint64_t count, cudaStream_t s);
+
     // generic fieldwise copy over [begin, end): one thread per element, all leaves,
     // plan interpreter on both sides (copy_generic.cu)
     cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,

@@ -187,14 +187,10 @@ namespace lamk
     {
         int dev = 0;
         cudaGetDevice(&dev);
+        // one pass, uncapped (see stream_grid); with FieldAccessCount the per-warp counter flush
+        // favours a persistent grid of 16 CTAs per SM
         const uint64_t want = (p.groups + 255) / 256;
-        static const uint64_t per = []
-        {
-            const char* e = getenv("LAMB_VEC_CTAS");
-            return static_cast<uint64_t>(e ? atoi(e) : 16);
-        }();
-        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * per;
-        const unsigned grid = static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
+        const unsigned grid = stream_grid(want, "LAMB_VEC_CTAS", (p.facS || p.facD) ? 16 : 0);
         if(leafSize == 4)
         {
             switch(p.nl)
