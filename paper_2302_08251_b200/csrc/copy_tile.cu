@@ -732,6 +732,230 @@ namespace lamk
         }
     }
 
+    // ---- warp-tile fast leaf loops ----------------------------------------------------------
+    // One leaf of a warp tile with its terminal addressing resolved into registers once: a
+    // term on a lanes == 1 stream (AoS record, SoA array, byte plane) sits at base + e * bs in
+    // the smem image.  Handles PHYS <-> PHYS (any sizes, with conversion) and PHYS <-> SPLIT
+    // (byte planes; 4 elements per lane so each plane gets one 32-bit smem access when the
+    // planes are packed arrays).  Returns false for anything else (the generic loop runs).
+    __device__ __forceinline__ uint64_t wt_ld(const uint8_t* b, uint32_t size)
+    {
+        switch(size)
+        {
+        case 1: return *b;
+        case 2: return *reinterpret_cast<const uint16_t*>(b);
+        case 4: return *reinterpret_cast<const uint32_t*>(b);
+        default: return *reinterpret_cast<const unsigned long long*>(b);
+        }
+    }
+
+    __device__ __forceinline__ void wt_st(uint8_t* b, uint32_t size, uint64_t v)
+    {
+        switch(size)
+        {
+        case 1: *b = static_cast<uint8_t>(v); break;
+        case 2: *reinterpret_cast<uint16_t*>(b) = static_cast<uint16_t>(v); break;
+        case 4: *reinterpret_cast<uint32_t*>(b) = static_cast<uint32_t>(v); break;
+        default: *reinterpret_cast<unsigned long long*>(b) = v; break;
+        }
+    }
+
+    // one leaf of a warp tile through its host-resolved descriptor; false = generic path
+    __device__ __forceinline__ bool wt_fast_leaf(const lamt_params& p, const lamt_leaf& L, const lamt_wfast& W,
+                                                 const uint8_t* sbuf, uint8_t* dbuf, uint32_t lane)
+    {
+        const uint32_t T = p.T;
+        auto fix = [&](uint64_t v) -> uint64_t
+        {
+            if(W.boolean)
+                v = v != 0;
+            if(W.conv)
+                v = lamd::convert_value(lamd::convert_value(v, L.stype, L.ltype), L.ltype, L.dtype);
+            return v;
+        };
+        switch(W.mode)
+        {
+        case LAMT_WF_SKIP:
+            return true;
+        case LAMT_WF_PP:
+            for(uint32_t e = lane; e < T; e += 32)
+                wt_st(dbuf + W.dbase[0] + e * W.dbs[0], W.dsz, fix(wt_ld(sbuf + W.sbase[0] + e * W.sbs[0], W.ssz)));
+            return true;
+        case LAMT_WF_PS_PLANES:
+            for(uint32_t e4 = 4 * lane; e4 < T; e4 += 128)
+            {
+                uint64_t v[4];
+#pragma unroll
+                for(int q = 0; q < 4; ++q)
+                    v[q] = fix(wt_ld(sbuf + W.sbase[0] + (e4 + q) * W.sbs[0], W.ssz));
+#pragma unroll
+                for(uint32_t k = 0; k < 8; ++k)
+                {
+                    if(k >= W.dn)
+                        break;
+                    const uint32_t sh = 8 * k;
+                    const uint32_t w = static_cast<uint32_t>((v[0] >> sh) & 0xFF)
+                        | static_cast<uint32_t>(((v[1] >> sh) & 0xFF) << 8) | static_cast<uint32_t>(((v[2] >> sh) & 0xFF) << 16)
+                        | static_cast<uint32_t>(((v[3] >> sh) & 0xFF) << 24);
+                    *reinterpret_cast<uint32_t*>(dbuf + W.dbase[k] + e4) = w;
+                }
+            }
+            return true;
+        case LAMT_WF_PS_BYTES:
+            for(uint32_t e = lane; e < T; e += 32)
+            {
+                const uint64_t v = fix(wt_ld(sbuf + W.sbase[0] + e * W.sbs[0], W.ssz));
+#pragma unroll
+                for(uint32_t k = 0; k < 8; ++k)
+                    if(k < W.dn)
+                        dbuf[W.dbase[k] + e * W.dbs[k]] = static_cast<uint8_t>(v >> (8 * k));
+            }
+            return true;
+        case LAMT_WF_SP_PLANES:
+            for(uint32_t e4 = 4 * lane; e4 < T; e4 += 128)
+            {
+                uint64_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+                for(uint32_t k = 0; k < 8; ++k)
+                {
+                    if(k >= W.sn)
+                        break;
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(sbuf + W.sbase[k] + e4);
+#pragma unroll
+                    for(int q = 0; q < 4; ++q)
+                        v[q] |= uint64_t((w >> (8 * q)) & 0xFF) << (8 * k);
+                }
+#pragma unroll
+                for(int q = 0; q < 4; ++q)
+                    wt_st(dbuf + W.dbase[0] + (e4 + q) * W.dbs[0], W.dsz, fix(v[q]));
+            }
+            return true;
+        case LAMT_WF_SP_BYTES:
+            for(uint32_t e = lane; e < T; e += 32)
+            {
+                uint64_t v = 0;
+#pragma unroll
+                for(uint32_t k = 0; k < 8; ++k)
+                    if(k < W.sn)
+                        v |= uint64_t(sbuf[W.sbase[k] + e * W.sbs[k]]) << (8 * k);
+                wt_st(dbuf + W.dbase[0] + e * W.dbs[0], W.dsz, fix(v));
+            }
+            return true;
+        default:
+            return false;
+        }
+    }
+
+    // General warp-tile engine: any pair of tile plans (byte splits, type conversions, mixed
+    // leaf sizes, bit-packed sides, non-power-of-two AoSoA, Null).  One warp owns one tile of
+    // p.T elements: every stream image of the tile is one contiguous, 16-byte aligned byte
+    // range, moved HBM -> smem with 16-byte loads (CH per lane in flight before the first smem
+    // store), transformed leaf by leaf in smem (read terminal(s) -> convert -> write
+    // terminal(s), the reference's dst.write(src.read), view.cpp:186-188), bit-packed
+    // destinations assembled as whole words, then smem -> HBM with 16-byte stores.  One tile
+    // per warp and a one-pass grid (the block scheduler walks the address space in order).
+    // Chunk c of the source images lives at sbuf + 16 c; p.st[j].pad holds stream j's first
+    // chunk index (prefix over the source, and separately over the destination, images).
+    template<int CH>
+    __global__ void __launch_bounds__(256, 4) k_warp_tile(const __grid_constant__ lamt_params p, uint32_t ntiles)
+    {
+        extern __shared__ __align__(16) uint8_t wsm[];
+        // chunk -> stream table (host-built, shared by the CTA's warps)
+        __shared__ __align__(16) uint8_t cst[1024];
+        __shared__ uint16_t s_pad[LAMT_MAX_STREAMS];
+        __shared__ unsigned long long s_base[8][LAMT_MAX_STREAMS];
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t warp = threadIdx.x >> 5;
+        const uint32_t ns = p.nsrc, nd = p.ndst;
+        const uint32_t chS = p.wt_chs, chD = p.wt_chd;
+        for(uint32_t k = threadIdx.x; k < (chS + chD + 15) / 16; k += blockDim.x)
+            reinterpret_cast<uint4*>(cst)[k] = reinterpret_cast<const uint4*>(p.wt_cst)[k];
+        for(uint32_t j = threadIdx.x; j < ns + nd; j += blockDim.x)
+            s_pad[j] = static_cast<uint16_t>(p.st[j].pad);
+        const uint8_t* s_cst = cst;
+        const uint8_t* d_cst = cst + chS;
+        const uint32_t wt = blockIdx.x * (blockDim.x >> 5) + warp;
+        const uint64_t t0 = p.begin + uint64_t(wt) * p.T;
+        if(wt < ntiles)
+            for(uint32_t j = lane; j < ns + nd; j += 32)
+                s_base[warp][j] = p.st[j].gptr + tile_global_off(p.st[j], t0);
+        __syncthreads();
+        if(wt >= ntiles)
+            return;
+        uint8_t* sbuf = wsm + warp * (p.src_bytes + p.dst_bytes);
+        uint8_t* dbuf = sbuf + p.src_bytes;
+        const unsigned long long* base = s_base[warp];
+        // ---- load: source images, CH 16-byte chunks per lane in flight ----
+        for(uint32_t c0 = 0; c0 < chS; c0 += 32 * CH)
+        {
+            uint4 v[CH];
+#pragma unroll
+            for(int u = 0; u < CH; ++u)
+            {
+                const uint32_t c = c0 + u * 32 + lane;
+                if(c < chS)
+                {
+                    const uint32_t j = s_cst[c];
+                    v[u] = __ldcs(reinterpret_cast<const uint4*>(base[j]) + (c - s_pad[j]));
+                }
+            }
+#pragma unroll
+            for(int u = 0; u < CH; ++u)
+            {
+                const uint32_t c = c0 + u * 32 + lane;
+                if(c < chS)
+                    reinterpret_cast<uint4*>(sbuf)[c] = v[u];
+            }
+        }
+        __syncwarp();
+        // ---- transform ----
+        for(uint32_t f = 0; f < p.nleaves; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            if(L.dkind == LAMT_K_NULL)
+                continue;
+            if(wt_fast_leaf(p, L, p.wf[f], sbuf, dbuf, lane))
+                continue;
+            for(uint32_t e = lane; e < p.T; e += 32)
+            {
+                uint64_t v = tile_read(p, L, sbuf, e);
+                v = lamd::convert_value(v, L.stype, L.ltype);
+                v = lamd::convert_value(v, L.ltype, L.dtype);
+                tile_write(p, L, dbuf, e, v);
+            }
+        }
+        __syncwarp();
+        if(p.any_bits)
+        {
+            for(uint32_t j = ns; j < ns + nd; ++j)
+                if(p.st[j].kind == 1)
+                    pack_words(p.st[j], dbuf, p.T, lane, 32);
+            __syncwarp();
+        }
+        // ---- store: destination images (contiguous in dbuf, chunk c at dbuf + 16 c) ----
+        for(uint32_t c = lane; c < chD; c += 32)
+        {
+            const uint32_t j = d_cst[c];
+            __stcs(reinterpret_cast<uint4*>(base[j]) + (c - s_pad[j]), reinterpret_cast<const uint4*>(dbuf)[c]);
+        }
+    }
+
+    cudaError_t warp_tile(const lamt_params& p, uint32_t ntiles, cudaStream_t s)
+    {
+        const uint32_t warps = 8;
+        const size_t smem = static_cast<size_t>(warps) * (p.src_bytes + p.dst_bytes);
+        static size_t attr = 0;
+        if(attr < smem)
+        {
+            cudaFuncSetAttribute(k_warp_tile<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr = smem;
+        }
+        const unsigned grid = static_cast<unsigned>((uint64_t(ntiles) + warps - 1) / warps);
+        k_warp_tile<8><<<grid, warps * 32, smem, s>>>(p, ntiles);
+        count_launch();
+        return cudaGetLastError();
+    }
+
     cudaError_t uniform_warp(const lamt_params& p, uint32_t ntiles, cudaStream_t s)
     {
         int dev = 0;

@@ -13,6 +13,7 @@ namespace lamk
     cudaError_t tile_copy(const lamt_params& p, uint32_t smemBytes, uint32_t ctasPerSm, cudaStream_t s);
     cudaError_t uniform_direct(const lamt_params& p, uint64_t n, cudaStream_t s);
     cudaError_t uniform_warp(const lamt_params& p, uint32_t ntiles, cudaStream_t s);
+    cudaError_t warp_tile(const lamt_params& p, uint32_t ntiles, cudaStream_t s);
 
     struct VecSide
     {
@@ -353,6 +354,12 @@ namespace lamhost
         }
     } // namespace
 
+    // General warp-tile engine (copy_tile.cu k_warp_tile): re-tile the plan for one warp per
+    // tile of `wt` elements (about 6 KB of images + bit scratch per warp), every image 16-byte
+    // aligned in global memory and a multiple of 16 bytes long.
+    static bool tryWarpTile(const lamt_params& p, const Lowered& S, const Lowered& D, const DeviceImage& si,
+                            DeviceImage& di, uint64_t begin, uint64_t end, cudaStream_t s);
+
     // FieldAccessCount under copyView (view.cpp:186-188): every element of the range reads each
     // source leaf once and writes each destination leaf once, so the specialised kernels add
     // the counts in closed form (one tiny launch) instead of atomics in the streaming loop
@@ -364,6 +371,126 @@ namespace lamhost
                                      p.facD ? reinterpret_cast<unsigned long long*>(p.facDst) : nullptr,
                                      static_cast<uint32_t>(S.roots.size()), count, s),
                        "fac_add");
+    }
+
+    static bool tryWarpTile(const lamt_params& p, const Lowered& S, const Lowered& D, const DeviceImage& si,
+                            DeviceImage& di, uint64_t begin, uint64_t end, cudaStream_t s)
+    {
+        const uint64_t unit = lcm64(lcm64(S.shardUnit, D.shardUnit), 32);
+        double bpe = 0;
+        for(uint32_t k = 0; k < p.nsrc + p.ndst; ++k)
+        {
+            const lamt_stream& t = p.st[k];
+            bpe += t.kind ? t.bs / 8.0 : double(t.bs) / t.lanes;
+            if(k >= p.nsrc && t.kind)
+                bpe += t.bs > 32 ? 8 : 4;
+        }
+        const double target = envNum("LAMB_WARP_TILE_KB", 6.0) * 1024;
+        uint64_t wt = static_cast<uint64_t>(target / (bpe > 0 ? bpe : 1) / unit) * unit;
+        if(wt < unit)
+            wt = unit;
+        const uint64_t ntw = (end - begin) / wt;
+        if(ntw == 0 || ntw > 0x7FFFFFFFull || wt > 4096 || p.nsrc + p.ndst > 255)
+            return false;
+        lamt_params q = p;
+        q.T = static_cast<uint32_t>(wt);
+        uint32_t off = 0, chunk = 0;
+        for(uint32_t k = 0; k < q.nsrc + q.ndst; ++k)
+        {
+            lamt_stream& t = q.st[k];
+            if(k == q.nsrc)
+            {
+                q.src_bytes = off;
+                off = 0;
+                chunk = 0;
+            }
+            const uint64_t bytes = t.kind ? wt * t.bs / 8 : wt / t.lanes * t.bs;
+            if(bytes % 16 || (t.gptr + (t.kind ? (begin * t.bs) / 8 : begin / t.lanes * t.bs)) % 16)
+                return false;
+            t.tile_bytes = static_cast<uint32_t>(bytes);
+            t.smem_off = off;
+            t.pad = chunk;
+            off += static_cast<uint32_t>(bytes);
+            chunk += static_cast<uint32_t>(bytes / 16);
+        }
+        for(uint32_t k = q.nsrc; k < q.nsrc + q.ndst; ++k)
+        {
+            lamt_stream& t = q.st[k];
+            if(t.kind == 1)
+            {
+                t.scratch64 = t.bs > 32;
+                t.scratch_off = off;
+                off += static_cast<uint32_t>(((wt + 2) * (t.scratch64 ? 8 : 4) + 15) & ~uint64_t{15});
+            }
+        }
+        q.dst_bytes = off;
+        const uint32_t chS = q.src_bytes / 16, chD = chunk;
+        if(8ull * (q.src_bytes + q.dst_bytes) > 180 * 1024 || chS + chD > 1024)
+            return false;
+        q.wt_chs = chS;
+        q.wt_chd = chD;
+        for(uint32_t k = 0; k < q.nsrc + q.ndst; ++k)
+        {
+            const lamt_stream& t = q.st[k];
+            for(uint32_t c = 0; c < t.tile_bytes / 16; ++c)
+                q.wt_cst[(k < q.nsrc ? 0 : chS) + t.pad + c] = static_cast<uint8_t>(k);
+        }
+        q.facS = 0; // closed form below
+        q.facD = 0;
+        // per-leaf fast descriptors (terms on lanes == 1 streams: smem offset + element stride)
+        for(uint32_t f = 0; f < q.nleaves; ++f)
+        {
+            const lamt_leaf& L = q.leaf[f];
+            lamt_wfast& W = q.wf[f];
+            W = lamt_wfast{};
+            W.mode = LAMT_WF_GENERIC;
+            if(L.dkind == LAMT_K_NULL)
+            {
+                W.mode = LAMT_WF_SKIP;
+                continue;
+            }
+            const bool sPhys = L.skind == LAMT_K_PHYS, dPhys = L.dkind == LAMT_K_PHYS;
+            const bool sSplit = L.skind == LAMT_K_SPLIT, dSplit = L.dkind == LAMT_K_SPLIT;
+            if(!((sPhys || sSplit) && (dPhys || dSplit)) || (sSplit && dSplit))
+                continue;
+            W.sn = sPhys ? 1 : L.sn;
+            W.dn = dPhys ? 1 : L.dn;
+            bool ok = W.sn <= 8 && W.dn <= 8;
+            bool planes = q.T % 4 == 0;
+            auto term = [&](const lamt_term& t, uint32_t& base, uint32_t& bs, bool split) -> bool
+            {
+                const lamt_stream& st = q.st[t.stream];
+                if(st.kind != 0 || st.lanes != 1 || !t.aligned)
+                    return false;
+                base = st.smem_off + t.inblock;
+                bs = st.bs;
+                if(split)
+                    planes = planes && bs == 1 && (base & 3) == 0;
+                return true;
+            };
+            for(uint32_t k = 0; ok && k < W.sn; ++k)
+                ok = term(L.s[k], W.sbase[k], W.sbs[k], sSplit);
+            for(uint32_t k = 0; ok && k < W.dn; ++k)
+                ok = term(L.d[k], W.dbase[k], W.dbs[k], dSplit);
+            if(!ok)
+                continue;
+            W.ssz = sPhys ? L.s[0].size : 1;
+            W.dsz = dPhys ? L.d[0].size : 1;
+            W.conv = !(L.stype == L.ltype && L.ltype == L.dtype);
+            W.boolean = L.stype == Bool;
+            W.mode = sPhys && dPhys ? LAMT_WF_PP
+                   : dSplit       ? (planes ? LAMT_WF_PS_PLANES : LAMT_WF_PS_BYTES)
+                                  : (planes ? LAMT_WF_SP_PLANES : LAMT_WF_SP_BYTES);
+        }
+        lam_cuda_check(lamk::warp_tile(q, static_cast<uint32_t>(ntw), s), "warp_tile");
+        addAccessCounts(p, S, ntw * wt, s);
+        const uint64_t doneEnd = begin + ntw * wt;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s),
+                           "generic_copy(tail)");
+        (void)D;
+        return true;
     }
 
     // register-transpose path (vec_transpose.cu) for uniform 4/8-byte-leaf pairs whose sides are
@@ -652,6 +779,8 @@ namespace lamhost
                 }
             }
         }
+        if(envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s))
+            return true;
         lam_cuda_check(lamk::tile_copy(p, pl.smem, pl.ctas, s), "tile_copy");
         const uint64_t doneEnd = begin + ntiles * p.T;
         if(doneEnd < end)

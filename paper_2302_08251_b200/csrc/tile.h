@@ -54,6 +54,20 @@ struct lamt_leaf
     lamt_term d[LAMT_MAX_TERMS];
 };
 
+// warp-tile engine: a leaf's terminal addressing resolved on the host (k_warp_tile)
+#define LAMT_WF_GENERIC 0
+#define LAMT_WF_PP 1        // PHYS -> PHYS
+#define LAMT_WF_PS_PLANES 2 // PHYS -> byte planes (packed u8 arrays): 4 elements per lane, u32 per plane
+#define LAMT_WF_PS_BYTES 3  // PHYS -> byte terms
+#define LAMT_WF_SP_PLANES 4 // byte planes -> PHYS
+#define LAMT_WF_SP_BYTES 5  // byte terms -> PHYS
+#define LAMT_WF_SKIP 6      // Null destination
+struct lamt_wfast
+{
+    uint8_t mode, sn, dn, conv, boolean, ssz, dsz, pad;
+    uint32_t sbase[8], sbs[8], dbase[8], dbs[8]; // smem image offset (incl. inblock) and element stride
+};
+
 #define LAMT_MAX_WARPS 32
 #define LAMT_MAX_STAGES 4
 #define LAMT_UNI_LEAVES 16
@@ -86,4 +100,9 @@ struct lamt_params
     uint32_t uoff_s[LAMT_UNI_LEAVES], uoff_d[LAMT_UNI_LEAVES];
     lamt_stream st[LAMT_MAX_STREAMS];
     lamt_leaf leaf[LAMT_MAX_LEAVES];
+    lamt_wfast wf[LAMT_MAX_LEAVES];
+    // warp-tile engine: stream of each 16-byte image chunk, source chunks then destination
+    // chunks (host-built, copied to shared memory by each CTA)
+    uint32_t wt_chs, wt_chd;
+    __align__(16) uint8_t wt_cst[1024];
 };
