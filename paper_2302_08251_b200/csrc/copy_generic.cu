@@ -43,11 +43,17 @@ namespace lamk
     // CTA per field (instrument.cpp:57-72 counts one relaxed increment per access)
     template<typename Idx>
     __global__ void __launch_bounds__(256) k_generic_copy(const lamp_view* __restrict__ S, const lamp_view* __restrict__ D,
-                                                           uint64_t begin, uint64_t end, uint32_t nleaves, int facS, int facD)
+                                                           uint64_t begin, uint64_t end, uint32_t nleaves, int facS, int facD,
+                                                           int countHeat)
     {
         extern __shared__ unsigned long long s_cnt[]; // [nleaves] reads, [nleaves] writes
-        const lamd::ViewCtx sv = lamd::make_ctx(S);
-        const lamd::ViewCtx dv = lamd::make_ctx(D);
+        lamd::ViewCtx sv = lamd::make_ctx(S);
+        lamd::ViewCtx dv = lamd::make_ctx(D);
+        if(!countHeat)
+        {
+            sv.heat = nullptr;
+            dv.heat = nullptr;
+        }
         const uint16_t* sroots = S->roots;
         const uint16_t* droots = D->roots;
         if(facS | facD)
@@ -92,7 +98,7 @@ namespace lamk
     }
 
     cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,
-                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s)
+                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s, bool countHeat)
     {
         if(end <= begin || nleaves == 0)
             return cudaSuccess;
@@ -104,9 +110,9 @@ namespace lamk
         const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
         const size_t smem = (facSrc || facDst) ? 2 * nleaves * sizeof(unsigned long long) : 0;
         if(end <= 0x7FFFFFFFull)
-            k_generic_copy<uint32_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst);
+            k_generic_copy<uint32_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst, countHeat);
         else
-            k_generic_copy<uint64_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst);
+            k_generic_copy<uint64_t><<<grid, 256, smem, s>>>(src, dst, begin, end, nleaves, facSrc, facDst, countHeat);
         count_launch();
         return cudaGetLastError();
     }
@@ -138,6 +144,28 @@ namespace lamk
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         for(uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
             d[i] = s[i];
+    }
+
+    // Heatmap accounting of copyView over [begin, end): every element touches every leaf's
+    // access ranges once (view.cpp:186-188 through Heatmap::read/write, instrument.cpp:163-176)
+    __global__ void __launch_bounds__(256) k_heat_account(const lamp_view* __restrict__ V, uint64_t begin, uint64_t end,
+                                                         uint32_t nleaves)
+    {
+        const lamd::ViewCtx c = lamd::make_ctx(V);
+        for(uint64_t i = begin + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < end;
+            i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+            for(uint32_t f = 0; f < nleaves; ++f)
+                lamd::touch_node<LAMP_MAX_DEPTH>(c, V->roots[f], i);
+    }
+
+    cudaError_t heat_account(const lamp_view* v, uint64_t begin, uint64_t end, uint32_t nleaves, cudaStream_t s)
+    {
+        if(end <= begin)
+            return cudaSuccess;
+        const unsigned grid = stream_grid((end - begin + 255) / 256, "LAMB_HEAT_CTAS", 16);
+        k_heat_account<<<grid, 256, 0, s>>>(v, begin, end, nleaves);
+        count_launch();
+        return cudaGetLastError();
     }
 
     __global__ void k_fac_add(unsigned long long* src, unsigned long long* dst, uint32_t nl, unsigned long long cnt)

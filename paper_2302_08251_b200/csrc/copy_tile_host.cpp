@@ -186,9 +186,7 @@ namespace lamhost
 
         Plan makePlan(const Lowered& S, const Lowered& D)
         {
-            Plan pl;
-            if(S.heat || D.heat)
-                return pl;
+            Plan pl; // heatmaps are accounted separately (launchTile -> heat_account)
             const size_t nleaves = S.roots.size();
             if(nleaves == 0 || nleaves > LAMT_MAX_LEAVES)
                 return pl;
@@ -487,7 +485,7 @@ namespace lamhost
         const uint64_t doneEnd = begin + ntw * wt;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s),
+                                              D.fac, s, false),
                            "generic_copy(tail)");
         (void)D;
         return true;
@@ -563,7 +561,7 @@ namespace lamhost
         const uint64_t doneEnd = begin + vp.groups * V;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s),
+                                              D.fac, s, false),
                            "generic_copy(tail)");
         (void)D;
         return true;
@@ -636,7 +634,7 @@ namespace lamhost
         const uint64_t doneEnd = begin + groups * 32;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s),
+                                              D.fac, s, false),
                            "generic_copy(tail)");
         return true;
     }
@@ -687,14 +685,34 @@ namespace lamhost
         const uint64_t doneEnd = begin + sp.groups * 4;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s),
+                                              D.fac, s, false),
                            "generic_copy(tail)");
         return true;
     }
 
+    static bool launchTileData(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr,
+                               const Lowered& D, DeviceImage& di, const std::vector<uint8_t*>& dptr, uint64_t begin,
+                               uint64_t end, cudaStream_t s);
+
+    // the data moves through the tile kernels (none of which counts heat); a Heatmap on either
+    // side is then accounted over the whole range in one pass that touches ranges, not data
     static bool launchTile(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr, const Lowered& D,
                            DeviceImage& di, const std::vector<uint8_t*>& dptr, uint64_t begin, uint64_t end,
                            cudaStream_t s)
+    {
+        if(!launchTileData(S, si, sptr, D, di, dptr, begin, end, s))
+            return false;
+        const uint32_t nl = static_cast<uint32_t>(S.roots.size());
+        if(S.heat)
+            lam_cuda_check(lamk::heat_account(si.hdr, begin, end, nl, s), "heat_account(src)");
+        if(D.heat)
+            lam_cuda_check(lamk::heat_account(di.hdr, begin, end, nl, s), "heat_account(dst)");
+        return true;
+    }
+
+    static bool launchTileData(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr,
+                               const Lowered& D, DeviceImage& di, const std::vector<uint8_t*>& dptr, uint64_t begin,
+                               uint64_t end, cudaStream_t s)
     {
         Plan pl = makePlan(S, D);
         if(!pl.ok)
@@ -773,7 +791,7 @@ namespace lamhost
                     const uint64_t doneEnd = begin + ntw * wt;
                     if(doneEnd < end)
                         lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end,
-                                                          static_cast<uint32_t>(S.roots.size()), S.fac, D.fac, s),
+                                                          static_cast<uint32_t>(S.roots.size()), S.fac, D.fac, s, false),
                                        "generic_copy(tail)");
                     return true;
                 }
@@ -785,7 +803,7 @@ namespace lamhost
         const uint64_t doneEnd = begin + ntiles * p.T;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()),
-                                              S.fac, D.fac, s),
+                                              S.fac, D.fac, s, false),
                            "generic_copy(tail)");
         return true;
     }

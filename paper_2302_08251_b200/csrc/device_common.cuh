@@ -322,12 +322,19 @@ namespace lamd
         return blk * st.block_stride + inblock + lane * ls;
     }
 
+    // Heatmap touch of byte range [begin, end) of blob nr (instrument.cpp:163-176).  Lanes that
+    // hit the same first block (neighbouring elements of one leaf, g >= element stride) are
+    // combined into one atomic by the lowest such lane (opportunistic warp aggregation).
     LAM_DEV void heat_touch(const ViewCtx& v, uint32_t nr, uint64_t begin, uint64_t end)
     {
         if(begin >= end)
             return;
         const uint64_t first = begin / v.gran, last = (end - 1) / v.gran;
-        for(uint64_t b = first; b <= last; ++b)
+        const unsigned long long idx = v.heatOff[nr] + first;
+        const unsigned peers = __match_any_sync(__activemask(), idx);
+        if((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
+            atomicAdd(&v.heat[idx], v.heatMul * static_cast<unsigned long long>(__popc(peers)));
+        for(uint64_t b = first + 1; b <= last; ++b)
             atomicAdd(&v.heat[v.heatOff[nr] + b], v.heatMul);
     }
 
@@ -443,6 +450,49 @@ namespace lamd
                 __trap();
             return;
         default: // LAMP_NULL: discarded
+            return;
+        }
+    }
+
+    // The heatmap ranges of one access of node n at element i (Mapping::accessRanges: physical
+    // = [off, off+size), bit fields = outward-rounded bytes, byte splits = their s bytes), without
+    // touching the data: heat accounting for copies whose data moved through a fast kernel.
+    template<int D>
+    __device__ __noinline__ void touch_node(const ViewCtx& v, uint32_t n, uint64_t i)
+    {
+        const lamp_node nd = v.nodes[n];
+        switch(nd.kind)
+        {
+        case LAMP_PHYS:
+        {
+            const lamp_stream st = v.streams[nd.stream];
+            const uint64_t rel = block_rel(st, i, nd.a, nd.b);
+            heat_touch(v, st.nr, st.base0 + rel, st.base0 + rel + scalar_size(nd.type));
+            return;
+        }
+        case LAMP_BITS_INT:
+        {
+            const uint64_t off = i * nd.a;
+            heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + nd.a + 7) / 8);
+            return;
+        }
+        case LAMP_BITS_FLT:
+        {
+            const uint32_t w = 1 + nd.a + nd.b;
+            const uint64_t off = i * w;
+            heat_touch(v, v.streams[nd.stream].nr, off / 8, (off + w + 7) / 8);
+            return;
+        }
+        case LAMP_CONVERT:
+            if constexpr(D > 1)
+                touch_node<D - 1>(v, nd.child, i);
+            return;
+        case LAMP_SPLIT:
+            if constexpr(D > 1)
+                for(uint32_t k = 0; k < nd.nchild; ++k)
+                    touch_node<D - 1>(v, nd.child + k, i);
+            return;
+        default:
             return;
         }
     }

@@ -32,7 +32,9 @@ namespace lamk
     // generic fieldwise copy over [begin, end): one thread per element, all leaves,
     // plan interpreter on both sides (copy_generic.cu)
     cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,
-                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s);
+                             uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s, bool countHeat = true);
+    // Heatmap accounting of a copy over [begin, end) whose data moved through a fast kernel
+    cudaError_t heat_account(const lamp_view* v, uint64_t begin, uint64_t end, uint32_t nleaves, cudaStream_t s);
     // byte-exact blob copy (copyView's sameLayout memcpy path)
     cudaError_t blob_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
     cudaError_t read_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, uint64_t* out, size_t n,
