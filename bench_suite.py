@@ -44,7 +44,16 @@ def _fill(L, view, seed):
     torch.cuda.synchronize()
 
 
-def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5")):
+OTHER_PAIRS = [  # compositions outside the BASELINE configs (informative)
+    (R32, "aos-packed", "bytesplit:soa-mb", 0), (R32, "bytesplit:soa-mb", "aos-packed", 0),
+    (R32, "aos-packed", "changetype:f32=f64:soa-mb", 0), (R32, "aos-packed", "split:Pos:soa-mb:aos-packed", 0),
+    (R32, "aos-packed", "aosoa:3", 0), (R32, "aos-packed", "aos-aligned", 0), (R32, "soa-mb", "aos-packed", 1),
+    (R32, "aos-packed", "soa-mb", 2), (R32, "aos-packed", "bitpack-float:5,10", 0),
+    ("Record{a:f64,b:u16,c:i8,d:f32}", "aos-packed", "soa-mb", 0),
+]
+
+
+def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")):
     import torch
     out = {}
     # ---- C1 ------------------------------------------------------------------------------
@@ -125,6 +134,23 @@ def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5")):
             "GB/s": 84 * n / ms / 1e6, "frac": 84 * n / ms / 1e6 / peak_gbs, "ms": ms,
             "writes_per_leaf_after_runs": [int(x) for x in w]}
         del src, dst
+    # ---- C6 (not a BASELINE config): other compositions, 2^26 records ---------------------
+    if "C6" in parts:
+        n = 1 << 26
+        c6 = {}
+        for schema, a, b, wrap in OTHER_PAIRS:
+            la = L.Layout(schema, f"i32:[{n}]", a)
+            lb = L.Layout(schema, f"i32:[{n}]", b, wrap=wrap, granularity=64)
+            s, d = L.View(la), L.View(lb)
+            _fill(L, s, 6)
+            ms = _time(lambda: L.copy_view(s, d), reps=3, warm=1)
+            # algorithmic bytes: source storage read + destination storage written
+            byt = sum(la.blob_sizes) + sum(lb.blob_sizes)
+            tag = {0: "", 1: " +FieldAccessCount", 2: " +Heatmap(64)"}[wrap]
+            c6[f"{a} -> {b}{tag}" + ("" if schema == R32 else " (mixed record)")] = {
+                "GB/s": byt / ms / 1e6, "frac": byt / ms / 1e6 / peak_gbs}
+            del s, d
+        out["C6_other_compositions_2^26"] = c6
     return out
 
 
@@ -133,4 +159,4 @@ if __name__ == "__main__":
     import sys
     sys.path.insert(0, ".")
     from paper_2302_08251_b200 import lamina
-    print(json.dumps(run_suite(lamina, 0, parts=tuple(sys.argv[1:]) or ("C1", "C3", "C4", "C5")), indent=1))
+    print(json.dumps(run_suite(lamina, 0, parts=tuple(sys.argv[1:]) or ("C1", "C3", "C4", "C5", "C6")), indent=1))

@@ -1,2 +1,3 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for kb in 4 9; do echo KB=$kb; LAMB_WARP_TILE_KB=$kb python tools/misc_pairs.py 2>&1 | tail -12 | head -5; done
+python bench_suite.py C6 > gpurun_out/c6.json 2>&1; python -c "
+import json; d=json.load(open('gpurun_out/c6.json'))
+for k,v in d['C6_other_compositions_2^26'].items(): print(k, round(v['GB/s']), round(v['frac'],3))"

@@ -20,3 +20,5 @@ for k, v in c4.items():
         print("C4", k, {m: (round(x["interactions/s"] / 1e9, 1), round(x["frac_measured_fp32_peak"], 3))
                         for m, x in v.items() if isinstance(x, dict)})
 print("C4 peak", c4.get("fp32_peak_measured_tflops"), c4.get("clocks_during_nbody"))
+for k, v in (s.get("C6_other_compositions_2^26") or {}).items():
+    print("C6", k, round(v["GB/s"]), round(v["frac"], 3))
