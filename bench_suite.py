@@ -50,6 +50,7 @@ OTHER_PAIRS = [  # compositions outside the BASELINE configs (informative)
     (R32, "aos-packed", "aosoa:3", 0), (R32, "aos-packed", "aos-aligned", 0), (R32, "soa-mb", "aos-packed", 1),
     (R32, "aos-packed", "soa-mb", 2), (R32, "aos-packed", "bitpack-float:5,10", 0),
     ("Record{a:f64,b:u16,c:i8,d:f32}", "aos-packed", "soa-mb", 0),
+    (R64, "aos-packed", "bytesplit:soa-mb", 0), (R64, "changetype:f64=f32:bytesplit:soa-mb", "aos-packed", 0),
 ]
 
 
@@ -147,7 +148,7 @@ def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")
             # algorithmic bytes: source storage read + destination storage written
             byt = sum(la.blob_sizes) + sum(lb.blob_sizes)
             tag = {0: "", 1: " +FieldAccessCount", 2: " +Heatmap(64)"}[wrap]
-            c6[f"{a} -> {b}{tag}" + ("" if schema == R32 else " (mixed record)")] = {
+            c6[f"{a} -> {b}{tag}" + {R32: "", R64: " (R64)"}.get(schema, " (mixed record)")] = {
                 "GB/s": byt / ms / 1e6, "frac": byt / ms / 1e6 / peak_gbs}
             del s, d
         out["C6_other_compositions_2^26"] = c6

@@ -874,69 +874,72 @@ namespace lamk
             s_pad[j] = static_cast<uint16_t>(p.st[j].pad);
         const uint8_t* s_cst = cst;
         const uint8_t* d_cst = cst + chS;
-        const uint32_t wt = blockIdx.x * (blockDim.x >> 5) + warp;
-        const uint64_t t0 = p.begin + uint64_t(wt) * p.T;
-        if(wt < ntiles)
-            for(uint32_t j = lane; j < ns + nd; j += 32)
-                s_base[warp][j] = p.st[j].gptr + tile_global_off(p.st[j], t0);
         __syncthreads();
-        if(wt >= ntiles)
-            return;
         uint8_t* sbuf = wsm + warp * (p.src_bytes + p.dst_bytes);
         uint8_t* dbuf = sbuf + p.src_bytes;
-        const unsigned long long* base = s_base[warp];
-        // ---- load: source images, CH 16-byte chunks per lane in flight ----
-        for(uint32_t c0 = 0; c0 < chS; c0 += 32 * CH)
+        unsigned long long* base = s_base[warp];
+        // tiles in warp order: at any moment the active warps work on adjacent tiles
+        const uint32_t tw = gridDim.x * (blockDim.x >> 5);
+        for(uint32_t wt = blockIdx.x * (blockDim.x >> 5) + warp; wt < ntiles; wt += tw)
         {
-            uint4 v[CH];
-#pragma unroll
-            for(int u = 0; u < CH; ++u)
+            const uint64_t t0 = p.begin + uint64_t(wt) * p.T;
+            for(uint32_t j = lane; j < ns + nd; j += 32)
+                base[j] = p.st[j].gptr + tile_global_off(p.st[j], t0);
+            __syncwarp();
+            // ---- load: source images, CH 16-byte chunks per lane in flight ----
+            for(uint32_t c0 = 0; c0 < chS; c0 += 32 * CH)
             {
-                const uint32_t c = c0 + u * 32 + lane;
-                if(c < chS)
+                uint4 v[CH];
+    #pragma unroll
+                for(int u = 0; u < CH; ++u)
                 {
-                    const uint32_t j = s_cst[c];
-                    v[u] = __ldcs(reinterpret_cast<const uint4*>(base[j]) + (c - s_pad[j]));
+                    const uint32_t c = c0 + u * 32 + lane;
+                    if(c < chS)
+                    {
+                        const uint32_t j = s_cst[c];
+                        v[u] = __ldcs(reinterpret_cast<const uint4*>(base[j]) + (c - s_pad[j]));
+                    }
+                }
+    #pragma unroll
+                for(int u = 0; u < CH; ++u)
+                {
+                    const uint32_t c = c0 + u * 32 + lane;
+                    if(c < chS)
+                        reinterpret_cast<uint4*>(sbuf)[c] = v[u];
                 }
             }
-#pragma unroll
-            for(int u = 0; u < CH; ++u)
-            {
-                const uint32_t c = c0 + u * 32 + lane;
-                if(c < chS)
-                    reinterpret_cast<uint4*>(sbuf)[c] = v[u];
-            }
-        }
-        __syncwarp();
-        // ---- transform ----
-        for(uint32_t f = 0; f < p.nleaves; ++f)
-        {
-            const lamt_leaf& L = p.leaf[f];
-            if(L.dkind == LAMT_K_NULL)
-                continue;
-            if(wt_fast_leaf(p, L, p.wf[f], sbuf, dbuf, lane))
-                continue;
-            for(uint32_t e = lane; e < p.T; e += 32)
-            {
-                uint64_t v = tile_read(p, L, sbuf, e);
-                v = lamd::convert_value(v, L.stype, L.ltype);
-                v = lamd::convert_value(v, L.ltype, L.dtype);
-                tile_write(p, L, dbuf, e, v);
-            }
-        }
-        __syncwarp();
-        if(p.any_bits)
-        {
-            for(uint32_t j = ns; j < ns + nd; ++j)
-                if(p.st[j].kind == 1)
-                    pack_words(p.st[j], dbuf, p.T, lane, 32);
             __syncwarp();
-        }
-        // ---- store: destination images (contiguous in dbuf, chunk c at dbuf + 16 c) ----
-        for(uint32_t c = lane; c < chD; c += 32)
-        {
-            const uint32_t j = d_cst[c];
-            __stcs(reinterpret_cast<uint4*>(base[j]) + (c - s_pad[j]), reinterpret_cast<const uint4*>(dbuf)[c]);
+            // ---- transform ----
+            for(uint32_t f = 0; f < p.nleaves; ++f)
+            {
+                const lamt_leaf& L = p.leaf[f];
+                if(L.dkind == LAMT_K_NULL)
+                    continue;
+                if(wt_fast_leaf(p, L, p.wf[f], sbuf, dbuf, lane))
+                    continue;
+                for(uint32_t e = lane; e < p.T; e += 32)
+                {
+                    uint64_t v = tile_read(p, L, sbuf, e);
+                    v = lamd::convert_value(v, L.stype, L.ltype);
+                    v = lamd::convert_value(v, L.ltype, L.dtype);
+                    tile_write(p, L, dbuf, e, v);
+                }
+            }
+            __syncwarp();
+            if(p.any_bits)
+            {
+                for(uint32_t j = ns; j < ns + nd; ++j)
+                    if(p.st[j].kind == 1)
+                        pack_words(p.st[j], dbuf, p.T, lane, 32);
+                __syncwarp();
+            }
+            // ---- store: destination images (contiguous in dbuf, chunk c at dbuf + 16 c) ----
+            for(uint32_t c = lane; c < chD; c += 32)
+            {
+                const uint32_t j = d_cst[c];
+                __stcs(reinterpret_cast<uint4*>(base[j]) + (c - s_pad[j]), reinterpret_cast<const uint4*>(dbuf)[c]);
+            }
+            __syncwarp();
         }
     }
 
@@ -950,7 +953,7 @@ namespace lamk
             cudaFuncSetAttribute(k_warp_tile<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             attr = smem;
         }
-        const unsigned grid = static_cast<unsigned>((uint64_t(ntiles) + warps - 1) / warps);
+        const unsigned grid = stream_grid((uint64_t(ntiles) + warps - 1) / warps, "LAMB_WT_CTAS", 8);
         k_warp_tile<8><<<grid, warps * 32, smem, s>>>(p, ntiles);
         count_launch();
         return cudaGetLastError();

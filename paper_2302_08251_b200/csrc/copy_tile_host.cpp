@@ -42,15 +42,14 @@ namespace lamk
     };
     bool pack32(const PackParams& p, bool pack, cudaStream_t s);
 
-    struct SplitParams
+    struct PlaneParams
     {
         unsigned long long rec;
-        unsigned long long plane[8][4];
+        unsigned long long plane[8][8];
         unsigned long long begin, groups;
-        unsigned long long facSrc, facDst;
-        uint32_t nl, facS, facD;
+        uint32_t nl;
     };
-    bool f64_to_f32_planes(const SplitParams& p, cudaStream_t s);
+    bool planes_copy(const PlaneParams& p, uint32_t sb, bool cvt, bool toPlanes, cudaStream_t s);
 }
 
 using namespace lamb;
@@ -640,49 +639,61 @@ namespace lamhost
     }
 
     // K5: record-contiguous f64 -> changetype f32 -> bytesplit into 1-byte SoA planes
+    // Bytesplit against a record-contiguous side (planes.cu): every leaf an SB-byte physical leaf
+    // of one packed record stream on one side, and byte planes (packed u8 arrays) on the other,
+    // either the same type (plain bytesplit) or f64 records <-> f32 planes (ChangeType, C5).
     static bool trySplit(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
                          const Lowered& S, const Lowered& D, cudaStream_t s)
     {
         if(begin % 4 || p.nleaves > 8 || envNum("LAMB_SPLITK", 1) == 0)
             return false;
         const uint32_t nl = p.nleaves;
-        lamk::SplitParams sp{};
-        const lamt_term& s0 = p.leaf[0].s[0];
+        const bool toPlanes = p.leaf[0].skind == LAMT_K_PHYS;
+        lamk::PlaneParams pp{};
+        const lamt_term& r0 = toPlanes ? p.leaf[0].s[0] : p.leaf[0].d[0];
+        const uint32_t sb = r0.size;
+        bool cvt = false;
         for(uint32_t f = 0; f < nl; ++f)
         {
             const lamt_leaf& L = p.leaf[f];
-            if(L.skind != LAMT_K_PHYS || L.stype != F64 || L.ltype != F64 || L.dkind != LAMT_K_SPLIT || L.dtype != F32
-               || L.dn != 4)
+            const uint8_t recKind = toPlanes ? L.skind : L.dkind, plKind = toPlanes ? L.dkind : L.skind;
+            const uint32_t pn = toPlanes ? L.dn : L.sn;
+            if(recKind != LAMT_K_PHYS || plKind != LAMT_K_SPLIT)
                 return false;
-            const lamt_term& t = L.s[0];
+            const bool pure = L.stype == L.ltype && L.ltype == L.dtype && pn == sb;
+            const bool conv = sb == 8 && pn == 4
+                && (toPlanes ? (L.stype == F64 && L.ltype == F64 && L.dtype == F32)
+                             : (L.stype == F32 && L.ltype == F64 && L.dtype == F64));
+            if(!(pure || conv) || (f > 0 && conv != cvt))
+                return false;
+            cvt = conv;
+            const lamt_term& t = toPlanes ? L.s[0] : L.d[0];
             const lamt_stream& st = p.st[t.stream];
-            if(t.stream != s0.stream || t.inblock != f * 8 || st.lanes != 1 || st.bs != nl * 8)
+            if(t.stream != r0.stream || t.size != sb || t.inblock != f * sb || st.lanes != 1 || st.bs != nl * sb)
                 return false;
-            for(uint32_t k = 0; k < 4; ++k)
+            for(uint32_t k = 0; k < pn; ++k)
             {
-                const lamt_term& d = L.d[k];
+                const lamt_term& d = toPlanes ? L.d[k] : L.s[k];
                 const lamt_stream& ds = p.st[d.stream];
                 if(ds.lanes != 1 || ds.bs != 1)
                     return false;
-                sp.plane[f][k] = ds.gptr + d.inblock;
-                if((sp.plane[f][k] + begin) % 4)
+                pp.plane[f][k] = ds.gptr + d.inblock;
+                if((pp.plane[f][k] + begin) % 4)
                     return false;
             }
         }
-        sp.rec = p.st[s0.stream].gptr;
-        if((sp.rec + begin * nl * 8) % 16)
+        if(sb != 4 && sb != 8)
             return false;
-        sp.begin = begin;
-        sp.groups = (end - begin) / 4;
-        sp.nl = nl;
-        sp.facS = 0; // counted in closed form below (fac_add)
-        sp.facD = 0;
-        sp.facSrc = p.facSrc;
-        sp.facDst = p.facDst;
-        if(sp.groups == 0 || !lamk::f64_to_f32_planes(sp, s))
+        pp.rec = p.st[r0.stream].gptr;
+        if((pp.rec + begin * nl * sb) % 16)
             return false;
-        addAccessCounts(p, S, sp.groups * 4, s);
-        const uint64_t doneEnd = begin + sp.groups * 4;
+        pp.begin = begin;
+        pp.groups = (end - begin) / 4;
+        pp.nl = nl;
+        if(pp.groups == 0 || !lamk::planes_copy(pp, sb, cvt, toPlanes, s))
+            return false;
+        addAccessCounts(p, S, pp.groups * 4, s);
+        const uint64_t doneEnd = begin + pp.groups * 4;
         if(doneEnd < end)
             lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
                                               D.fac, s, false),

@@ -473,86 +473,4 @@ namespace lamk
         return true;
     }
 
-    // ---- K5: f64 record-contiguous -> f32 -> 4 byte planes per leaf ------------------------
-    struct SplitParams
-    {
-        unsigned long long rec;           // source records (NL x f64, packed), element 0
-        unsigned long long plane[8][4];   // plane[f][k]: byte k of leaf f, element 0
-        unsigned long long begin, groups; // groups of 4 records
-        unsigned long long facSrc, facDst;
-        uint32_t nl, facS, facD;
-    };
-
-    template<int NL>
-    __global__ void __launch_bounds__(256) k_f64_to_f32_planes(const __grid_constant__ SplitParams p)
-    {
-        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-        unsigned long long cnt = 0;
-        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < p.groups; g += stride)
-        {
-            const uint64_t e0 = p.begin + g * 4;
-            const uint4* src = reinterpret_cast<const uint4*>(p.rec + e0 * (NL * 8));
-            uint32_t f32[4][NL];
-#pragma unroll
-            for(int q = 0; q < 2 * NL; ++q)
-            {
-                const uint4 x = __ldcs(src + q);
-                // vector q holds doubles 2q, 2q+1 of the 4*NL record-major doubles
-                const int d0 = 2 * q, d1 = 2 * q + 1;
-                f32[d0 / NL][d0 % NL] = lamd::f64_to_f32_bits((uint64_t(x.y) << 32) | x.x);
-                f32[d1 / NL][d1 % NL] = lamd::f64_to_f32_bits((uint64_t(x.w) << 32) | x.z);
-            }
-#pragma unroll
-            for(int f = 0; f < NL; ++f)
-            {
-#pragma unroll
-                for(int k = 0; k < 4; ++k)
-                {
-                    // byte k of the 4 consecutive elements -> one 32-bit word of plane (f, k)
-                    const uint32_t w = ((f32[0][f] >> (8 * k)) & 0xFF) | (((f32[1][f] >> (8 * k)) & 0xFF) << 8)
-                        | (((f32[2][f] >> (8 * k)) & 0xFF) << 16) | (((f32[3][f] >> (8 * k)) & 0xFF) << 24);
-                    __stcs(reinterpret_cast<uint32_t*>(p.plane[f][k] + e0), w);
-                }
-            }
-            cnt += 4;
-        }
-        if(p.facS || p.facD)
-        {
-            for(int o = 16; o > 0; o >>= 1)
-                cnt += __shfl_down_sync(0xFFFFFFFFu, cnt, o);
-            if((threadIdx.x & 31) == 0 && cnt)
-                for(uint32_t f = 0; f < p.nl; ++f)
-                {
-                    if(p.facS)
-                        atomicAdd(reinterpret_cast<unsigned long long*>(p.facSrc) + f, cnt);
-                    if(p.facD)
-                        atomicAdd(reinterpret_cast<unsigned long long*>(p.facDst) + p.nl + f, cnt);
-                }
-        }
-    }
-
-    bool f64_to_f32_planes(const SplitParams& p, cudaStream_t s)
-    {
-        if(p.groups == 0)
-            return false;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const uint64_t want = (p.groups + 255) / 256;
-        const unsigned grid = stream_grid(want, "LAMB_SPLIT_CTAS", (p.facS || p.facD) ? 8 : 0);
-        switch(p.nl)
-        {
-        case 1: k_f64_to_f32_planes<1><<<grid, 256, 0, s>>>(p); break;
-        case 2: k_f64_to_f32_planes<2><<<grid, 256, 0, s>>>(p); break;
-        case 3: k_f64_to_f32_planes<3><<<grid, 256, 0, s>>>(p); break;
-        case 4: k_f64_to_f32_planes<4><<<grid, 256, 0, s>>>(p); break;
-        case 5: k_f64_to_f32_planes<5><<<grid, 256, 0, s>>>(p); break;
-        case 6: k_f64_to_f32_planes<6><<<grid, 256, 0, s>>>(p); break;
-        case 7: k_f64_to_f32_planes<7><<<grid, 256, 0, s>>>(p); break;
-        case 8: k_f64_to_f32_planes<8><<<grid, 256, 0, s>>>(p); break;
-        default: return false;
-        }
-        count_launch();
-        lam_cuda_check(cudaGetLastError(), "kernel launch");
-        return true;
-    }
 } // namespace lamk

@@ -12,7 +12,7 @@
 #include <stdint.h>
 
 #define LAMT_MAX_LEAVES 32
-#define LAMT_MAX_STREAMS 48
+#define LAMT_MAX_STREAMS 64
 #define LAMT_MAX_TERMS 8
 
 #define LAMT_K_PHYS 0

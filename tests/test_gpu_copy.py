@@ -118,6 +118,19 @@ def test_c5_layout_r64():
     run_pair(R64, n, "aos-packed", "bytesplit:changetype:f64=f32", vals, dst_wrap=1)
 
 
+@pytest.mark.parametrize("a,b,wrap", [
+    ("changetype:f64=f32:bytesplit:soa-mb", "aos-packed", 1),   # planes -> f64 records (f32 -> f64 read)
+    ("aos-packed", "bytesplit:soa-mb", 0),                      # f64 records -> 8 planes per leaf
+    ("bytesplit:soa-mb", "aos-packed", 2),                      # 8 planes -> records, heatmap on dst
+])
+def test_record_plane_kernels_r64(a, b, wrap):
+    """planes.cu both directions at a size with a non-multiple-of-4 tail."""
+    rng = np.random.default_rng(15)
+    n = 4099
+    vals = random_values(rng, [9] * 7, n)
+    run_pair(R64, n, a, b, vals, src_wrap=wrap if wrap == 1 else 0, dst_wrap=wrap if wrap == 2 else 0)
+
+
 def test_untouched_bytes_survive():
     """Bytes copyView never writes keep their prior content (padding, tails)."""
     rng = np.random.default_rng(9)
