@@ -31,6 +31,7 @@ namespace lamk
         uint32_t nl, facS, facD;
     };
     bool vec_transpose(const VecParams& p, uint32_t leafSize, cudaStream_t s);
+    bool vec_convert(const VecParams& p, uint32_t ss, uint32_t ds, cudaStream_t s);
 
     struct PackParams
     {
@@ -566,6 +567,82 @@ namespace lamhost
         return true;
     }
 
+    // ChangeType f32 <-> f64 over uniform geometries (vec_transpose.cu k_vec_convert): every leaf
+    // PHYS -> PHYS with source size SS and destination size DS (4 <-> 8), one conversion
+    // f32 -> f64 or f64 -> f32 between them; each side record-contiguous or leaf-contiguous.
+    static bool tryVecConvert(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si,
+                              DeviceImage& di, const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        const uint32_t nl = p.nleaves;
+        if(nl < 1 || nl > 8 || begin % 4 || envNum("LAMB_VEC_CONVERT", 1) == 0)
+            return false;
+        const uint32_t ss = p.leaf[0].s[0].size, ds = p.leaf[0].d[0].size;
+        if(!((ss == 4 && ds == 8) || (ss == 8 && ds == 4)))
+            return false;
+        for(uint32_t f = 0; f < nl; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != ss || L.d[0].size != ds)
+                return false;
+            // exactly one f32 <-> f64 conversion on the way (storage -> logical -> storage)
+            const bool widen = ss == 4 && L.stype == F32 && L.dtype == F64 && (L.ltype == F32 || L.ltype == F64);
+            const bool narrow = ss == 8 && L.stype == F64 && L.dtype == F32 && (L.ltype == F32 || L.ltype == F64);
+            if(!(widen || narrow))
+                return false;
+        }
+        lamk::VecParams vp{};
+        auto side = [&](bool src, lamk::VecSide& sd) -> bool
+        {
+            const uint32_t S0 = src ? ss : ds;
+            const lamt_term& t0 = src ? p.leaf[0].s[0] : p.leaf[0].d[0];
+            const lamt_stream& st0 = p.st[t0.stream];
+            bool rec = st0.lanes == 1 && st0.bs == nl * S0;
+            for(uint32_t f = 0; f < nl && rec; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                rec = t.stream == t0.stream && t.inblock == f * S0;
+            }
+            if(rec)
+            {
+                sd.recordContig = 1;
+                sd.recBase = st0.gptr;
+                return (sd.recBase + begin * nl * S0) % 16 == 0;
+            }
+            sd.recordContig = 0;
+            sd.bs = st0.bs;
+            sd.lanes = st0.lanes;
+            sd.lshift = st0.lanes == 1 ? 0 : st0.lshift;
+            if(!((st0.lanes == 1 && st0.bs == S0)
+                 || (st0.lanes > 1 && st0.lanes % 4 == 0 && st0.lshift != 0xFFFFFFFFu && st0.bs % 16 == 0)))
+                return false;
+            for(uint32_t f = 0; f < nl; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                const lamt_stream& st = p.st[t.stream];
+                if(st.lanes != st0.lanes || st.bs != st0.bs || (st.lanes > 1 && t.ls != S0))
+                    return false;
+                sd.leafBase[f] = st.gptr + t.inblock;
+                if((sd.leafBase[f] + (st.lanes == 1 ? begin * S0 : 0)) % 16)
+                    return false;
+            }
+            return true;
+        };
+        if(!side(true, vp.s) || !side(false, vp.d))
+            return false;
+        vp.begin = begin;
+        vp.groups = (end - begin) / 4;
+        vp.nl = nl;
+        if(vp.groups == 0 || !lamk::vec_convert(vp, ss, ds, s))
+            return false;
+        addAccessCounts(p, S, vp.groups * 4, s);
+        const uint64_t doneEnd = begin + vp.groups * 4;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s, false),
+                           "generic_copy(tail)");
+        return true;
+    }
+
     // K3/K4: every leaf 4-byte physical (SoA or AoSoA with 32 | L) <-> bit stream of width <= 32
     static bool tryPack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
                         const Lowered& S, const Lowered& D, cudaStream_t s)
@@ -758,6 +835,8 @@ namespace lamhost
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && trySplit(p, begin, end, si, di, S, D, s))
+            return true;
+        if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
             return true;
         if(p.uni && !p.facS && !p.facD && envNum("LAMB_DIRECT", 0) != 0 && (p.ush_s != 0xFFFFFFFFu || p.ul_s == 1)
            && (p.ush_d != 0xFFFFFFFFu || p.ul_d == 1))

@@ -227,4 +227,188 @@ namespace lamk
         lam_cuda_check(cudaGetLastError(), "kernel launch");
         return true;
     }
+
+    // ---- ChangeType f32 <-> f64 on a uniform pair: the register transpose plus one conversion
+    // per value (ScalarValue::convertTo, scalar.hpp:295-306, x86 NaN rules).  A thread owns 4
+    // consecutive elements: per leaf 4 x SS bytes in, 4 x DS bytes out; record-contiguous sides
+    // move the 4 records as 16-byte vectors (destination staged through the warp's smem slice).
+    template<int SS, int DS>
+    __device__ __forceinline__ uint64_t cvt_bits(uint64_t v)
+    {
+        if constexpr(SS == 4 && DS == 8)
+            return lamd::f32_to_f64_bits(static_cast<uint32_t>(v));
+        else if constexpr(SS == 8 && DS == 4)
+            return lamd::f64_to_f32_bits(v);
+        else
+            return v;
+    }
+
+    __device__ __forceinline__ uint64_t side_off(const VecSide& sd, uint64_t e0, uint32_t size)
+    {
+        if(sd.lanes == 1)
+            return e0 * sd.bs;
+        return (e0 >> sd.lshift) * sd.bs + (e0 & (sd.lanes - 1)) * size;
+    }
+
+    template<int NL, int SS, int DS>
+    __global__ void __launch_bounds__(256) k_vec_convert(const __grid_constant__ VecParams p)
+    {
+        constexpr int NVS = NL * SS / 4, NVD = NL * DS / 4; // 16-byte vectors per 4 records
+        extern __shared__ __align__(16) uint8_t csm[];
+        const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const uint32_t lane = threadIdx.x & 31;
+        const bool live = g < p.groups;
+        const uint64_t e0 = p.begin + g * 4;
+        uint64_t v[NL][4];
+        if(live)
+        {
+            if(p.s.recordContig)
+            {
+                const uint4* base = reinterpret_cast<const uint4*>(p.s.recBase + e0 * (NL * SS));
+                uint32_t w[NVS * 4];
+#pragma unroll
+                for(int q = 0; q < NVS; ++q)
+                {
+                    const uint4 x = __ldcs(base + q);
+                    w[4 * q] = x.x;
+                    w[4 * q + 1] = x.y;
+                    w[4 * q + 2] = x.z;
+                    w[4 * q + 3] = x.w;
+                }
+#pragma unroll
+                for(int r = 0; r < 4; ++r)
+#pragma unroll
+                    for(int f = 0; f < NL; ++f)
+                    {
+                        const int k = (r * NL + f) * (SS / 4);
+                        v[f][r] = SS == 4 ? w[k] : ((uint64_t(w[k + 1]) << 32) | w[k]);
+                    }
+            }
+            else
+            {
+                const uint64_t off = side_off(p.s, e0, SS);
+#pragma unroll
+                for(int f = 0; f < NL; ++f)
+                {
+                    const uint4* b = reinterpret_cast<const uint4*>(p.s.leafBase[f] + off);
+                    const uint4 x = __ldcs(b);
+                    if constexpr(SS == 4)
+                    {
+                        v[f][0] = x.x;
+                        v[f][1] = x.y;
+                        v[f][2] = x.z;
+                        v[f][3] = x.w;
+                    }
+                    else
+                    {
+                        const uint4 y = __ldcs(b + 1);
+                        v[f][0] = (uint64_t(x.y) << 32) | x.x;
+                        v[f][1] = (uint64_t(x.w) << 32) | x.z;
+                        v[f][2] = (uint64_t(y.y) << 32) | y.x;
+                        v[f][3] = (uint64_t(y.w) << 32) | y.z;
+                    }
+                }
+            }
+#pragma unroll
+            for(int f = 0; f < NL; ++f)
+#pragma unroll
+                for(int r = 0; r < 4; ++r)
+                    v[f][r] = cvt_bits<SS, DS>(v[f][r]);
+        }
+        if(p.d.recordContig)
+        {
+            uint4* slice = reinterpret_cast<uint4*>(csm) + (threadIdx.x >> 5) * (32 * NVD);
+            if(live)
+            {
+                uint32_t w[NVD * 4];
+#pragma unroll
+                for(int r = 0; r < 4; ++r)
+#pragma unroll
+                    for(int f = 0; f < NL; ++f)
+                    {
+                        const int k = (r * NL + f) * (DS / 4);
+                        w[k] = static_cast<uint32_t>(v[f][r]);
+                        if constexpr(DS == 8)
+                            w[k + 1] = static_cast<uint32_t>(v[f][r] >> 32);
+                    }
+#pragma unroll
+                for(int q = 0; q < NVD; ++q)
+                    slice[lane * NVD + q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            }
+            __syncwarp();
+            const uint64_t warpG = g - lane;
+            const uint32_t liveLanes =
+                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            uint4* dst = reinterpret_cast<uint4*>(p.d.recBase + (p.begin + warpG * 4) * (NL * DS));
+            for(uint32_t c = lane; c < liveLanes * NVD; c += 32)
+                __stcs(dst + c, slice[c]);
+        }
+        else if(live)
+        {
+            const uint64_t off = side_off(p.d, e0, DS);
+#pragma unroll
+            for(int f = 0; f < NL; ++f)
+            {
+                uint4* b = reinterpret_cast<uint4*>(p.d.leafBase[f] + off);
+                if constexpr(DS == 4)
+                    __stcs(b, make_uint4(static_cast<uint32_t>(v[f][0]), static_cast<uint32_t>(v[f][1]),
+                                         static_cast<uint32_t>(v[f][2]), static_cast<uint32_t>(v[f][3])));
+                else
+                {
+                    __stcs(b, make_uint4(static_cast<uint32_t>(v[f][0]), static_cast<uint32_t>(v[f][0] >> 32),
+                                         static_cast<uint32_t>(v[f][1]), static_cast<uint32_t>(v[f][1] >> 32)));
+                    __stcs(b + 1, make_uint4(static_cast<uint32_t>(v[f][2]), static_cast<uint32_t>(v[f][2] >> 32),
+                                             static_cast<uint32_t>(v[f][3]), static_cast<uint32_t>(v[f][3] >> 32)));
+                }
+            }
+        }
+    }
+
+    template<int NL, int SS, int DS>
+    static void launch_convert(const VecParams& p, cudaStream_t s)
+    {
+        const size_t smem = p.d.recordContig ? 8 * 32 * (NL * DS / 4) * 16 : 0;
+        static bool attr = false;
+        if(!attr)
+        {
+            cudaFuncSetAttribute(k_vec_convert<NL, SS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            attr = true;
+        }
+        k_vec_convert<NL, SS, DS><<<stream_grid((p.groups + 255) / 256, "LAMB_VEC_CTAS", 0), 256, smem, s>>>(p);
+    }
+
+    template<int SS, int DS>
+    static bool convert_nl(const VecParams& p, cudaStream_t s)
+    {
+        switch(p.nl)
+        {
+        case 1: launch_convert<1, SS, DS>(p, s); break;
+        case 2: launch_convert<2, SS, DS>(p, s); break;
+        case 3: launch_convert<3, SS, DS>(p, s); break;
+        case 4: launch_convert<4, SS, DS>(p, s); break;
+        case 5: launch_convert<5, SS, DS>(p, s); break;
+        case 6: launch_convert<6, SS, DS>(p, s); break;
+        case 7: launch_convert<7, SS, DS>(p, s); break;
+        case 8: launch_convert<8, SS, DS>(p, s); break;
+        default: return false;
+        }
+        return true;
+    }
+
+    // groups are 4 elements; ss/ds = leaf bytes of the two sides (4 <-> 8)
+    bool vec_convert(const VecParams& p, uint32_t ss, uint32_t ds, cudaStream_t s)
+    {
+        bool ok;
+        if(ss == 4 && ds == 8)
+            ok = convert_nl<4, 8>(p, s);
+        else if(ss == 8 && ds == 4)
+            ok = convert_nl<8, 4>(p, s);
+        else
+            return false;
+        if(!ok)
+            return false;
+        count_launch();
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
+    }
 } // namespace lamk
