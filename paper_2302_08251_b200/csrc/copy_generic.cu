@@ -168,6 +168,106 @@ namespace lamk
         return cudaGetLastError();
     }
 
+    // ---- Heatmap accounting over physical terminals, blocks owned per CTA ---------------------
+    // Every terminal of the heat side is a physical byte range (PHYS leaves, ChangeType over
+    // PHYS, byte splits): a CTA takes E consecutive elements, histograms the touched blocks of
+    // one stream at a time in shared memory, then adds its counts to the global counters with
+    // a plain read-modify-write for the blocks only it can touch (interior of its byte span)
+    // and an atomic for the two edge blocks it may share with its neighbours.
+    __global__ void __launch_bounds__(256) k_heat_phys(const __grid_constant__ HeatParams p)
+    {
+        extern __shared__ unsigned long long hist[];
+        const uint64_t cb = p.begin + static_cast<uint64_t>(blockIdx.x) * p.E;
+        const uint64_t ce = cb + p.E < p.end ? cb + p.E : p.end;
+        for(uint32_t si = 0; si < p.nstreams; ++si)
+        {
+            const HeatStream& st = p.st[si];
+            const uint64_t lo = st.base0 + (cb / st.lanes) * st.bs;
+            const uint64_t hi = st.base0 + ((ce + st.lanes - 1) / st.lanes) * st.bs;
+            const uint64_t b0 = lo / p.gran, b1 = (hi - 1) / p.gran;
+            const uint32_t W = static_cast<uint32_t>(b1 - b0 + 1);
+            for(uint32_t w = threadIdx.x; w < W; w += blockDim.x)
+                hist[w] = 0;
+            __syncthreads();
+            // each thread walks a contiguous run of elements: block indices mostly repeat, so
+            // touches are run-length combined before the shared-memory atomic
+            const uint64_t per = (ce - cb + blockDim.x - 1) / blockDim.x;
+            const uint64_t eb = cb + threadIdx.x * per, ee = eb + per < ce ? eb + per : ce;
+            uint64_t cur = ~0ull;
+            unsigned long long run = 0;
+            for(uint64_t e = eb; e < ee; ++e)
+            {
+                uint64_t blk, lane;
+                if(st.lanes == 1)
+                {
+                    blk = e;
+                    lane = 0;
+                }
+                else if(st.lshift != 0xFFFFFFFFu)
+                {
+                    blk = e >> st.lshift;
+                    lane = e & (st.lanes - 1);
+                }
+                else
+                {
+                    blk = e / st.lanes;
+                    lane = e - blk * st.lanes;
+                }
+                for(uint32_t t = st.t0; t < st.t1; ++t)
+                {
+                    const HeatTerm& ht = p.term[t];
+                    const uint64_t a = st.base0 + blk * st.bs + ht.inblock + lane * ht.ls;
+                    const uint64_t f = p.gshift < 64 ? a >> p.gshift : a / p.gran;
+                    const uint64_t l = p.gshift < 64 ? (a + ht.size - 1) >> p.gshift : (a + ht.size - 1) / p.gran;
+                    for(uint64_t b = f; b <= l; ++b)
+                    {
+                        if(b == cur)
+                            ++run;
+                        else
+                        {
+                            if(run)
+                                atomicAdd(&hist[cur - b0], run);
+                            cur = b;
+                            run = 1;
+                        }
+                    }
+                }
+            }
+            if(run)
+                atomicAdd(&hist[cur - b0], run);
+            __syncthreads();
+            unsigned long long* heat = p.heat + p.heatOff[st.nr];
+            for(uint32_t w = threadIdx.x; w < W; w += blockDim.x)
+            {
+                const unsigned long long c = hist[w];
+                if(!c)
+                    continue;
+                if(w == 0 || w == W - 1)
+                    atomicAdd(heat + b0 + w, c);
+                else
+                    heat[b0 + w] += c;
+            }
+            __syncthreads();
+        }
+    }
+
+    cudaError_t heat_phys(const HeatParams& p, cudaStream_t s)
+    {
+        if(p.end <= p.begin || p.nstreams == 0)
+            return cudaSuccess;
+        const uint64_t ctas = (p.end - p.begin + p.E - 1) / p.E; // E is sized on the host
+        const size_t smem = static_cast<size_t>(p.maxWindow) * sizeof(unsigned long long);
+        static size_t attr = 0;
+        if(attr < smem)
+        {
+            cudaFuncSetAttribute(k_heat_phys, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr = smem;
+        }
+        k_heat_phys<<<static_cast<unsigned>(ctas), 256, smem, s>>>(p);
+        count_launch();
+        return cudaGetLastError();
+    }
+
     __global__ void k_fac_add(unsigned long long* src, unsigned long long* dst, uint32_t nl, unsigned long long cnt)
     {
         for(uint32_t f = threadIdx.x; f < nl; f += blockDim.x)

@@ -782,6 +782,94 @@ namespace lamhost
                                const Lowered& D, DeviceImage& di, const std::vector<uint8_t*>& dptr, uint64_t begin,
                                uint64_t end, cudaStream_t s);
 
+    // Heatmap accounting when every terminal of the side is a physical byte range (PHYS leaves,
+    // ChangeType over PHYS, byte splits): copy_generic.cu k_heat_phys.  False = not eligible.
+    static bool heatPhys(const Lowered& L, const DeviceImage& img, uint64_t begin, uint64_t end, cudaStream_t s)
+    {
+        if(envNum("LAMB_HEAT_PHYS", 1) == 0 || !img.heat || L.heatGran == 0)
+            return false;
+        std::vector<std::vector<lamk::HeatTerm>> perStream(L.streams.size());
+        std::vector<uint32_t> stack;
+        for(uint16_t r : L.roots)
+        {
+            stack.assign(1, r);
+            while(!stack.empty())
+            {
+                const lamp_node& nd = L.nodes[stack.back()];
+                stack.pop_back();
+                switch(nd.kind)
+                {
+                case LAMP_PHYS:
+                    perStream[nd.stream].push_back({nd.a, nd.b, static_cast<uint32_t>(scalarSize(nd.type))});
+                    break;
+                case LAMP_CONVERT:
+                    stack.push_back(nd.child);
+                    break;
+                case LAMP_SPLIT:
+                    for(uint32_t k = 0; k < nd.nchild; ++k)
+                        stack.push_back(nd.child + k);
+                    break;
+                case LAMP_NULL:
+                    break;
+                default:
+                    return false; // bit streams: the generic range pass
+                }
+            }
+        }
+        lamk::HeatParams hp{};
+        hp.heat = static_cast<unsigned long long*>(img.heat);
+        hp.heatOff = reinterpret_cast<const uint64_t*>(static_cast<const uint8_t*>(img.mem) + img.offHeatOff);
+        hp.begin = begin;
+        hp.end = end;
+        hp.gran = L.heatGran;
+        hp.gshift = 64;
+        if((L.heatGran & (L.heatGran - 1)) == 0)
+            for(uint32_t k = 0; k < 64; ++k)
+                if((uint64_t{1} << k) == L.heatGran)
+                    hp.gshift = k;
+        const uint32_t maxW = 6144;
+        uint64_t E = 1u << 16, unit = 1;
+        uint32_t nt = 0;
+        for(size_t k = 0; k < L.streams.size(); ++k)
+        {
+            if(perStream[k].empty())
+                continue;
+            const lamp_stream& st = L.streams[k];
+            if(st.kind != LAMS_PHYS || hp.nstreams >= 64 || nt + perStream[k].size() > 256)
+                return false;
+            lamk::HeatStream& h = hp.st[hp.nstreams++];
+            h.base0 = st.base0;
+            h.bs = st.block_stride;
+            h.lanes = st.lanes;
+            h.lshift = st.lane_shift;
+            h.nr = st.nr;
+            h.t0 = nt;
+            for(const auto& t : perStream[k])
+                hp.term[nt++] = t;
+            h.t1 = nt;
+            // elements per CTA such that the block window of this stream fits in maxW counters
+            const uint64_t e = (maxW - 4) * L.heatGran * st.lanes / st.block_stride;
+            E = std::min<uint64_t>(E, e);
+            unit = lcm64(unit, st.lanes);
+        }
+        if(hp.nstreams == 0)
+            return true; // nothing physical to touch (Null leaves only)
+        // enough CTAs to fill the SMs (several per SM), each element run still long enough
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t fill = (end - begin) / (static_cast<uint64_t>(lamk::sm_count(dev)) * 8);
+        if(fill >= 4096 && fill < E)
+            E = fill;
+        E = E / unit * unit;
+        if(E < 64 || begin % unit)
+            return false;
+        hp.E = E;
+        hp.maxWindow = maxW;
+        lam_cuda_check(lamk::heat_phys(hp, s), "heat_phys");
+        return true;
+    }
+
+
     // the data moves through the tile kernels (none of which counts heat); a Heatmap on either
     // side is then accounted over the whole range in one pass that touches ranges, not data
     static bool launchTile(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr, const Lowered& D,
@@ -791,9 +879,9 @@ namespace lamhost
         if(!launchTileData(S, si, sptr, D, di, dptr, begin, end, s))
             return false;
         const uint32_t nl = static_cast<uint32_t>(S.roots.size());
-        if(S.heat)
+        if(S.heat && !heatPhys(S, si, begin, end, s))
             lam_cuda_check(lamk::heat_account(si.hdr, begin, end, nl, s), "heat_account(src)");
-        if(D.heat)
+        if(D.heat && !heatPhys(D, di, begin, end, s))
             lam_cuda_check(lamk::heat_account(di.hdr, begin, end, nl, s), "heat_account(dst)");
         return true;
     }

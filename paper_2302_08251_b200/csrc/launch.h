@@ -33,6 +33,28 @@ namespace lamk
     // plan interpreter on both sides (copy_generic.cu)
     cudaError_t generic_copy(const lamp_view* src, const lamp_view* dst, uint64_t begin, uint64_t end,
                              uint32_t nleaves, bool facSrc, bool facDst, cudaStream_t s, bool countHeat = true);
+    // Heatmap accounting when every terminal of the side is a physical byte range
+    struct HeatTerm
+    {
+        uint32_t inblock, ls, size;
+    };
+    struct HeatStream
+    {
+        uint64_t base0, bs, lanes;
+        uint32_t lshift, nr, t0, t1; // terms [t0, t1) live on this stream
+    };
+    struct HeatParams
+    {
+        unsigned long long* heat;
+        const uint64_t* heatOff; // device: first counter of blob nr
+        uint64_t begin, end, E, gran;
+        uint32_t gshift; // log2(gran) when a power of two, else 64
+        uint32_t nstreams, maxWindow;
+        HeatStream st[64];
+        HeatTerm term[256];
+    };
+    cudaError_t heat_phys(const HeatParams& p, cudaStream_t s);
+
     // Heatmap accounting of a copy over [begin, end) whose data moved through a fast kernel
     cudaError_t heat_account(const lamp_view* v, uint64_t begin, uint64_t end, uint32_t nleaves, cudaStream_t s);
     // byte-exact blob copy (copyView's sameLayout memcpy path)
