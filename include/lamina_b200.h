@@ -101,6 +101,12 @@ int lam_layout_physical_offset(const lam_layout* layout, uint64_t linear, size_t
                                uint64_t* offset);
 /* Heatmap::blockCount summed over blobs (instrument.hpp:107); 0 when not wrapped. */
 uint64_t lam_layout_heatmap_blocks(const lam_layout* layout, size_t nr);
+/* Mapping::contiguousRun (core/include/lamina/mapping.hpp:122-135, mappings.cpp:44-50,96-101,
+ * 140-148, computed.cpp:386-394): *has_run = 1 and (nr, offset) of element `linear` when the n
+ * values of leaf `flat_leaf` starting there are contiguous with stride = leaf size; 0 otherwise
+ * (computed leaves, counting wrappers, strided AoS runs, runs crossing an AoSoA block). */
+int lam_layout_contiguous_run(const lam_layout* layout, uint64_t linear, size_t flat_leaf, uint64_t n, int* has_run,
+                              size_t* nr, uint64_t* offset);
 /* Element alignment unit for sharding/chunking: every multiple of it starts every blob
  * stream on a 16-byte boundary (AoSoA lanes, bit-stream words). */
 uint64_t lam_layout_shard_unit(const lam_layout* layout);

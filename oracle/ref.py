@@ -61,6 +61,8 @@ def lib():
         L.ref_nbody.argtypes = [cp, u64, u64, i32, u64, i32, i32, P(vp), P(dbl), P(dbl), P(dbl)]
         L.ref_nbody_cli.argtypes = [cp, u64, u64, i32, u64, i32]
         L.ref_nbody_trace.argtypes = [cp, u64, u64, i32, u64, i32, u64, cp, cp]
+        L.ref_contiguous_run.argtypes = [cp, cp, P(u64), C.c_size_t, cp, i32, u64, u64, C.c_size_t, u64, P(C.c_int),
+                                         P(C.c_size_t), P(u64)]
         _lib = L
     return _lib
 
@@ -198,3 +200,12 @@ def nbody_trace(layout, n, steps, report_dir, trace=True, heat_gran=0, f64=False
                                str(report_dir).encode(), csv_path.encode() if csv_path else None)
     if rc != 0:
         raise RefError(5, f"ref_nbody_trace exit code {rc}")
+
+
+def contiguous_run(schema, extents, layout, linear, leaf, n, dyn=(), wrap=0, gran=1):
+    """Mapping::contiguousRun of the reference: (nr, offset) or None."""
+    d, nd = _dyn(dyn)
+    has, nr, off = C.c_int(), C.c_size_t(), C.c_uint64()
+    _check(lib().ref_contiguous_run(schema.encode(), extents.encode(), d, nd, layout.encode(), wrap, gran, linear, leaf,
+                                    n, C.byref(has), C.byref(nr), C.byref(off)))
+    return (nr.value, off.value) if has.value else None

@@ -584,6 +584,25 @@ extern "C"
         return nbody::runBenchmark(cfg);
     }
 
+    // Mapping::contiguousRun of the reference mapping (mapping.hpp:122-135)
+    int ref_contiguous_run(const char* schema, const char* extents, const std::uint64_t* dyn, std::size_t ndyn,
+                           const char* layout, int wrap, std::uint64_t gran, std::uint64_t linear, std::size_t leaf,
+                           std::uint64_t n, int* has, std::size_t* nr, std::uint64_t* off)
+    {
+        return guarded(
+            [&]
+            {
+                const MappingPtr m = makeMapping(schema, extents, dyn, ndyn, layout, wrap, gran);
+                const auto run = m->contiguousRun(linear, leaf, n);
+                *has = run ? 1 : 0;
+                if(run)
+                {
+                    *nr = run->nr;
+                    *off = run->offset;
+                }
+            });
+    }
+
     // the runner with --trace-fields / --heatmap <g>: writes fields_{update,move}.csv and
     // heatmap_{update,move}.csv into reportDir (runner.cpp:344-436)
     int ref_nbody_trace(const char* layout, std::uint64_t n, std::uint64_t steps, int f64, std::uint64_t seed,

@@ -49,6 +49,7 @@ _SIGS = {
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
     "lam_view_device_plan": (vp, [vp]),
+    "lam_layout_contiguous_run": (i32, [vp, u64, sz, u64, C.POINTER(C.c_int), C.POINTER(sz), C.POINTER(u64)]),
     "lam_layout_dump_meta": (sz, [vp, cp, sz]),
     "lam_view_dump": (i32, [vp, cp]),
     "lam_view_restore": (i32, [cp, i32, vp, C.POINTER(vp), C.POINTER(vp)]),

@@ -322,6 +322,42 @@ extern "C"
             });
     }
 
+    int lam_layout_contiguous_run(const lam_layout* l, uint64_t i, size_t f, uint64_t n, int* has, size_t* nr,
+                                  uint64_t* off)
+    {
+        return guard(
+            [&]
+            {
+                const Lowered& L = *l->L;
+                const auto& m = *L.map;
+                if(f >= m.schema().leafCount())
+                    throw std::out_of_range("index out of range: leaf " + std::to_string(f));
+                if(i >= m.elementCount())
+                    throw std::out_of_range("index out of range: element " + std::to_string(i));
+                *has = 0;
+                // counting wrappers and computed leaves want per-element access (mapping.hpp:122-135)
+                if(L.fac || L.heat)
+                    return;
+                const lamp_node& nd = L.nodes[L.roots[f]];
+                if(nd.kind != LAMP_PHYS)
+                    return;
+                const lamp_stream& st = L.streams[nd.stream];
+                const uint64_t size = scalarSize(nd.type);
+                bool run = n <= 1;
+                if(st.lanes == 1)
+                    run = run || st.block_stride == size;                   // SoA; AoS of one leaf (mappings.cpp:44-50,96-101)
+                else
+                    run = run || (st.block_stride == st.lanes * size && nd.b == size) // one-leaf AoSoA
+                        || (i % st.lanes + n <= st.lanes);                   // inside one block (mappings.cpp:140-148)
+                if(!run)
+                    return;
+                const auto o = m.offsetOf(i, f);
+                *has = 1;
+                *nr = o.first;
+                *off = o.second;
+            });
+    }
+
     uint64_t lam_layout_heatmap_blocks(const lam_layout* l, size_t nr)
     {
         if(!l->L->heat || nr >= l->L->map->blobCount())

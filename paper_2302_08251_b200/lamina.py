@@ -112,6 +112,12 @@ class Layout:
         self.dyn = ()
         return self
 
+    def contiguous_run(self, linear: int, leaf: int, n: int):
+        """Mapping::contiguousRun: (nr, offset) when n values of the leaf are contiguous, else None."""
+        has, nr, off = C.c_int(), C.c_size_t(), C.c_uint64()
+        _check(lib().lam_layout_contiguous_run(self._h, linear, leaf, n, C.byref(has), C.byref(nr), C.byref(off)))
+        return (nr.value, off.value) if has.value else None
+
     def dump_meta(self) -> str:
         """The .meta sidecar text writeViewDump writes for a view of this layout (view_io.cpp:30-44)."""
         return _str(lib().lam_layout_dump_meta, self._h)

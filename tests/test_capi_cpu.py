@@ -174,3 +174,25 @@ def test_restore_missing_dump(tmp_path):
     from paper_2302_08251_b200 import lamina as L
     with pytest.raises(L.ReferenceRuntimeError, match="cannot read"):
         L.read_view_dump(str(tmp_path / "absent"))
+
+
+# ---- Mapping::contiguousRun vs the compiled reference ---------------------------------------
+@pytest.mark.parametrize("layout", ["aos-packed", "soa-sb", "soa-mb", "aosoa:8", "aosoa:3", "split:Pos:soa-mb:aos-packed",
+                                    "changetype:f32=f64:soa-mb", "changetype:f32=f32:aosoa:4", "bytesplit:soa-mb",
+                                    "bitpack-float:8,23", "soa-mb+fac", "aos-packed+heat", "null"])
+@pytest.mark.parametrize("schema", ["R32", "ONE"])
+def test_contiguous_run_matches_reference(layout, schema, ref):
+    from paper_2302_08251_b200 import lamina as L
+    sch = R32 if schema == "R32" else "Record{v:f32}"
+    ext = "i32:[37]"
+    wrap = 1 if layout.endswith("+fac") else (2 if layout.endswith("+heat") else 0)
+    layout = layout.split("+")[0]
+    if schema == "ONE" and "Pos" in layout:
+        pytest.skip("split selects a field of R32")
+    lay = L.Layout(sch, ext, layout, wrap=wrap, granularity=8)
+    nl = lay.leaf_count
+    for linear in (0, 1, 5, 7, 8, 30, 36):
+        for f in range(nl):
+            for n in (0, 1, 2, 3, 8, 37 - linear):
+                want = ref.contiguous_run(sch, ext, layout, linear, f, n, wrap=wrap, gran=8)
+                assert lay.contiguous_run(linear, f, n) == want, (layout, linear, f, n)
