@@ -199,6 +199,19 @@ int lam_nbody_init(lam_view* view, uint64_t seed, void* stream);
 int lam_nbody_update(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_move(lam_view* view, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_checksum(const lam_view* view, double* out);
+/* The fused multi-GPU update step: elements [i_begin, i_end) of `view` against j-sources read
+ * directly from other views -- view k supplies particles [j_begin[k], j_end[k]) (global indices,
+ * visited in the given order, so exact mode matches the single-view update when the ranges tile
+ * [0, n) in order).  Peer GPUs' shards are mapped with lam_ipc_open and wrapped as views
+ * (lam_view_wrap) on the updating device: the all-gather of the reference's one-process loop
+ * (steps.hpp:13-42) becomes NVLink loads inside the update kernel.  Up to 64 sources. */
+int lam_nbody_update_multi(lam_view* view, const lam_view* const* j_views, const uint64_t* j_begin,
+                           const uint64_t* j_end, size_t n_sources, int mode, uint64_t i_begin, uint64_t i_end,
+                           void* stream);
+/* CUDA IPC of device allocations (64-byte handles) for the fused multi-GPU step. */
+int lam_ipc_get_handle(const void* device_ptr, void* handle64_out);
+int lam_ipc_open(const void* handle64, int device, void** device_ptr);
+int lam_ipc_close(void* device_ptr);
 
 /* ---- misc ------------------------------------------------------------------------------- */
 /* Number of kernels this library launched on the calling process (all devices). */

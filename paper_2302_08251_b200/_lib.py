@@ -49,6 +49,10 @@ _SIGS = {
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
     "lam_view_device_plan": (vp, [vp]),
+    "lam_nbody_update_multi": (i32, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), sz, i32, u64, u64, vp]),
+    "lam_ipc_get_handle": (i32, [vp, vp]),
+    "lam_ipc_open": (i32, [vp, i32, C.POINTER(vp)]),
+    "lam_ipc_close": (i32, [vp]),
     "lam_layout_contiguous_run": (i32, [vp, u64, sz, u64, C.POINTER(C.c_int), C.POINTER(sz), C.POINTER(u64)]),
     "lam_layout_dump_meta": (sz, [vp, cp, sz]),
     "lam_view_dump": (i32, [vp, cp]),

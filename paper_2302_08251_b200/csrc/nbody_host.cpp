@@ -3,6 +3,7 @@
 
 #include <cstring>
 #include <random>
+#include <vector>
 
 namespace lamk
 {
@@ -10,6 +11,9 @@ namespace lamk
                              cudaStream_t s);
     cudaError_t nbody_move(const lamp_view* v, bool f64, bool phys, uint64_t ib, uint64_t ie, cudaStream_t s);
     cudaError_t nbody_account(const lamp_view* v, bool move, uint64_t n, uint64_t ib, uint64_t ie, cudaStream_t s);
+    cudaError_t nbody_update_multi(const lamp_view* v, bool f64, bool exact, bool phys, const lamp_view* const* jv,
+                                   const uint64_t* jb, const uint64_t* je, size_t nj, uint64_t ib, uint64_t ie,
+                                   cudaStream_t s);
 } // namespace lamk
 
 using namespace lamb;
@@ -163,6 +167,74 @@ extern "C"
                     lam_cuda_check(lamk::nbody_account(v->img.hdr, false, n, ib, ie, static_cast<cudaStream_t>(stream)),
                                    "nbody_account");
             });
+    }
+
+    int lam_nbody_update_multi(lam_view* v, const lam_view* const* jviews, const uint64_t* jbegin, const uint64_t* jend,
+                               size_t nj, int mode, uint64_t ib, uint64_t ie, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                const uint64_t n = v->L->map->elementCount();
+                if(ib > ie || ie > n)
+                    throw std::out_of_range("index out of range: particles [" + std::to_string(ib) + ", "
+                                            + std::to_string(ie) + ")");
+                if(nj == 0 || nj > 64 || !jviews || !jbegin || !jend)
+                    throw std::invalid_argument("n-body j-sources: 1..64 views with ranges");
+                if(v->L->fac || v->L->heat)
+                    throw std::invalid_argument("instrumented views: use lam_nbody_update (single view)");
+                bool phys = particlePhys(v);
+                std::vector<const lamp_view*> hdr(nj);
+                for(size_t k = 0; k < nj; ++k)
+                {
+                    const lam_view* j = jviews[k];
+                    if(!(j->L->map->schema() == v->L->map->schema()) || !(j->L->map->extents() == v->L->map->extents()))
+                        throw std::invalid_argument("incompatible views");
+                    if(j->device != v->device)
+                        throw std::invalid_argument("j-source views must live on the updating device (wrap peer memory)");
+                    if(j->L->fac || j->L->heat)
+                        throw std::invalid_argument("instrumented views: use lam_nbody_update (single view)");
+                    if(jbegin[k] > jend[k] || jend[k] > n)
+                        throw std::out_of_range("index out of range: j-source range");
+                    phys = phys && particlePhys(j);
+                    hdr[k] = j->img.hdr;
+                }
+                DeviceGuard g(v->device);
+                lam_cuda_check(lamk::nbody_update_multi(v->img.hdr, f64, mode == LAM_NBODY_EXACT, phys, hdr.data(), jbegin,
+                                                        jend, nj, ib, ie, static_cast<cudaStream_t>(stream)),
+                               "nbody_update_multi");
+            });
+    }
+
+    // CUDA IPC for the fused multi-GPU n-body step: a rank exports its blob allocations, the
+    // others map them and wrap them as views (lam_view_wrap) on their own device
+    int lam_ipc_get_handle(const void* device_ptr, void* handle_out)
+    {
+        return guard2(
+            [&]
+            {
+                cudaIpcMemHandle_t h;
+                lam_cuda_check(cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)), "cudaIpcGetMemHandle");
+                std::memcpy(handle_out, &h, sizeof(h));
+            });
+    }
+
+    int lam_ipc_open(const void* handle, int device, void** device_ptr)
+    {
+        return guard2(
+            [&]
+            {
+                DeviceGuard g(device);
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, handle, sizeof(h));
+                lam_cuda_check(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            });
+    }
+
+    int lam_ipc_close(void* device_ptr)
+    {
+        return guard2([&] { lam_cuda_check(cudaIpcCloseMemHandle(device_ptr), "cudaIpcCloseMemHandle"); });
     }
 
     int lam_nbody_move(lam_view* v, uint64_t ib, uint64_t ie, void* stream)

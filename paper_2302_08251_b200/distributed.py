@@ -49,11 +49,18 @@ def allgather_regions(layout, blobs, world: int, group=None):
 
 
 def nbody_distributed(layout_text: str, n: int, steps: int, mode: int = 0, seed: int = 42, f64: bool = False,
-                      group=None):
+                      group=None, transport: str = "allgather"):
     """Run the n-body benchmark with the particles sharded over the process group.
+
+    transport "allgather": every rank updates and moves its i-shard, then the shards' blob
+    regions are all-gathered (NCCL over NVLink).  transport "p2p": the fused step -- every
+    rank maps its peers' views (CUDA IPC) and the update kernel reads their positions over
+    NVLink directly (lam_nbody_update_multi); a barrier separates update and move.
 
     Returns (view, blobs): the view holds the whole replicated state after the last step.
     """
+    if transport == "p2p":
+        return _nbody_p2p(layout_text, n, steps, mode, seed, f64, group)
     import torch
     import torch.distributed as dist
 
@@ -74,3 +81,46 @@ def nbody_distributed(layout_text: str, n: int, steps: int, mode: int = 0, seed:
         allgather_regions(lay, blobs, world, group)
     torch.cuda.synchronize()
     return view, blobs
+
+
+def _nbody_p2p(layout_text, n, steps, mode, seed, f64, group):
+    import torch
+    import torch.distributed as dist
+
+    from . import lamina as L
+    t = "f64" if f64 else "f32"
+    schema = f"Record{{Pos:Record{{x:{t},y:{t},z:{t}}},Vel:Record{{x:{t},y:{t},z:{t}}},Mass:{t}}}"
+    lay = L.Layout(schema, f"i64:[{n}]", layout_text)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = torch.cuda.current_device()
+    view = L.View(lay, device=dev)  # cudaMalloc'd blobs: IPC handles cover them exactly
+    view.nbody_init(seed)
+    torch.cuda.synchronize()
+    handles = [L.ipc_handle(view.blob_ptr(nr)) for nr in range(lay.blob_count) if lay.blob_sizes[nr]]
+    everyone = [None] * world
+    dist.all_gather_object(everyone, handles, group=group)
+    ranges = [shard_range(n, lay.shard_unit, r, world) for r in range(world)]
+    peers, mapped = {}, []
+    for r in range(world):
+        if r == rank:
+            continue
+        ptrs = [L.ipc_open(h, dev) for h in everyone[r]]
+        mapped += ptrs
+        peers[r] = L.View(lay, device=dev, blobs=ptrs, blob_bytes=[s for s in lay.blob_sizes if s])
+    sources = [(view if r == rank else peers[r], lo, hi) for r, (lo, hi) in enumerate(ranges)]
+    lo, hi = ranges[rank]
+    for _ in range(steps):
+        view.nbody_update_from(sources, mode, lo, hi)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every rank has read the positions before anyone moves
+        view.nbody_move(lo, hi)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+    for r, pv in peers.items():  # replicate the final state locally (NVLink reads)
+        L.copy_view_range(pv, view, *ranges[r])
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+    del peers
+    for p in mapped:
+        L.ipc_close(p)
+    return view, None

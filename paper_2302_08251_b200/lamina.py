@@ -345,6 +345,16 @@ class View:
         end = self.layout.element_count if end is None else end
         _check(lib().lam_nbody_move(self._h, begin, end, _stream_handle(stream)))
 
+    def nbody_update_from(self, sources, mode: int = NBODY_EXACT, begin: int = 0, end: int | None = None,
+                          stream=None) -> None:
+        """Fused update: j-particles read from other views, sources = [(view, j_begin, j_end), ...]."""
+        end = self.layout.element_count if end is None else end
+        k = len(sources)
+        hv = (C.c_void_p * k)(*[v.handle for v, _, _ in sources])
+        jb = (C.c_uint64 * k)(*[int(b) for _, b, _ in sources])
+        je = (C.c_uint64 * k)(*[int(e) for _, _, e in sources])
+        _check(lib().lam_nbody_update_multi(self._h, hv, jb, je, k, mode, begin, end, _stream_handle(stream)))
+
     def nbody_checksum(self) -> float:
         out = C.c_double()
         _check(lib().lam_nbody_checksum(self._h, C.byref(out)))
@@ -365,6 +375,24 @@ def read_view_dump(stem: str, device: int = 0, stream=None) -> View:
     v.device = device
     v._h = vh
     return v
+
+
+def ipc_handle(device_ptr: int) -> bytes:
+    """cudaIpcGetMemHandle of a device allocation (64 bytes)."""
+    buf = C.create_string_buffer(64)
+    _check(lib().lam_ipc_get_handle(C.c_void_p(device_ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map a peer allocation into this process (cudaIpcOpenMemHandle, lazy peer access)."""
+    p = C.c_void_p()
+    _check(lib().lam_ipc_open(C.create_string_buffer(handle, 64), device, C.byref(p)))
+    return p.value or 0
+
+
+def ipc_close(device_ptr: int) -> None:
+    _check(lib().lam_ipc_close(C.c_void_p(device_ptr)))
 
 
 def copy_view(src: View, dst: View, stream=None) -> None:
