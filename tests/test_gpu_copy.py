@@ -237,3 +237,29 @@ def test_restore_and_redump_reference_files(case, tmp_path):
     L.copy_view(v, dst)
     md = O.make(case["schema"], case["extents"], "aos-packed", dyn=case["dyn"])
     assert np.array_equal(O.read_all(md, dst.download_all()), want)
+
+
+@pytest.mark.parametrize("ext,dyn", [("u16:[4,dyn,5]", [7]), ("i16:[3,3,3]", []), ("u64:[dyn]", [1234]),
+                                      ("u32:[11,dyn]", [9])])
+@pytest.mark.parametrize("a,b", [("aos-packed", "soa-mb"), ("soa-sb", "aosoa:4"), ("aos-aligned", "bytesplit:soa-mb"),
+                                 ("soa-mb", "changetype:f64=f32,i8=i64:aosoa:2")])
+def test_copy_multidim_extents(ext, dyn, a, b):
+    """Row-major linear index over multi-dimensional, dynamic and small-index-type extents
+    (extents.cpp:94-103): the copy sees the same element order as the reference."""
+    L = lm()
+    rng = np.random.default_rng(3)
+    ms = O.make(MIXED, ext, a, dyn=dyn)
+    md = O.make(MIXED, ext, b, dyn=dyn)
+    n = ms.n
+    types = [l.type for l in O.Schema.parse(MIXED).leaves]
+    vals = random_values(rng, types, n)
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    db = O.zero_blobs(md)
+    O.copy_view(ms, sb, md, db)
+    gs = L.View(L.Layout(MIXED, ext, a, dyn=dyn))
+    gd = L.View(L.Layout(MIXED, ext, b, dyn=dyn))
+    gs.upload_all(sb)
+    L.copy_view(gs, gd)
+    for x, y in zip(gd.download_all(), db):
+        assert np.array_equal(x, y)
