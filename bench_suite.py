@@ -54,6 +54,56 @@ OTHER_PAIRS = [  # compositions outside the BASELINE configs (informative)
 ]
 
 
+def cpu_reference(parts):
+    """The reference's CPU path (oracle/_ref, the unmodified library) on bounded samples of each
+    config, on 1 core (as shipped) and on every host core (the loop body over disjoint ranges,
+    SURVEY 8(d) variant ii), timed on this box in the same run."""
+    import os
+
+    import numpy as np
+    from oracle import ref
+    if not ref.available():
+        return {"unavailable": "oracle/_ref not built"}
+    cores = os.cpu_count() or 1
+    out = {"cores_all": cores}
+    rng = np.random.default_rng(1)
+
+    def copy_rate(schema, n, a, b, bytes_per, wrap=0, threads=1):
+        ext = f"i32:[{n}]"
+        src = [rng.integers(0, 256, sz, dtype=np.uint8) for sz in ref.layout_info(schema, ext, a)["blob_sizes"]]
+        if "Record{v:f32}" in schema or schema == R64:
+            # finite float values so the minifloat / conversion paths see real numbers
+            vals = (rng.standard_normal(n * (7 if schema == R64 else 1)) * 100)
+            src = ref.write_values(schema, ext, a, (vals.astype(np.float64 if schema == R64 else np.float32)
+                                                    .view(np.uint64 if schema == R64 else np.uint32)
+                                                    .astype(np.uint64).reshape(n, -1)))
+        dst = ref.zero_blobs(schema, ext, b)
+        r = ref.copy(schema, ext, a, src, b, dst, dst_wrap=wrap, nthreads=threads)
+        return bytes_per * n / r["seconds"] / 1e9
+
+    if "C3" in parts:
+        c3 = {}
+        for bits in (3, 12, 31):
+            byt = 4 + bits / 8
+            c3[f"int{bits}_pack_GB/s"] = {t: copy_rate("Record{v:u32}", 1 << 22, "soa-mb", f"bitpack-int:{bits}", byt,
+                                                       threads=t) for t in (1, cores)}
+        c3["e8m10_pack_GB/s"] = {t: copy_rate("Record{v:f32}", 1 << 21, "soa-mb", "bitpack-float:8,10", 4 + 19 / 8,
+                                              threads=t) for t in (1, cores)}
+        out["C3"] = dict(c3, sample="2^22 (int) / 2^21 (float) values per measurement")
+    if "C4" in parts:
+        c4 = {}
+        for t in (1, cores):
+            n = 16384 if t == 1 else 65536
+            _, _, us, _ = ref.nbody("soa-mb", n, 1, seed=42, nthreads=t, with_blobs=False)
+            c4[t] = n * n / us
+        out["C4_interactions/s"] = dict(c4, sample="one update step, soa-mb, N=16384 (1 core) / 65536 (all cores)")
+    if "C5" in parts:
+        out["C5_GB/s"] = {t: copy_rate(R64, 1 << 20, "aos-packed", "changetype:f64=f32:bytesplit:soa-mb", 84, wrap=1,
+                                       threads=t) for t in (1, cores)}
+        out["C5_sample"] = "2^20 records per measurement"
+    return out
+
+
 def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")):
     import torch
     out = {}
@@ -152,6 +202,7 @@ def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")
                 "GB/s": byt / ms / 1e6, "frac": byt / ms / 1e6 / peak_gbs}
             del s, d
         out["C6_other_compositions_2^26"] = c6
+    out["cpu_reference"] = cpu_reference(parts)
     return out
 
 

@@ -22,3 +22,5 @@ for k, v in c4.items():
 print("C4 peak", c4.get("fp32_peak_measured_tflops"), c4.get("clocks_during_nbody"))
 for k, v in (s.get("C6_other_compositions_2^26") or {}).items():
     print("C6", k, round(v["GB/s"]), round(v["frac"], 3))
+if s.get("cpu_reference"):
+    print("cpu_reference", json.dumps(s["cpu_reference"]))
