@@ -367,6 +367,7 @@ def main():
                         "achieved": res["achieved_tile"], "peak": peak, "unit": "GB/s",
                         "frac": res["achieved_tile"] / peak, "traffic": traffic,
                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                        "spec_peak_GBps": 8000.0, "frac_of_spec": res["achieved_tile"] / 8000.0,
                         "algorithmic_bytes_per_launch": 56 * n}
     line["per_pair_gbs"] = res["per_pair_gbs"]
     if not args.no_e2e:
