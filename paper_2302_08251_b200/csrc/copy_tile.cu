@@ -738,8 +738,17 @@ namespace lamk
     // the smem image.  Handles PHYS <-> PHYS (any sizes, with conversion) and PHYS <-> SPLIT
     // (byte planes; 4 elements per lane so each plane gets one 32-bit smem access when the
     // planes are packed arrays).  Returns false for anything else (the generic loop runs).
+    // size | 0x80: the term is not naturally aligned in the smem image (packed AoS of mixed
+    // leaf sizes): byte-wise little-endian access
     __device__ __forceinline__ uint64_t wt_ld(const uint8_t* b, uint32_t size)
     {
+        if(size & 0x80)
+        {
+            uint64_t v = 0;
+            for(uint32_t k = 0; k < (size & 0x7F); ++k)
+                v |= uint64_t(b[k]) << (8 * k);
+            return v;
+        }
         switch(size)
         {
         case 1: return *b;
@@ -751,6 +760,12 @@ namespace lamk
 
     __device__ __forceinline__ void wt_st(uint8_t* b, uint32_t size, uint64_t v)
     {
+        if(size & 0x80)
+        {
+            for(uint32_t k = 0; k < (size & 0x7F); ++k)
+                b[k] = static_cast<uint8_t>(v >> (8 * k));
+            return;
+        }
         switch(size)
         {
         case 1: *b = static_cast<uint8_t>(v); break;
@@ -778,6 +793,41 @@ namespace lamk
         case LAMT_WF_SKIP:
             return true;
         case LAMT_WF_PP:
+            if(((W.ssz | W.dsz) & 0x80) == 0)
+            {
+                // sizes as template parameters: one typed load and store per element
+                auto pp = [&](auto ss, auto ds)
+                {
+                    using TS = decltype(ss);
+                    using TD = decltype(ds);
+                    if(!W.conv && !W.boolean)
+                        for(uint32_t e = lane; e < T; e += 32)
+                            *reinterpret_cast<TD*>(dbuf + W.dbase[0] + e * W.dbs[0])
+                                = static_cast<TD>(*reinterpret_cast<const TS*>(sbuf + W.sbase[0] + e * W.sbs[0]));
+                    else
+                        for(uint32_t e = lane; e < T; e += 32)
+                            *reinterpret_cast<TD*>(dbuf + W.dbase[0] + e * W.dbs[0]) = static_cast<TD>(
+                                fix(*reinterpret_cast<const TS*>(sbuf + W.sbase[0] + e * W.sbs[0])));
+                };
+                auto dst = [&](auto ss)
+                {
+                    switch(W.dsz)
+                    {
+                    case 1: pp(ss, uint8_t{}); break;
+                    case 2: pp(ss, uint16_t{}); break;
+                    case 4: pp(ss, uint32_t{}); break;
+                    default: pp(ss, static_cast<unsigned long long>(0)); break;
+                    }
+                };
+                switch(W.ssz)
+                {
+                case 1: dst(uint8_t{}); break;
+                case 2: dst(uint16_t{}); break;
+                case 4: dst(uint32_t{}); break;
+                default: dst(static_cast<unsigned long long>(0)); break;
+                }
+                return true;
+            }
             for(uint32_t e = lane; e < T; e += 32)
                 wt_st(dbuf + W.dbase[0] + e * W.dbs[0], W.dsz, fix(wt_ld(sbuf + W.sbase[0] + e * W.sbs[0], W.ssz)));
             return true;

@@ -455,11 +455,14 @@ namespace lamhost
             W.dn = dPhys ? 1 : L.dn;
             bool ok = W.sn <= 8 && W.dn <= 8;
             bool planes = q.T % 4 == 0;
+            bool unalignedS = false, unalignedD = false;
             auto term = [&](const lamt_term& t, uint32_t& base, uint32_t& bs, bool split) -> bool
             {
                 const lamt_stream& st = q.st[t.stream];
-                if(st.kind != 0 || st.lanes != 1 || !t.aligned)
+                if(st.kind != 0 || st.lanes != 1 || (split && !t.aligned))
                     return false;
+                if(!t.aligned)
+                    (&t == &L.s[0] ? unalignedS : unalignedD) = true;
                 base = st.smem_off + t.inblock;
                 bs = st.bs;
                 if(split)
@@ -472,8 +475,8 @@ namespace lamhost
                 ok = term(L.d[k], W.dbase[k], W.dbs[k], dSplit);
             if(!ok)
                 continue;
-            W.ssz = sPhys ? L.s[0].size : 1;
-            W.dsz = dPhys ? L.d[0].size : 1;
+            W.ssz = static_cast<uint8_t>((sPhys ? L.s[0].size : 1) | (unalignedS ? 0x80 : 0));
+            W.dsz = static_cast<uint8_t>((dPhys ? L.d[0].size : 1) | (unalignedD ? 0x80 : 0));
             W.conv = !(L.stype == L.ltype && L.ltype == L.dtype);
             W.boolean = L.stype == Bool;
             W.mode = sPhys && dPhys ? LAMT_WF_PP
