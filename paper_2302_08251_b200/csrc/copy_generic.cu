@@ -251,8 +251,66 @@ namespace lamk
         }
     }
 
+    // Closed form for streams with one element per block stride (AoS, SoA, byte planes): heat
+    // block b of stream y receives, for each term, the number of elements e in [begin, end) whose
+    // range [base0 + e*bs + inblock, +size) overlaps [b*g, (b+1)*g).  One thread per block; a
+    // stream's interior blocks are touched by no other stream, its two edge blocks may be.
+    __device__ __forceinline__ int64_t floor_div(int64_t a, int64_t b)
+    {
+        return a >= 0 ? a / b : -((-a + b - 1) / b);
+    }
+
+    __global__ void __launch_bounds__(256) k_heat_closed(const __grid_constant__ HeatParams p)
+    {
+        const HeatStream& st = p.st[blockIdx.y];
+        const int64_t g = static_cast<int64_t>(p.gran), bs = static_cast<int64_t>(st.bs), b0 = static_cast<int64_t>(st.base0);
+        const int64_t first = (b0 + static_cast<int64_t>(p.begin) * bs) / g;
+        const int64_t last = (b0 + static_cast<int64_t>(p.end) * bs - 1) / g;
+        const int64_t eb = static_cast<int64_t>(p.begin), ee = static_cast<int64_t>(p.end) - 1;
+        unsigned long long* heat = p.heat + p.heatOff[st.nr];
+        for(int64_t b = first + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b <= last;
+            b += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        {
+            unsigned long long c = 0;
+            for(uint32_t t = st.t0; t < st.t1; ++t)
+            {
+                const HeatTerm& ht = p.term[t];
+                const int64_t off = b0 + ht.inblock;
+                // overlap: off + e*bs < (b+1)g  and  off + e*bs + size > b*g
+                int64_t lo = floor_div(b * g - off - static_cast<int64_t>(ht.size), bs) + 1;
+                int64_t hi = floor_div((b + 1) * g - off - 1, bs);
+                lo = lo < eb ? eb : lo;
+                hi = hi > ee ? ee : hi;
+                if(hi >= lo)
+                    c += static_cast<unsigned long long>(hi - lo + 1);
+            }
+            if(!c)
+                continue;
+            if(b == first || b == last)
+                atomicAdd(heat + b, c);
+            else
+                heat[b] += c;
+        }
+    }
+
     cudaError_t heat_phys(const HeatParams& p, cudaStream_t s)
     {
+        bool closed = p.nstreams > 0;
+        uint64_t maxBlocks = 0;
+        for(uint32_t k = 0; k < p.nstreams; ++k)
+        {
+            const HeatStream& st = p.st[k];
+            closed = closed && st.lanes == 1;
+            const uint64_t span = ((st.base0 + p.end * st.bs - 1) / p.gran) - ((st.base0 + p.begin * st.bs) / p.gran) + 1;
+            maxBlocks = span > maxBlocks ? span : maxBlocks;
+        }
+        if(closed && p.end > p.begin)
+        {
+            const unsigned gx = stream_grid((maxBlocks + 255) / 256, "LAMB_HEAT_CTAS", 0);
+            k_heat_closed<<<dim3(gx, p.nstreams), 256, 0, s>>>(p);
+            count_launch();
+            return cudaGetLastError();
+        }
         if(p.end <= p.begin || p.nstreams == 0)
             return cudaSuccess;
         const uint64_t ctas = (p.end - p.begin + p.E - 1) / p.E; // E is sized on the host

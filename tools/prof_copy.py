@@ -18,12 +18,13 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 26)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--dst-wrap", type=int, default=0)
+    ap.add_argument("--gran", type=int, default=64)
     a = ap.parse_args()
     import torch
     from paper_2302_08251_b200 import lamina as L
     ext = f"i32:[{a.n}]"
     s = L.View(L.Layout(a.schema, ext, a.src))
-    d = L.View(L.Layout(a.schema, ext, a.dst, wrap=a.dst_wrap))
+    d = L.View(L.Layout(a.schema, ext, a.dst, wrap=a.dst_wrap, granularity=a.gran))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.reps)]
     for r in range(a.reps):
         ev[2 * r].record()
