@@ -165,6 +165,9 @@ int lam_copy_range(const lam_view* src, lam_view* dst, uint64_t begin, uint64_t 
 /* copyView over HOST views: host blobs in, host blobs out (dst blobs are in/out so that
  * bytes the copy never writes keep their values).  Streams chunks through the GPU with
  * overlapped H2D / kernel / D2H.  Synchronous.  Host memory should be pinned. */
+/* lam_copy for n (src[k], dst[k]) pairs, each on its own device (SURVEY 8(b) lam_copy_sharded):
+ * all copies in flight at once on per-device streams, returns when all are done. */
+int lam_copy_sharded(const lam_view* const* src, lam_view* const* dst, size_t n);
 int lam_copy_host(const lam_layout* src_layout, const void* const* src_host_blobs, const lam_layout* dst_layout,
                   void* const* dst_host_blobs, int device, uint64_t* src_counters, uint64_t* dst_counters);
 
@@ -198,6 +201,8 @@ int lam_view_write_values(lam_view* view, const uint64_t* linear, const uint32_t
 int lam_nbody_init(lam_view* view, uint64_t seed, void* stream);
 int lam_nbody_update(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_move(lam_view* view, uint64_t i_begin, uint64_t i_end, void* stream);
+/* One runner step (runner.cpp:387-421): lam_nbody_update then lam_nbody_move over [i_begin, i_end). */
+int lam_nbody_step(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_checksum(const lam_view* view, double* out);
 /* The fused multi-GPU update step: elements [i_begin, i_end) of `view` against j-sources read
  * directly from other views -- view k supplies particles [j_begin[k], j_end[k]) (global indices,

@@ -49,6 +49,8 @@ _SIGS = {
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
     "lam_view_device_plan": (vp, [vp]),
+    "lam_copy_sharded": (i32, [C.POINTER(vp), C.POINTER(vp), sz]),
+    "lam_nbody_step": (i32, [vp, i32, u64, u64, vp]),
     "lam_nbody_update_multi": (i32, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), sz, i32, u64, u64, vp]),
     "lam_ipc_get_handle": (i32, [vp, vp]),
     "lam_ipc_open": (i32, [vp, i32, C.POINTER(vp)]),

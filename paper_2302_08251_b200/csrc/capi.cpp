@@ -9,6 +9,7 @@
 #include <fstream>
 #include <map>
 #include <mutex>
+#include <vector>
 
 using namespace lamb;
 
@@ -693,6 +694,42 @@ extern "C"
     int lam_copy_range(const lam_view* src, lam_view* dst, uint64_t begin, uint64_t end, void* stream)
     {
         return guard([&] { lamhost::copyViews(*src, *dst, begin, end, static_cast<cudaStream_t>(stream)); });
+    }
+
+    int lam_copy_sharded(const lam_view* const* src, lam_view* const* dst, size_t n)
+    {
+        return guard(
+            [&]
+            {
+                // one non-blocking stream per pair, all pairs in flight, then one join (each pair
+                // on its own GPU: the weak-scaling layout of SURVEY 8(e) from a single process)
+                std::vector<cudaStream_t> streams(n, nullptr);
+                struct Cleanup
+                {
+                    std::vector<cudaStream_t>& s;
+                    const lam_view* const* src;
+                    ~Cleanup()
+                    {
+                        for(size_t k = 0; k < s.size(); ++k)
+                            if(s[k])
+                            {
+                                cudaSetDevice(src[k]->device);
+                                cudaStreamDestroy(s[k]);
+                            }
+                    }
+                } cleanup{streams, src};
+                for(size_t k = 0; k < n; ++k)
+                {
+                    DeviceGuard g(src[k]->device);
+                    lam_cuda_check(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking), "stream");
+                    lamhost::copyViews(*src[k], *dst[k], 0, src[k]->L->map->elementCount(), streams[k]);
+                }
+                for(size_t k = 0; k < n; ++k)
+                {
+                    DeviceGuard g(src[k]->device);
+                    lam_cuda_check(cudaStreamSynchronize(streams[k]), "sync");
+                }
+            });
     }
 
     int lam_copy_host(const lam_layout* sl, const void* const* sb, const lam_layout* dl, void* const* db, int device,

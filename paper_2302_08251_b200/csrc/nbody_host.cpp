@@ -237,6 +237,12 @@ extern "C"
         return guard2([&] { lam_cuda_check(cudaIpcCloseMemHandle(device_ptr), "cudaIpcCloseMemHandle"); });
     }
 
+    int lam_nbody_step(lam_view* v, int mode, uint64_t ib, uint64_t ie, void* stream)
+    {
+        const int rc = lam_nbody_update(v, mode, ib, ie, stream);
+        return rc != LAM_OK ? rc : lam_nbody_move(v, ib, ie, stream);
+    }
+
     int lam_nbody_move(lam_view* v, uint64_t ib, uint64_t ie, void* stream)
     {
         return guard2(

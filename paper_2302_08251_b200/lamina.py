@@ -345,6 +345,10 @@ class View:
         end = self.layout.element_count if end is None else end
         _check(lib().lam_nbody_move(self._h, begin, end, _stream_handle(stream)))
 
+    def nbody_step(self, mode: int = NBODY_EXACT, begin: int = 0, end: int | None = None, stream=None) -> None:
+        end = self.layout.element_count if end is None else end
+        _check(lib().lam_nbody_step(self._h, mode, begin, end, _stream_handle(stream)))
+
     def nbody_update_from(self, sources, mode: int = NBODY_EXACT, begin: int = 0, end: int | None = None,
                           stream=None) -> None:
         """Fused update: j-particles read from other views, sources = [(view, j_begin, j_end), ...]."""
@@ -375,6 +379,14 @@ def read_view_dump(stem: str, device: int = 0, stream=None) -> View:
     v.device = device
     v._h = vh
     return v
+
+
+def copy_sharded(pairs) -> None:
+    """lam_copy_sharded: copyView for every (src, dst) pair, each on its own device, all in flight."""
+    k = len(pairs)
+    s = (C.c_void_p * max(1, k))(*[a.handle for a, _ in pairs])
+    d = (C.c_void_p * max(1, k))(*[b.handle for _, b in pairs])
+    _check(lib().lam_copy_sharded(s, d, k))
 
 
 def ipc_handle(device_ptr: int) -> bytes:

@@ -263,3 +263,27 @@ def test_copy_multidim_extents(ext, dyn, a, b):
     L.copy_view(gs, gd)
     for x, y in zip(gd.download_all(), db):
         assert np.array_equal(x, y)
+
+
+def test_copy_sharded_pairs():
+    """lam_copy_sharded: several (src, dst) pairs in flight at once (one GPU here)."""
+    L = lm()
+    n = 50_001
+    ext = f"i32:[{n}]"
+    rng = np.random.default_rng(21)
+    vals = random_values(rng, [8] * 7, n)
+    pairs, want = [], []
+    for a, b in [("aos-packed", "soa-mb"), ("soa-sb", "aosoa:8"), ("aosoa:32", "bytesplit:soa-mb")]:
+        ms, md = O.make(R32, ext, a), O.make(R32, ext, b)
+        sb = O.zero_blobs(ms)
+        O.write_all(ms, sb, vals)
+        db = O.zero_blobs(md)
+        O.copy_view(ms, sb, md, db)
+        gs, gd = L.View(L.Layout(R32, ext, a)), L.View(L.Layout(R32, ext, b))
+        gs.upload_all(sb)
+        pairs.append((gs, gd))
+        want.append(db)
+    L.copy_sharded(pairs)
+    for (_, gd), db in zip(pairs, want):
+        for x, y in zip(gd.download_all(), db):
+            assert np.array_equal(x, y)

@@ -164,3 +164,15 @@ def test_ipc_handle_exports():
     v = L.View(L.Layout(schema("f32"), "i64:[64]", "soa-mb"))
     h = L.ipc_handle(v.blob_ptr(0))
     assert len(h) == 64 and any(h)
+
+
+def test_nbody_step_is_update_then_move():
+    from paper_2302_08251_b200 import lamina as L
+    lay = L.Layout(schema("f32"), "i64:[700]", "aosoa:8")
+    a, b = L.View(lay), L.View(lay)
+    for v in (a, b):
+        v.nbody_init(7)
+    a.nbody_update(0)
+    a.nbody_move()
+    b.nbody_step(0)
+    assert all(np.array_equal(x, y) for x, y in zip(a.download_all(), b.download_all()))
