@@ -3,6 +3,8 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <string>
 
 using namespace lamb;
 
@@ -24,6 +26,108 @@ namespace lamhost
         // view.cpp:175-176
         return a.name() == b.name() && !a.hasMutableState() && !b.hasMutableState() && a.isFullyPhysical()
             && b.isFullyPhysical();
+    }
+
+    // Bit-packed <-> record-contiguous (AoS / AoSoA) copies of 32-bit leaves have no one-pass
+    // kernel: stage through an SoA multi-blob scratch view so both halves run on the specialised
+    // kernels (k_vec_transpose, k_pack32 / k_unpack32).  Every element is still read once from
+    // the source view and written once to the destination view (counters unchanged).
+    static bool hasBits(const Lowered& L)
+    {
+        for(const auto& st : L.streams)
+            if(st.kind == LAMS_BITS)
+                return true;
+        return false;
+    }
+
+    static bool leafContig32(const Lowered& L)
+    {
+        // every leaf a 4-byte physical leaf in its own SoA array (what k_pack32 reads directly)
+        for(uint16_t r : L.roots)
+        {
+            const lamp_node& nd = L.nodes[r];
+            if(nd.kind != LAMP_PHYS || scalarSize(nd.type) != 4)
+                return false;
+            const lamp_stream& st = L.streams[nd.stream];
+            if(!(st.lanes == 1 && st.block_stride == 4) && !(st.lanes % 32 == 0 && nd.b == 4))
+                return false;
+        }
+        return true;
+    }
+
+    static bool all32(const Lowered& L)
+    {
+        for(const auto& l : L.map->schema().leaves())
+            if(scalarSize(l.type) != 4)
+                return false;
+        return true;
+    }
+
+    static bool stagingHelps(const Lowered& S, const Lowered& D)
+    {
+        if(std::getenv("LAMB_STAGE") && std::getenv("LAMB_STAGE")[0] == '0')
+            return false;
+        if(!all32(S) || S.heat || D.heat)
+            return false;
+        const bool sb = hasBits(S), db = hasBits(D);
+        if(sb == db)
+            return false;
+        const Lowered& phys = sb ? D : S; // the non-packed side
+        for(uint16_t r : phys.roots)
+            if(phys.nodes[r].kind != LAMP_PHYS)
+                return false;
+        return !leafContig32(phys);
+    }
+
+    // scratch SoA views, cached per (device, stream, schema+extents): allocation and plan lowering happen
+    // once, not per copy (a 2^26-record scratch is 1.9 GB; at most 4 are kept)
+    struct ScratchSoA
+    {
+        std::shared_ptr<Lowered> L;
+        lam_view v;
+        std::string key;
+        ScratchSoA(const lam_view& like, std::string k) : key(std::move(k))
+        {
+            const Map& m = *like.L->map;
+            L = lower(std::make_shared<SoAMap>(m.schema(), m.extents(), true));
+            v.L = L;
+            v.device = like.device;
+            v.owned = false;
+            DeviceGuard g(like.device);
+            for(size_t nr = 0; nr < L->map->blobCount(); ++nr)
+            {
+                void* p = nullptr;
+                lam_cuda_check(cudaMalloc(&p, std::max<uint64_t>(16, L->map->blobSize(nr))), "scratch blob");
+                v.blobs.push_back(p);
+            }
+            v.img.build(*L, like.device, streamPtrsFor(*L, v.blobs));
+        }
+        ~ScratchSoA()
+        {
+            DeviceGuard g(v.device);
+            cudaDeviceSynchronize();
+            v.img.release();
+            for(void* p : v.blobs)
+                cudaFree(p);
+        }
+    };
+
+    static lam_view& scratchFor(const lam_view& like, cudaStream_t s)
+    {
+        static std::mutex mu;
+        static std::vector<std::unique_ptr<ScratchSoA>> cache;
+        const Map& m = *like.L->map;
+        // one scratch per stream: copies on different streams may run concurrently
+        const std::string key = std::to_string(like.device) + "|" + std::to_string(reinterpret_cast<uintptr_t>(s)) + "|"
+            + m.schema().toString() + "|" + m.extents().toString();
+        std::lock_guard<std::mutex> lk(mu);
+        for(auto& c : cache)
+            if(c->key == key)
+                return c->v;
+        if(cache.size() >= 4)
+            cache.erase(cache.begin());
+        cache.push_back(std::make_unique<ScratchSoA>(like, key));
+        return cache.back()->v;
     }
 
     void copyViews(const lam_view& src, lam_view& dst, uint64_t begin, uint64_t end, cudaStream_t s)
@@ -60,6 +164,13 @@ namespace lamhost
         // LAMB_FORCE_GENERIC=1 (tests only): cross-check the specialised kernels against the
         // plan interpreter on identical inputs
         const char* fg = std::getenv("LAMB_FORCE_GENERIC");
+        if(full && !(fg && fg[0] == '1') && stagingHelps(*src.L, *dst.L))
+        {
+            lam_view& tmp = scratchFor(src, s);
+            copyViews(src, tmp, begin, end, s);
+            copyViews(tmp, dst, begin, end, s);
+            return;
+        }
         if(!(fg && fg[0] == '1') && tileCopy(src, dst, begin, end, s))
             return;
         lam_cuda_check(lamk::generic_copy(src.img.hdr, dst.img.hdr, begin, end,
