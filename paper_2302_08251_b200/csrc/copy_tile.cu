@@ -793,6 +793,20 @@ namespace lamk
         case LAMT_WF_SKIP:
             return true;
         case LAMT_WF_PP:
+            if(W.sL != 1 || W.dL != 1)
+            {
+                // AoSoA on either side: block / lane split by a magic multiply
+                auto addr = [](uint32_t base, uint32_t bs, uint32_t L, uint32_t ls, uint32_t magic, uint32_t e) {
+                    if(L == 1)
+                        return base + e * bs;
+                    const uint32_t q = __umulhi(e, magic);
+                    return base + q * bs + (e - q * L) * ls;
+                };
+                for(uint32_t e = lane; e < T; e += 32)
+                    wt_st(dbuf + addr(W.dbase[0], W.dbs[0], W.dL, W.dls, W.dmagic, e), W.dsz,
+                          fix(wt_ld(sbuf + addr(W.sbase[0], W.sbs[0], W.sL, W.sls, W.smagic, e), W.ssz)));
+                return true;
+            }
             if(((W.ssz | W.dsz) & 0x80) == 0)
             {
                 // sizes as template parameters: one typed load and store per element

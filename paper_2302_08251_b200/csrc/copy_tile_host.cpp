@@ -456,11 +456,22 @@ namespace lamhost
             bool ok = W.sn <= 8 && W.dn <= 8;
             bool planes = q.T % 4 == 0;
             bool unalignedS = false, unalignedD = false;
+            W.sL = W.dL = 1;
             auto term = [&](const lamt_term& t, uint32_t& base, uint32_t& bs, bool split) -> bool
             {
                 const lamt_stream& st = q.st[t.stream];
-                if(st.kind != 0 || st.lanes != 1 || (split && !t.aligned))
+                if(st.kind != 0 || (split && !t.aligned))
                     return false;
+                if(st.lanes != 1)
+                {
+                    // AoSoA: only as the single term of a PHYS -> PHYS leaf
+                    if(split || !(sPhys && dPhys) || st.lanes >= (1u << 16) || q.T >= (1u << 16))
+                        return false;
+                    const bool isSrc = &t == &L.s[0];
+                    (isSrc ? W.sL : W.dL) = st.lanes;
+                    (isSrc ? W.sls : W.dls) = t.ls;
+                    (isSrc ? W.smagic : W.dmagic) = static_cast<uint32_t>(((uint64_t{1} << 32) + st.lanes - 1) / st.lanes);
+                }
                 if(!t.aligned)
                     (&t == &L.s[0] ? unalignedS : unalignedD) = true;
                 base = st.smem_off + t.inblock;

@@ -66,6 +66,9 @@ struct lamt_wfast
 {
     uint8_t mode, sn, dn, conv, boolean, ssz, dsz, pad;
     uint32_t sbase[8], sbs[8], dbase[8], dbs[8]; // smem image offset (incl. inblock) and element stride
+    // PHYS terms on AoSoA streams (lanes L > 1): element e at base + (e / L) * bs + (e % L) * ls,
+    // e / L = __umulhi(e, magic) with magic = ceil(2^32 / L) (exact for tile-local e < 2^16)
+    uint32_t sL, sls, smagic, dL, dls, dmagic;
 };
 
 #define LAMT_MAX_WARPS 32
