@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -78,7 +79,38 @@ namespace lamina_b200
             return h_.get();
         }
 
+        /// Mapping::contiguousRun (mapping.hpp:122-135): (nr, offset) when the n values of the
+        /// leaf starting at `linear` are contiguous; nullopt otherwise.
+        std::optional<std::pair<std::size_t, std::uint64_t>> contiguousRun(std::uint64_t linear, std::size_t flatLeaf,
+                                                                           std::uint64_t n) const
+        {
+            int has = 0;
+            std::size_t nr = 0;
+            std::uint64_t off = 0;
+            check(lam_layout_contiguous_run(h_.get(), linear, flatLeaf, n, &has, &nr, &off));
+            if(!has)
+                return std::nullopt;
+            return std::make_pair(nr, off);
+        }
+
+        /// the .meta sidecar writeViewDump writes for a view of this mapping (view_io.cpp:30-44)
+        std::string dumpMeta() const
+        {
+            std::string s(lam_layout_dump_meta(h_.get(), nullptr, 0), '\0');
+            lam_layout_dump_meta(h_.get(), s.data(), s.size() + 1);
+            return s;
+        }
+
+        /// adopt a layout handle created by the C ABI (lam_view_restore)
+        static std::shared_ptr<const Mapping> adopt(lam_layout* h)
+        {
+            auto m = std::shared_ptr<Mapping>(new Mapping());
+            m->h_.reset(h, lam_layout_destroy);
+            return m;
+        }
+
     private:
+        Mapping() = default;
         std::shared_ptr<lam_layout> h_;
     };
 
@@ -120,10 +152,39 @@ namespace lamina_b200
             return v_.get();
         }
 
+        /// FieldAccessCount::counters() of an instrumented view: (reads, writes) per leaf
+        std::pair<std::vector<std::uint64_t>, std::vector<std::uint64_t>> counters(std::size_t leaves) const
+        {
+            std::vector<std::uint64_t> r(leaves), w(leaves);
+            check(lam_counters_read(v_.get(), r.data(), w.data()));
+            return {r, w};
+        }
+
+        /// adopt a (layout, view) pair created by the C ABI (lam_view_restore)
+        View(MappingPtr m, lam_view* v) : m_(std::move(m))
+        {
+            v_.reset(v, lam_view_free);
+        }
+
     private:
         MappingPtr m_;
         std::shared_ptr<lam_view> v_;
     };
+
+    /// lamina::writeViewDump (view_io.cpp:28-59): <stem>.meta + <stem>.blob<nr>.bin
+    inline void writeViewDump(const View& view, const std::string& stem)
+    {
+        check(lam_view_dump(view.handle(), stem.c_str()));
+    }
+
+    /// lamina::readViewDump (view_io.cpp:61-129) onto a device
+    inline View readViewDump(const std::string& stem, int device = 0, void* stream = nullptr)
+    {
+        lam_layout* l = nullptr;
+        lam_view* v = nullptr;
+        check(lam_view_restore(stem.c_str(), device, stream, &l, &v));
+        return View(Mapping::adopt(l), v);
+    }
 
     /// lamina::copyView(const View&, View&) (view.hpp:285) on the GPU, stream-ordered.
     inline void copyView(const View& src, View& dst, void* stream = nullptr)

@@ -21,7 +21,15 @@ int main()
     try { lamina_b200::parseLayout("aos-packed", R32, "i16:[40000]"); }
     catch(const std::overflow_error& e) { caught += 1; }
     std::printf("caught %d\n", caught);
-    return caught == 2 ? 0 : 1;
+    // Mapping::contiguousRun: SoA always, AoS never for n > 1, AoSoA inside a block
+    auto soa = lamina_b200::parseLayout("soa-mb", R32, "i32:[100]");
+    auto aos = lamina_b200::parseLayout("aos-packed", R32, "i32:[100]");
+    auto aosoa = lamina_b200::parseLayout("aosoa:8", R32, "i32:[100]");
+    const bool runs = soa->contiguousRun(5, 1, 50).has_value() && !aos->contiguousRun(5, 1, 2).has_value()
+        && aosoa->contiguousRun(8, 2, 8).has_value() && !aosoa->contiguousRun(7, 2, 2).has_value();
+    std::printf("runs %d\n", runs ? 1 : 0);
+    std::printf("%s", soa->dumpMeta().c_str());
+    return caught == 2 && runs ? 0 : 1;
 }
 """
 
@@ -39,3 +47,5 @@ def test_cpp_mirror_compiles_and_maps_errors(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     # f32 -> f64 storage, split into 8 one-byte planes per leaf: 7 x 8 = 56 blobs of n bytes
     assert out.stdout.splitlines()[0] == "changetype:f32=f64:bytesplit:soa-mb 56 1000"
+    assert "runs 1" in out.stdout
+    assert "mapping=soa-mb\nblobs=7\nblob0-size=400\n" in out.stdout
