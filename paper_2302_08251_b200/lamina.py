@@ -421,8 +421,8 @@ def copy_view_host(src: Layout, src_blobs: Sequence[np.ndarray], dst: Layout, ds
                    device: int = 0):
     """copyView over HOST blobs through the GPU (H2D, copy, D2H inside).
 
-    dst_blobs are updated in place.  Returns (src_counters, dst_counters): for
-    FieldAccessCount views [reads..., writes...] followed by heatmap blocks, else None.
+    dst_blobs are updated in place.  Returns (src_counters, dst_counters): [reads..., writes...]
+    for a FieldAccessCount view, followed by the heatmap blocks of a Heatmap view, else None.
     """
     def ptrs(bl):
         arr = (C.c_void_p * max(1, len(bl)))()
@@ -435,9 +435,9 @@ def copy_view_host(src: Layout, src_blobs: Sequence[np.ndarray], dst: Layout, ds
         return arr
 
     def counters(lay: Layout):
-        n = 0
-        if lay.has_mutable_state:
-            n = 2 * lay.leaf_count + sum(lay.heatmap_blocks(k) for k in range(lay.blob_count))
+        # [reads, writes] when FieldAccessCount wraps the mapping, then the heatmap blocks
+        n = 2 * lay.leaf_count if "field-access-count(" in lay.name else 0
+        n += sum(lay.heatmap_blocks(k) for k in range(lay.blob_count))
         return np.zeros(max(1, n), dtype=np.uint64), n
 
     if len(src_blobs) != src.blob_count or len(dst_blobs) != dst.blob_count:

@@ -287,3 +287,24 @@ def test_copy_sharded_pairs():
     for (_, gd), db in zip(pairs, want):
         for x, y in zip(gd.download_all(), db):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("wrap", [2, 3])
+def test_copy_host_pipeline_heatmap(wrap):
+    """lam_copy_host with a Heatmap (and FieldAccessCount) destination: chunked counters sum."""
+    L = lm()
+    rng = np.random.default_rng(13)
+    n = 2_000_003
+    ext = f"i32:[{n}]"
+    vals = random_values(rng, [8] * 7, n)
+    ms, md = O.make(R32, ext, "aos-packed"), O.make(R32, ext, "soa-mb", wrap=wrap, gran=64)
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    db = O.zero_blobs(md)
+    O.copy_view(ms, sb, md, db)
+    got = [np.zeros_like(x) for x in db]
+    _, dc = L.copy_view_host(L.Layout(R32, ext, "aos-packed"), sb, L.Layout(R32, ext, "soa-mb", wrap=wrap, granularity=64),
+                             got)
+    for x, y in zip(got, db):
+        assert np.array_equal(x, y)
+    assert np.array_equal(dc, O.counters(md))
