@@ -105,14 +105,23 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU (torchrun env).  LAMB_DIST_BACKEND=gloo with more ranks than GPUs
+    (ranks share devices round-robin) exercises the multi-rank path on a one-GPU box; the
+    numbers are then not a scaling measurement."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
+        backend = os.environ.get("LAMB_DIST_BACKEND", "nccl")
+        if backend != "nccl":
+            local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
