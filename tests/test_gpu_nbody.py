@@ -176,3 +176,17 @@ def test_nbody_step_is_update_then_move():
     a.nbody_move()
     b.nbody_step(0)
     assert all(np.array_equal(x, y) for x, y in zip(a.download_all(), b.download_all()))
+
+
+@pytest.mark.parametrize("layout", ["soa-mb", "aosoa:8"])
+def test_fused_p2p_transport_two_processes(layout):
+    """nbody_distributed(transport="p2p"): two processes map each other's shards with CUDA IPC
+    (here on one GPU) and update through lam_nbody_update_multi; exact mode == single view."""
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29541", "tools/p2p_check.py", layout, "3000",
+                        "3"], cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "OK" in r.stdout, r.stdout + r.stderr[-2000:]
