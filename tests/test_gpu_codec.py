@@ -70,3 +70,16 @@ def test_random_subset_against_reference(fmt, ref):
     got = O.read_bits(packed, np.arange(bits.size, dtype=np.uint64) * np.uint64(w), w)
     want = ref.float_encode_f32(bits, e, m)
     assert np.array_equal(got, want)
+
+
+def test_fast_sqrt_rcp_equal_ieee_over_exact_nbody_range(tmp_path):
+    """The exact n-body's MUFU + Newton 1/sqrt equals __frcp_rn(__fsqrt_rn(x)) on every float of
+    its fast-path range (sqrt over [2^-40, 2^40], rcp over [2^-20, 2^20]), exhaustively."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = os.path.join(root, "tools", "scratch", "sqrt_rcp.cu")
+    exe = tmp_path / "sqrt_rcp"
+    subprocess.run(["nvcc", "-std=c++20", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", str(exe), src],
+                   check=True, capture_output=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300).stdout
+    assert out.count("mismatches") == 2 and out.count(": 0\n") == 2, out
