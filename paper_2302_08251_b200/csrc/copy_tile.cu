@@ -605,13 +605,22 @@ namespace lamk
             {
                 const uint64_t i = i0 + uint64_t(u) * blockDim.x;
                 const uint64_t ii = i < p.begin + n ? i : p.begin;
-                const uint64_t es = p.ul_s == 1 ? ii * p.ubs_s
-                                                : (ii >> p.ush_s) * p.ubs_s + (ii & (p.ul_s - 1)) * p.uls_s;
-                ed[u] = p.ul_d == 1 ? ii * p.ubs_d : (ii >> p.ush_d) * p.ubs_d + (ii & (p.ul_d - 1)) * p.uls_d;
+                auto off = [&](uint32_t L, uint32_t sh, uint32_t mag, uint32_t bs, uint32_t ls) -> uint64_t {
+                    if(L == 1)
+                        return ii * bs;
+                    if(sh != 0xFFFFFFFFu)
+                        return (ii >> sh) * bs + (ii & (L - 1)) * ls;
+                    const uint64_t q = __umulhi(static_cast<uint32_t>(ii), mag); // ii < 2^32 / L (host-checked)
+                    return q * bs + (ii - q * L) * ls;
+                };
+                const uint64_t es = off(p.ul_s, p.ush_s, p.umag_s, p.ubs_s, p.uls_s);
+                ed[u] = off(p.ul_d, p.ush_d, p.umag_d, p.ubs_d, p.uls_d);
+                // 4-byte gathers from record-strided sources: keep them in L1 so the next
+                // leaves' loads of the same lines hit
 #pragma unroll
                 for(int f = 0; f < LAMT_UNI_LEAVES; ++f)
                     if(f < nl)
-                        v[u][f] = __ldcs(reinterpret_cast<const W*>(sbase[f] + es));
+                        v[u][f] = __ldg(reinterpret_cast<const W*>(sbase[f] + es));
             }
 #pragma unroll
             for(int u = 0; u < UNROLL; ++u)

@@ -940,10 +940,18 @@ namespace lamhost
             return true;
         if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
             return true;
-        if(p.uni && !p.facS && !p.facD && envNum("LAMB_DIRECT", 0) != 0 && (p.ush_s != 0xFFFFFFFFu || p.ul_s == 1)
-           && (p.ush_d != 0xFFFFFFFFu || p.ul_d == 1))
+        // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
+        // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /
+        // lane by a magic multiply -- measured 1.7x over the warp-tile transpose (aosoa:2, aosoa:3)
+        const uint64_t maxL = std::max<uint64_t>(std::max<uint64_t>(p.ul_s, p.ul_d), 1);
+        if(p.uni && envNum("LAMB_DIRECT", 1) != 0 && end < (uint64_t{1} << 32) / maxL)
         {
-            lam_cuda_check(lamk::uniform_direct(p, end - begin, s), "uniform_direct");
+            lamt_params q = p;
+            q.umag_s = q.ul_s > 1 ? static_cast<uint32_t>(((uint64_t{1} << 32) + q.ul_s - 1) / q.ul_s) : 0;
+            q.umag_d = q.ul_d > 1 ? static_cast<uint32_t>(((uint64_t{1} << 32) + q.ul_d - 1) / q.ul_d) : 0;
+            q.facS = q.facD = 0;
+            lam_cuda_check(lamk::uniform_direct(q, end - begin, s), "uniform_direct");
+            addAccessCounts(p, S, end - begin, s);
             return true;
         }
         if(p.uni && !p.any_coop && envNum("LAMB_UNI_WARP", 1) != 0)

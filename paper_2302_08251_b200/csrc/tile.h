@@ -100,6 +100,7 @@ struct lamt_params
     uint32_t uni, usize;
     uint32_t ubs_s, ul_s, ush_s, uls_s;
     uint32_t ubs_d, ul_d, ush_d, uls_d;
+    uint32_t umag_s, umag_d; // ceil(2^32 / L) for non-power-of-two lanes (e / L = umulhi(e, mag), e < 2^32 / L)
     uint32_t uoff_s[LAMT_UNI_LEAVES], uoff_d[LAMT_UNI_LEAVES];
     lamt_stream st[LAMT_MAX_STREAMS];
     lamt_leaf leaf[LAMT_MAX_LEAVES];
