@@ -114,7 +114,12 @@ def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")
         b = L.View(L.Layout(R32, f"i32:[{n}]", "soa-mb"))
         _fill(L, a, 1)
         ms = _time(lambda: L.copy_view(a, b))
-        out["C1_aos_to_soamb_1M"] = {"GB/s": 56 * n / ms / 1e6, "ms": ms, "note": "58.7 MB working set is L2-resident"}
+        K = 50
+        msk = _time(lambda: [L.copy_view(a, b) for _ in range(K)], reps=3, warm=1) / K
+        out["C1_aos_to_soamb_1M"] = {
+            "GB/s": 56 * n / msk / 1e6, "ms_per_copy": msk, "single_call_ms": ms,
+            "note": "58.7 MB working set is L2-resident; GB/s over 50 back-to-back copies (device time per copy); "
+                    "single_call_ms includes the ~6 us host dispatch of one call"}
         del a, b
     # ---- C3 ------------------------------------------------------------------------------
     if "C3" in parts:
