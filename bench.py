@@ -323,7 +323,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        # the reference arm is CPU-only: no process group, rank 0 alone works and prints
+        world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    else:
+        world, rank, local = dist_setup()
     n = args.records
     config = {"workload": "C2: copyView over all 25 ordered pairs of {aos-packed, soa-sb, soa-mb, aosoa:8, aosoa:32}",
               "record": "n-body Record{Pos{x,y,z},Vel{x,y,z},Mass} 7 x f32 = 28 B", "records_per_gpu": n,
