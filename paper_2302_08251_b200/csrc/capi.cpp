@@ -1,7 +1,9 @@
 // C ABI (include/lamina_b200.h): host-side plumbing of the B200 path.  Owns layout
-// handles, device views (blobs + device plan + device counters) and the copy dispatch:
+// handles, device views (blobs + device plan + device counters), view dump/restore and the
+// copy entry points.  The copy dispatch itself (copy_dispatch.cpp -> copy_tile_host.cpp):
 //   copyView fast path (view.cpp:175-181)      -> lamk::blob_copy per blob
-//   tile-eligible pairs                          -> lamk::tile_copy  (copy_tile.cu)
+//   plan pairs with a specialised kernel        -> vec_transpose / pack32 / planes / vec_convert /
+//                                                  uniform_direct / warp_tile (copy_tile_host.cpp)
 //   everything else                              -> lamk::generic_copy (copy_generic.cu)
 #include "capi_internal.hpp"
 

@@ -3,7 +3,7 @@
 // with one thread per element i and the mapping trees resolved by the device plan
 // interpreter (device_common.cuh).  Handles every mapping composition the layout grammar
 // can express (Split, One, Null, nested ChangeType/Bytesplit, bit packing, instrumentation);
-// the specialised tile engine (copy_tile.cu) takes the common shapes.  Bit-stream
+// the specialised kernels (copy_tile_host.cpp dispatch) take every shape they can express.  Bit-stream
 // writes use word atomics, so neighbouring fields never race (bitpack.hpp:16-17).
 #include "device_common.cuh"
 #include "launch.h"

@@ -1,4 +1,13 @@
-// Tile engine: persistent, double-buffered, TMA-bulk-staged layout copy (K1/K3/K4/K5/K6).
+// Tile kernels over the tile-plan form (tile.h):
+//   k_warp_tile      the general engine: one warp per tile, 16-byte loads of the source images
+//                    into smem, per-leaf transforms from host-resolved descriptors, 16-byte
+//                    stores (every plan pair without a specialised kernel)
+//   k_uniform_direct uniform pairs outside the register transpose (AoSoA lanes not a multiple
+//                    of 16/size or not a power of two): per-element moves through L1
+//   k_uniform_warp   warp-tile transpose for uniform pairs (kept behind LAMB_DIRECT=0)
+//   k_tile_copy      the first design (below): kept as the last resort for unaligned images.
+//
+// Tile engine: persistent, double-buffered, TMA-bulk-staged layout copy.
 //
 // Per CTA, per tile of T elements:
 //   load      every source stream image  HBM -> smem   (cp.async.bulk + mbarrier tx count)

@@ -1,7 +1,11 @@
-// Tile-engine planning on the host: decides whether a (src, dst) layout pair can run on
-// the TMA-staged tile kernel, sizes the tile, places stream images in shared memory and
-// fills the kernel parameter block.  Pairs it cannot express fall back to the generic
-// interpreter kernel (copy_generic.cu).
+// Copy planning on the host.  makePlan lowers a (src, dst) layout pair into the tile-plan
+// form (tile.h: streams, per-leaf terminals, conversions); launchTile then hands the plan to
+// the first specialised kernel whose predicate holds -- register transpose (vec_transpose.cu),
+// bit packing (pack.cu), record <-> byte planes (planes.cu), f32 <-> f64 transpose, direct L1
+// gathers for the remaining uniform pairs, the general warp-tile engine (copy_tile.cu), and
+// last the TMA tile engine -- adds FieldAccessCount in closed form and accounts a Heatmap in a
+// separate range-only pass.  Pairs no plan can express run on the generic interpreter kernel
+// (copy_generic.cu).
 #include "capi_internal.hpp"
 #include "tile.h"
 

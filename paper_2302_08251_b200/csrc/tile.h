@@ -1,4 +1,5 @@
-// Tile engine parameter block (host <-> device).
+// Tile-plan parameter block (host <-> device), shared by the tile kernels (copy_tile.cu) and
+// read by the specialised kernels' predicates (copy_tile_host.cpp).
 //
 // A tile is T consecutive elements (T a multiple of every AoSoA lane count, of 32 and of
 // both layouts' shard units).  Each blob stream of the source and destination occupies
