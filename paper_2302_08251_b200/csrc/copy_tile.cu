@@ -762,10 +762,16 @@ namespace lamk
     {
         if(size & 0x80)
         {
-            uint64_t v = 0;
-            for(uint32_t k = 0; k < (size & 0x7F); ++k)
-                v |= uint64_t(b[k]) << (8 * k);
-            return v;
+            // two aligned 8-byte smem loads and a funnel shift (the 8 bytes after a source
+            // image still lie inside the warp's buffer: the destination images follow it)
+            const uint32_t sz = size & 0x7F;
+            const uintptr_t a = reinterpret_cast<uintptr_t>(b);
+            const unsigned long long* w = reinterpret_cast<const unsigned long long*>(a & ~uintptr_t{7});
+            const uint32_t sh = static_cast<uint32_t>(a & 7) * 8;
+            uint64_t v = w[0] >> sh;
+            if(sh)
+                v |= w[1] << (64 - sh);
+            return sz == 8 ? v : (v & ((uint64_t{1} << (8 * sz)) - 1));
         }
         switch(size)
         {
