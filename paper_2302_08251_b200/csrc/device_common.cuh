@@ -176,11 +176,12 @@ namespace lamd
     {
         const uint32_t s = (b >> 31) << 18;
         const uint32_t a = b & 0x7FFFFFFFu;
-        // RNE of the low 13 mantissa bits, carry propagates into the exponent;
-        // 0x7F7FF000.. round up into 0x7F800000 = Inf, which is the overflow rule, and
-        // Inf itself (low bits 0) maps to 0x3FC00 unchanged
-        const uint32_t r = (a + 0xFFFu + ((a >> 13) & 1u)) >> 13;
-        return s | (a > 0x7F800000u ? 0x3FE00u : r); // NaN: exp all ones | quiet bit
+        // e8m10 is TF32: cvt.rn.tf32.f32 rounds to nearest-even into the top 19 bits, overflow
+        // to Inf -- equal to the integer RNE (a + 0xFFF + lsb) >> 13 on every non-NaN input
+        // (exhaustive, tools/scratch/tf32.cu); NaN keeps the reference's canonical quiet pattern
+        uint32_t t;
+        asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(t) : "f"(__uint_as_float(b)));
+        return a > 0x7F800000u ? (s | 0x3FE00u) : (t >> 13); // NaN: exp all ones | quiet bit
     }
 
     LAM_DEV uint32_t encode_e5m10_f32(uint32_t b)
