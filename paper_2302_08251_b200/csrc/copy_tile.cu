@@ -996,6 +996,15 @@ namespace lamk
                         reinterpret_cast<uint4*>(sbuf)[c] = v[u];
                 }
             }
+            if(p.dst_holes) // destination images with padding: start from their current bytes
+                for(uint32_t j = ns; j < ns + nd; ++j)
+                    if(p.st[j].preload)
+                    {
+                        const uint4* g = reinterpret_cast<const uint4*>(base[j]);
+                        uint4* sm = reinterpret_cast<uint4*>(dbuf + p.st[j].smem_off);
+                        for(uint32_t c = lane; c < (p.st[j].tile_bytes >> 4); c += 32)
+                            sm[c] = __ldcs(g + c);
+                    }
             __syncwarp();
             // ---- transform ----
             for(uint32_t f = 0; f < p.nleaves; ++f)

@@ -136,8 +136,8 @@ namespace lamhost
                     return false;
                 if(t.a + (st.lanes - 1) * uint64_t(t.b) + size > st.block_stride)
                     return false; // terminal straddles its block
-                if(isDst && !st.holefree)
-                    return false; // whole-image stores would clobber bytes copyView never writes
+                // a destination with padding is preloaded by the warp-tile engine (stream.preload);
+                // no other tile kernel may take such a plan
                 if(st.block_stride > 0xFFFFFFFFull || st.lanes > 0xFFFFFFFFull)
                     return false;
                 out.stream = static_cast<uint16_t>(streamBase + useStream(side, t.stream, order));
@@ -276,7 +276,12 @@ namespace lamhost
             p.src_bytes = off;
             off = 0;
             for(int k = 0; k < ndst; ++k)
-                fillStream(p.st[nsrc + k], D.streams[pl.dstStreams[k]]);
+            {
+                const lamp_stream& ls = D.streams[pl.dstStreams[k]];
+                fillStream(p.st[nsrc + k], ls);
+                p.st[nsrc + k].preload = ls.kind == LAMS_PHYS && !ls.holefree;
+                p.dst_holes |= p.st[nsrc + k].preload;
+            }
             for(int k = 0; k < ndst; ++k)
             {
                 lamt_stream& t = p.st[nsrc + k];
@@ -936,6 +941,8 @@ namespace lamhost
             p.any_coop |= p.st[k].tile_bytes && !p.st[k].tma;
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
+        if(p.dst_holes)
+            return envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s);
         if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))

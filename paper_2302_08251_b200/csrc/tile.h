@@ -34,7 +34,9 @@ struct lamt_stream
     uint32_t tma;            // image start is 16-byte aligned in global memory
     uint32_t scratch_off;    // BITS destination: per-element pattern scratch (stage-relative)
     uint32_t scratch64;      // scratch slots are 8 bytes (field width > 32)
-    uint32_t pad;
+    uint32_t pad;            // warp-tile engine: first 16-byte chunk of this image in its buffer
+    uint32_t preload;        // destination with bytes copyView never writes (padding): the image is
+                             // read before the transform so whole-image stores keep them
 };
 
 struct lamt_term
@@ -109,5 +111,6 @@ struct lamt_params
     // warp-tile engine: stream of each 16-byte image chunk, source chunks then destination
     // chunks (host-built, copied to shared memory by each CTA)
     uint32_t wt_chs, wt_chd;
+    uint32_t dst_holes; // some destination stream has preload set (only k_warp_tile handles it)
     __align__(16) uint8_t wt_cst[1024];
 };
