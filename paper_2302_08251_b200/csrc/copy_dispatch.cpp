@@ -63,6 +63,41 @@ namespace lamhost
         return true;
     }
 
+    // one record stream of 4-byte leaves (AoS packed, AoSoA<L> with L | 32, L < 32) against bit
+    // streams of one width/format: k_rec_pack / k_rec_unpack do it in one pass (tryRecPack)
+    static bool recordSide32(const Lowered& L)
+    {
+        const size_t nl = L.roots.size();
+        if(nl < 1 || nl > 8)
+            return false;
+        const uint16_t s0 = L.nodes[L.roots[0]].stream;
+        const lamp_stream& st = L.streams[s0];
+        for(size_t f = 0; f < nl; ++f)
+        {
+            const lamp_node& nd = L.nodes[L.roots[f]];
+            if(nd.kind != LAMP_PHYS || scalarSize(nd.type) != 4 || nd.stream != s0)
+                return false;
+            if(st.lanes == 1 ? (st.block_stride != nl * 4 || nd.a != f * 4)
+                             : (st.lanes >= 32 || 32 % st.lanes || st.lane_shift == 0xFFFFFFFFu
+                                || st.block_stride != st.lanes * nl * 4 || nd.a != f * 4 * st.lanes || nd.b != 4))
+                return false;
+        }
+        return true;
+    }
+
+    static bool uniformBits(const Lowered& L)
+    {
+        const lamp_node& n0 = L.nodes[L.roots[0]];
+        for(uint16_t r : L.roots)
+        {
+            const lamp_node& nd = L.nodes[r];
+            if((nd.kind != LAMP_BITS_INT && nd.kind != LAMP_BITS_FLT) || nd.kind != n0.kind || nd.a != n0.a
+               || nd.b != n0.b)
+                return false;
+        }
+        return true;
+    }
+
     static bool stagingHelps(const Lowered& S, const Lowered& D)
     {
         if(std::getenv("LAMB_STAGE") && std::getenv("LAMB_STAGE")[0] == '0')
@@ -76,6 +111,8 @@ namespace lamhost
         for(uint16_t r : phys.roots)
             if(phys.nodes[r].kind != LAMP_PHYS)
                 return false;
+        if(recordSide32(phys) && uniformBits(sb ? S : D) && !(std::getenv("LAMB_RECPACK") && std::getenv("LAMB_RECPACK")[0] == '0'))
+            return false;
         return !leafContig32(phys);
     }
 

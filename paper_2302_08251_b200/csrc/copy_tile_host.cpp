@@ -47,6 +47,16 @@ namespace lamk
     };
     bool pack32(const PackParams& p, bool pack, cudaStream_t s);
 
+    struct RecPackParams
+    {
+        unsigned long long rec;
+        unsigned long long bits[8];
+        unsigned long long begin, groups;
+        uint32_t nl, lanes, lsh, sgnMask;
+        uint32_t w, E, M;
+    };
+    bool rec_pack(const RecPackParams& q, uint32_t kind, bool pack, cudaStream_t s);
+
     struct PlaneParams
     {
         unsigned long long rec;
@@ -666,6 +676,72 @@ namespace lamhost
         return true;
     }
 
+    // K3/K4 record side: every leaf a 4-byte leaf of one record stream -- AoS packed, or AoSoA<L>
+    // with L | 32 and L < 32 -- against bit streams of one width and format (pack.cu k_rec_pack /
+    // k_rec_unpack, one pass instead of staging through an SoA scratch)
+    static bool tryRecPack(const lamt_params& p, uint64_t begin, uint64_t groups, cudaStream_t s)
+    {
+        const uint32_t nl = p.nleaves;
+        if(nl < 1 || nl > 8 || envNum("LAMB_RECPACK", 1) == 0)
+            return false;
+        lamk::RecPackParams q{};
+        bool packDir = false;
+        uint32_t kind = 0, stream0 = 0;
+        for(uint32_t f = 0; f < nl; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            const bool pk = L.skind == LAMT_K_PHYS && (L.dkind == LAMT_K_BITS_INT || L.dkind == LAMT_K_BITS_FLT);
+            const bool up = L.dkind == LAMT_K_PHYS && (L.skind == LAMT_K_BITS_INT || L.skind == LAMT_K_BITS_FLT);
+            if(!(pk || up) || (f && pk != packDir))
+                return false;
+            packDir = pk;
+            const lamt_term& vt = pk ? L.s[0] : L.d[0];
+            const lamt_stream& vs = p.st[vt.stream];
+            const lamt_stream& bs = p.st[pk ? L.d[0].stream : L.s[0].stream];
+            if(vt.size != 4 || L.stype != L.ltype || L.dtype != L.ltype || L.ltype == Bool)
+                return false;
+            const uint8_t k = pk ? L.dkind : L.skind;
+            const uint32_t kd = k == LAMT_K_BITS_FLT ? 1 : 0;
+            const uint32_t E = pk ? L.dE : L.sE, M = pk ? L.dM : L.sM;
+            const uint32_t w = kd ? 1 + E + M : E;
+            if(f == 0)
+            {
+                stream0 = vt.stream;
+                kind = kd;
+                q.E = E;
+                q.M = M;
+                q.w = w;
+                q.lanes = vs.lanes;
+                if(vs.lanes == 1)
+                {
+                    if(vs.bs != nl * 4)
+                        return false;
+                }
+                else if(vs.lanes >= 32 || 32 % vs.lanes || vs.lshift == 0xFFFFFFFFu || vs.bs != vs.lanes * nl * 4)
+                    return false;
+                q.lsh = vs.lanes == 1 ? 0 : vs.lshift;
+                q.rec = vs.gptr;
+            }
+            if(vt.stream != stream0 || kd != kind || E != q.E || M != q.M || w < 1 || w > 32 || bs.bs != w)
+                return false;
+            if(vs.lanes == 1 ? vt.inblock != f * 4 : (vt.inblock != f * 4 * vs.lanes || vt.ls != 4))
+                return false;
+            if(kd == 1 && L.ltype != F32)
+                return false;
+            q.bits[f] = bs.gptr;
+            if(bs.gptr % 4)
+                return false;
+            if(up && L.ssigned)
+                q.sgnMask |= 1u << f;
+        }
+        if(begin % q.lanes || (q.rec + begin * nl * 4) % 16)
+            return false;
+        q.nl = nl;
+        q.begin = begin;
+        q.groups = groups;
+        return lamk::rec_pack(q, kind, packDir, s);
+    }
+
     // K3/K4: every leaf 4-byte physical (SoA or AoSoA with 32 | L) <-> bit stream of width <= 32
     static bool tryPack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
                         const Lowered& S, const Lowered& D, cudaStream_t s)
@@ -675,6 +751,16 @@ namespace lamhost
         const uint64_t groups = (end - begin) / 32;
         if(groups == 0)
             return false;
+        if(tryRecPack(p, begin, groups, s))
+        {
+            addAccessCounts(p, S, groups * 32, s);
+            const uint64_t doneEnd = begin + groups * 32;
+            if(doneEnd < end)
+                lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()),
+                                                  S.fac, D.fac, s, false),
+                               "generic_copy(tail)");
+            return true;
+        }
         std::vector<lamk::PackParams> jobs;
         bool packDir = false;
         for(uint32_t f = 0; f < p.nleaves; ++f)

@@ -405,6 +405,314 @@ namespace lamk
         fac_flush(p, cnt);
     }
 
+    // ---- record-contiguous side <-> bit streams in one pass ----------------------------------
+    // AoS (packed, 4-byte leaves) or AoSoA<L> (L | 32) against BitpackIntSoA / BitpackFloatSoA
+    // with one width for every leaf (computed.cpp:48-222).  A CTA owns 1024 consecutive records:
+    // their record bytes are one contiguous region (28 KB for the n-body record), moved with
+    // 16-byte coalesced accesses into shared memory padded by one word per 32 records.  Warp l
+    // packs leaf l, lane g the 32 records of group g (its W words of stream l): the value reads
+    // are conflict-free because the group padding puts the 32 lanes on 32 banks.  Every record
+    // byte and every stream word crosses HBM exactly once.
+    struct RecPackParams
+    {
+        unsigned long long rec;     // record region of element 0 (AoS stream / AoSoA block 0)
+        unsigned long long bits[8]; // bit stream of each leaf (word 0 = element 0)
+        unsigned long long begin;   // first element (multiple of 32 and of lanes)
+        unsigned long long groups;  // groups of 32 elements
+        uint32_t nl, lanes, lsh, sgnMask;
+        uint32_t w, E, M;
+    };
+
+    __device__ __forceinline__ uint32_t rec_word(const RecPackParams& q, uint32_t e, uint32_t l)
+    {
+        const uint32_t w = q.lanes == 1 ? e * q.nl + l : ((e >> q.lsh) * q.nl + l) * q.lanes + (e & (q.lanes - 1));
+        return w + (e >> 5); // one pad word per group of 32 records
+    }
+
+    // region word `w0 + c` (c = 0..3 of a 16-byte chunk) lives at smem w0 + c + group; the four
+    // components are visited in a lane-rotated order so each STS/LDS.32 hits 32 distinct banks
+    __device__ __forceinline__ uint32_t comp(const uint4& x, uint32_t c)
+    {
+        return c == 0 ? x.x : c == 1 ? x.y : c == 2 ? x.z : x.w;
+    }
+
+    template<int W, int FMT>
+    __global__ void __launch_bounds__(256) k_rec_pack(const __grid_constant__ RecPackParams q)
+    {
+        extern __shared__ __align__(16) uint32_t psm[];
+        const uint32_t w = W ? W : q.w;
+        const uint32_t ws = wstride_of(w);
+        const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * 32;
+        const uint32_t ng = static_cast<uint32_t>(q.groups - g0 < 32 ? q.groups - g0 : 32);
+        const uint32_t gw = 32 * q.nl; // region words per group
+        const uint64_t e0 = q.begin + g0 * 32;
+        const uint4* src = reinterpret_cast<const uint4*>(q.rec + e0 * q.nl * 4);
+        const uint32_t chunks = ng * 8 * q.nl;
+        const uint32_t rot = lane >> 3;
+        if(ng == 32)
+        {
+            uint4 x[8];
+#pragma unroll
+            for(int k = 0; k < 8; ++k)
+                if(k < static_cast<int>(q.nl))
+                    x[k] = __ldcs(src + threadIdx.x + 256 * k);
+#pragma unroll
+            for(int k = 0; k < 8; ++k)
+                if(k < static_cast<int>(q.nl))
+                {
+                    const uint32_t w0 = 4 * (threadIdx.x + 256 * k);
+                    uint32_t* d = psm + w0 + w0 / gw;
+#pragma unroll
+                    for(uint32_t j = 0; j < 4; ++j)
+                    {
+                        const uint32_t c = (j + rot) & 3;
+                        d[c] = comp(x[k], c);
+                    }
+                }
+        }
+        else
+            for(uint32_t ch = threadIdx.x; ch < chunks; ch += 256)
+            {
+                const uint4 x = __ldcs(src + ch);
+                const uint32_t w0 = 4 * ch;
+                uint32_t* d = psm + w0 + w0 / gw;
+#pragma unroll
+                for(uint32_t j = 0; j < 4; ++j)
+                {
+                    const uint32_t c = (j + rot) & 3;
+                    d[c] = comp(x, c);
+                }
+            }
+        __syncthreads();
+        const bool live = wp < q.nl && lane < ng;
+        uint32_t words[W ? W : 32];
+        if(live)
+        {
+            PackParams p{};
+            p.E = q.E;
+            p.M = q.M;
+            const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
+            uint32_t v[32];
+#pragma unroll
+            for(int i = 0; i < 32; ++i)
+                v[i] = enc_t<FMT>(p, psm[rec_word(q, lane * 32 + i, wp)], mask);
+            if constexpr(W != 0)
+            {
+#pragma unroll
+                for(int k = 0; k < W; ++k)
+                {
+                    uint32_t word = 0;
+#pragma unroll
+                    for(int i = (32 * k) / W; i <= (32 * k + 31) / W && i < 32; ++i)
+                    {
+                        const int pos = i * W - 32 * k;
+                        word |= pos >= 0 ? v[i] << pos : v[i] >> (-pos);
+                    }
+                    words[k] = word;
+                }
+            }
+            else
+            {
+                unsigned long long acc = 0;
+                uint32_t nb = 0, k = 0;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    acc |= static_cast<unsigned long long>(v[i]) << nb;
+                    nb += w;
+                    if(nb >= 32)
+                    {
+                        words[k++] = static_cast<uint32_t>(acc);
+                        acc >>= 32;
+                        nb -= 32;
+                    }
+                }
+            }
+        }
+        __syncthreads(); // the region is consumed: the word slices may overwrite it
+        if(wp < q.nl)
+        {
+            uint32_t* slice = psm + wp * 32 * ws;
+            if(live)
+            {
+#pragma unroll
+                for(int k = 0; k < (W ? W : 32); ++k)
+                    if(W || k < static_cast<int>(w))
+                        slice[lane * ws + k] = words[k];
+            }
+            __syncwarp();
+            uint32_t* dst = reinterpret_cast<uint32_t*>(q.bits[wp]) + (q.begin / 32 + g0) * w;
+            const uint32_t nw = ng * w;
+            for(uint32_t t = lane; t < nw; t += 32)
+                __stcs(dst + t, slice[(t / w) * ws + (t % w)]);
+        }
+    }
+
+    template<int W, int FMT>
+    __global__ void __launch_bounds__(256) k_rec_unpack(const __grid_constant__ RecPackParams q)
+    {
+        extern __shared__ __align__(16) uint32_t psm[];
+        const uint32_t w = W ? W : q.w;
+        const uint32_t ws = wstride_of(w);
+        const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * 32;
+        const uint32_t ng = static_cast<uint32_t>(q.groups - g0 < 32 ? q.groups - g0 : 32);
+        const uint32_t gw = 32 * q.nl;
+        const uint64_t e0 = q.begin + g0 * 32;
+        const bool live = wp < q.nl && lane < ng;
+        uint32_t v[32];
+        if(wp < q.nl)
+        {
+            uint32_t* slice = psm + wp * 32 * ws;
+            const uint32_t* srcw = reinterpret_cast<const uint32_t*>(q.bits[wp]) + (q.begin / 32 + g0) * w;
+            const uint32_t nw = ng * w;
+            if(W != 0 && ng == 32)
+            {
+                uint32_t t[W ? W : 1];
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                    t[k] = __ldcs(srcw + lane + 32 * k);
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t x = lane + 32 * k;
+                    slice[(x / w) * ws + (x % w)] = t[k];
+                }
+            }
+            else
+                for(uint32_t x = lane; x < nw; x += 32)
+                    slice[(x / w) * ws + (x % w)] = __ldcs(srcw + x);
+            __syncwarp();
+            if(live)
+            {
+                PackParams p{};
+                p.E = q.E;
+                p.M = q.M;
+                p.sgn = (q.sgnMask >> wp) & 1u;
+                const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
+                const uint32_t* my = slice + lane * ws;
+                if constexpr(W != 0)
+                {
+                    uint32_t wd[W];
+#pragma unroll
+                    for(int k = 0; k < W; ++k)
+                        wd[k] = my[k];
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
+                    {
+                        const int bit = i * W, k = bit >> 5, sh = bit & 31;
+                        uint32_t pat = wd[k] >> sh;
+                        if(sh + W > 32)
+                            pat |= wd[k + 1] << (32 - sh);
+                        v[i] = dec_t<FMT>(p, pat & mask, w);
+                    }
+                }
+                else
+                {
+                    unsigned long long acc = my[0];
+                    uint32_t nb = 32, k = 1;
+#pragma unroll
+                    for(int i = 0; i < 32; ++i)
+                    {
+                        if(nb < w)
+                        {
+                            acc |= static_cast<unsigned long long>(my[k < w ? k : w - 1]) << nb;
+                            ++k;
+                            nb += 32;
+                        }
+                        v[i] = dec_t<FMT>(p, static_cast<uint32_t>(acc) & mask, w);
+                        acc >>= w;
+                        nb -= w;
+                    }
+                }
+            }
+        }
+        __syncthreads(); // every slice is consumed: the record region may overwrite them
+        if(live)
+        {
+#pragma unroll
+            for(int i = 0; i < 32; ++i)
+                psm[rec_word(q, lane * 32 + i, wp)] = v[i];
+        }
+        __syncthreads();
+        uint4* dst = reinterpret_cast<uint4*>(q.rec + e0 * q.nl * 4);
+        const uint32_t chunks = ng * 8 * q.nl;
+        const uint32_t rot = lane >> 3;
+        for(uint32_t ch = threadIdx.x; ch < chunks; ch += 256)
+        {
+            const uint32_t w0 = 4 * ch;
+            const uint32_t* s = psm + w0 + w0 / gw;
+            uint32_t r[4];
+#pragma unroll
+            for(uint32_t j = 0; j < 4; ++j)
+            {
+                const uint32_t c = (j + rot) & 3;
+                r[c] = s[c];
+            }
+            __stcs(dst + ch, make_uint4(r[0], r[1], r[2], r[3]));
+        }
+    }
+
+    template<int W, int FMT>
+    static void launch_rec(const RecPackParams& q, bool pack, unsigned grid, size_t smem, cudaStream_t s)
+    {
+        static size_t setPack = 0, setUnpack = 0;
+        if(pack)
+        {
+            if(setPack < smem)
+            {
+                cudaFuncSetAttribute(k_rec_pack<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                setPack = smem;
+            }
+            k_rec_pack<W, FMT><<<grid, 256, smem, s>>>(q);
+        }
+        else
+        {
+            if(setUnpack < smem)
+            {
+                cudaFuncSetAttribute(k_rec_unpack<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+                setUnpack = smem;
+            }
+            k_rec_unpack<W, FMT><<<grid, 256, smem, s>>>(q);
+        }
+    }
+
+    template<int... Ws>
+    static bool dispatch_rec_int(int w, const RecPackParams& q, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+                                 std::integer_sequence<int, Ws...>)
+    {
+        bool hit = false;
+        ((w == Ws + 1 ? (launch_rec<Ws + 1, 0>(q, pack, grid, smem, s), hit = true) : false), ...);
+        return hit;
+    }
+
+    // kind: 0 int, 1 float
+    bool rec_pack(const RecPackParams& q, uint32_t kind, bool pack, cudaStream_t s)
+    {
+        if(q.groups == 0 || q.w < 1 || q.w > 32 || q.nl < 1 || q.nl > 8 || q.begin % 32
+           || (q.lanes != 1 && (32 % q.lanes || q.begin % q.lanes)))
+            return false;
+        const uint64_t blocks = (q.groups + 31) / 32;
+        if(blocks > 0x7FFFFFFFull)
+            return false;
+        const size_t region = 1024 * q.nl + 32, slices = static_cast<size_t>(q.nl) * 32 * wstride_of(q.w);
+        const size_t smem = (region > slices ? region : slices) * sizeof(uint32_t);
+        const unsigned grid = static_cast<unsigned>(blocks);
+        if(kind == 0)
+            dispatch_rec_int(static_cast<int>(q.w), q, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
+        else if(q.E == 8 && q.M == 10)
+            launch_rec<19, 1>(q, pack, grid, smem, s);
+        else if(q.E == 5 && q.M == 10)
+            launch_rec<16, 2>(q, pack, grid, smem, s);
+        else
+            launch_rec<0, 3>(q, pack, grid, smem, s);
+        count_launch();
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
+    }
+
     // grid-stride kernels: never launch more CTAs than can be resident at once (a partial
     // second wave would run a full share of the work late)
     // grid-stride with 32 CTAs per SM (8-10 waves of the resident count): measured best across

@@ -308,3 +308,22 @@ def test_copy_host_pipeline_heatmap(wrap):
     for x, y in zip(got, db):
         assert np.array_equal(x, y)
     assert np.array_equal(dc, O.counters(md))
+
+
+@pytest.mark.parametrize("rec", ["aos-packed", "aosoa:4", "aosoa:8", "aosoa:16"])
+@pytest.mark.parametrize("n", [3239, 70001])
+def test_record_side_bitpack_one_pass(rec, n):
+    """pack.cu k_rec_pack / k_rec_unpack: a record-contiguous side (AoS, AoSoA<L>, L | 32) against
+    bit streams, several 1024-record CTAs, a partial CTA and a generic tail, both directions,
+    signed/unsigned ints and the three float codecs, FieldAccessCount on either side."""
+    rng = np.random.default_rng(n)
+    cases = [("Record{v:u32,w:i32,x:i32}", [6, 2, 2], f"bitpack-int:{b}") for b in (3, 12, 31)]
+    cases += [(R32, [8] * 7, f"bitpack-float:{f}") for f in ("8,10", "5,10", "4,3")]
+    for schema, types, packed in cases:
+        vals = random_values(rng, types, n)
+        run_pair(schema, n, rec, packed, vals, dst_wrap=1 if "5,10" in packed else 0)
+        pm = O.make(schema, f"i32:[{n}]", packed)
+        pb = O.zero_blobs(pm)
+        O.write_all(pm, pb, vals)
+        back = O.read_all(pm, pb)
+        run_pair(schema, n, packed, rec, back, src_wrap=1 if "8,10" in packed else 0)
