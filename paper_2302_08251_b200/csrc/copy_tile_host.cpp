@@ -54,6 +54,7 @@ namespace lamk
         unsigned long long begin, groups;
         uint32_t nl, lanes, lsh, sgnMask;
         uint32_t w, E, M;
+        uint32_t gmag;
     };
     bool rec_pack(const RecPackParams& q, uint32_t kind, bool pack, cudaStream_t s);
 
@@ -737,6 +738,7 @@ namespace lamhost
         if(begin % q.lanes || (q.rec + begin * nl * 4) % 16)
             return false;
         q.nl = nl;
+        q.gmag = ((1u << 24) + 32 * nl - 1) / (32 * nl);
         q.begin = begin;
         q.groups = groups;
         return lamk::rec_pack(q, kind, packDir, s);

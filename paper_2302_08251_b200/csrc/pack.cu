@@ -421,12 +421,19 @@ namespace lamk
         unsigned long long groups;  // groups of 32 elements
         uint32_t nl, lanes, lsh, sgnMask;
         uint32_t w, E, M;
+        uint32_t gmag; // ceil(2^24 / (32 nl)): region word -> group by multiply-shift (exact below 2^13 words)
     };
 
-    __device__ __forceinline__ uint32_t rec_word(const RecPackParams& q, uint32_t e, uint32_t l)
+    // region word w (record e, leaf l) sits at smem word w + e / 32 (one pad word per group of 32
+    // records); lane `g` of warp `l` reads record i of its group at base + (i >> lsh) * nl * L + (i & (L - 1))
+    __device__ __forceinline__ uint32_t rec_base(const RecPackParams& q, uint32_t lane, uint32_t wp)
     {
-        const uint32_t w = q.lanes == 1 ? e * q.nl + l : ((e >> q.lsh) * q.nl + l) * q.lanes + (e & (q.lanes - 1));
-        return w + (e >> 5); // one pad word per group of 32 records
+        return lane * (32 * q.nl + 1) + wp * q.lanes;
+    }
+
+    __device__ __forceinline__ uint32_t pad_of(const RecPackParams& q, uint32_t w0)
+    {
+        return (w0 * q.gmag) >> 24;
     }
 
     // region word `w0 + c` (c = 0..3 of a 16-byte chunk) lives at smem w0 + c + group; the four
@@ -445,7 +452,6 @@ namespace lamk
         const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
         const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * 32;
         const uint32_t ng = static_cast<uint32_t>(q.groups - g0 < 32 ? q.groups - g0 : 32);
-        const uint32_t gw = 32 * q.nl; // region words per group
         const uint64_t e0 = q.begin + g0 * 32;
         const uint4* src = reinterpret_cast<const uint4*>(q.rec + e0 * q.nl * 4);
         const uint32_t chunks = ng * 8 * q.nl;
@@ -462,7 +468,7 @@ namespace lamk
                 if(k < static_cast<int>(q.nl))
                 {
                     const uint32_t w0 = 4 * (threadIdx.x + 256 * k);
-                    uint32_t* d = psm + w0 + w0 / gw;
+                    uint32_t* d = psm + w0 + pad_of(q, w0);
 #pragma unroll
                     for(uint32_t j = 0; j < 4; ++j)
                     {
@@ -476,7 +482,7 @@ namespace lamk
             {
                 const uint4 x = __ldcs(src + ch);
                 const uint32_t w0 = 4 * ch;
-                uint32_t* d = psm + w0 + w0 / gw;
+                uint32_t* d = psm + w0 + pad_of(q, w0);
 #pragma unroll
                 for(uint32_t j = 0; j < 4; ++j)
                 {
@@ -494,9 +500,23 @@ namespace lamk
             p.M = q.M;
             const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
             uint32_t v[32];
+            const uint32_t* pv = psm + rec_base(q, lane, wp);
+            if(q.lanes == 1)
+            {
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                    v[i] = pv[i * q.nl];
+            }
+            else
+            {
+                const uint32_t nlL = q.nl * q.lanes, lm = q.lanes - 1;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                    v[i] = pv[(i >> q.lsh) * nlL + (i & lm)];
+            }
 #pragma unroll
             for(int i = 0; i < 32; ++i)
-                v[i] = enc_t<FMT>(p, psm[rec_word(q, lane * 32 + i, wp)], mask);
+                v[i] = enc_t<FMT>(p, v[i], mask);
             if constexpr(W != 0)
             {
 #pragma unroll
@@ -558,7 +578,6 @@ namespace lamk
         const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
         const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * 32;
         const uint32_t ng = static_cast<uint32_t>(q.groups - g0 < 32 ? q.groups - g0 : 32);
-        const uint32_t gw = 32 * q.nl;
         const uint64_t e0 = q.begin + g0 * 32;
         const bool live = wp < q.nl && lane < ng;
         uint32_t v[32];
@@ -631,9 +650,20 @@ namespace lamk
         __syncthreads(); // every slice is consumed: the record region may overwrite them
         if(live)
         {
+            uint32_t* pv = psm + rec_base(q, lane, wp);
+            if(q.lanes == 1)
+            {
 #pragma unroll
-            for(int i = 0; i < 32; ++i)
-                psm[rec_word(q, lane * 32 + i, wp)] = v[i];
+                for(int i = 0; i < 32; ++i)
+                    pv[i * q.nl] = v[i];
+            }
+            else
+            {
+                const uint32_t nlL = q.nl * q.lanes, lm = q.lanes - 1;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                    pv[(i >> q.lsh) * nlL + (i & lm)] = v[i];
+            }
         }
         __syncthreads();
         uint4* dst = reinterpret_cast<uint4*>(q.rec + e0 * q.nl * 4);
@@ -642,7 +672,7 @@ namespace lamk
         for(uint32_t ch = threadIdx.x; ch < chunks; ch += 256)
         {
             const uint32_t w0 = 4 * ch;
-            const uint32_t* s = psm + w0 + w0 / gw;
+            const uint32_t* s = psm + w0 + pad_of(q, w0);
             uint32_t r[4];
 #pragma unroll
             for(uint32_t j = 0; j < 4; ++j)
