@@ -442,6 +442,42 @@ namespace lamk
     {
         return c == 0 ? x.x : c == 1 ? x.y : c == 2 ? x.z : x.w;
     }
+#ifndef LAMB_REC_ROTATE
+#define LAMB_REC_ROTATE 0
+#endif
+    // rotated: conflict-free STS/LDS.32 at 3 selects per word; plain: 4-way conflicts (MIO
+    // wavefronts, not issue slots -- the kernels are issue-bound, so plain measured faster)
+#if LAMB_REC_ROTATE
+#define STORE4(d, vec)                                                                                                   \
+    _Pragma("unroll") for(uint32_t j = 0; j < 4; ++j)                                                                  \
+    {                                                                                                                  \
+        const uint32_t c = (j + rot) & 3;                                                                              \
+        (d)[c] = comp((vec), c);                                                                                         \
+    }
+#define LOAD4(r, s)                                                                                                    \
+    _Pragma("unroll") for(uint32_t j = 0; j < 4; ++j)                                                                  \
+    {                                                                                                                  \
+        const uint32_t c = (j + rot) & 3;                                                                              \
+        (r)[c] = (s)[c];                                                                                               \
+    }
+#else
+#define STORE4(d, vec)                                                                                                   \
+    {                                                                                                                  \
+        (void)rot;                                                                                                     \
+        (d)[0] = (vec).x;                                                                                                \
+        (d)[1] = (vec).y;                                                                                                \
+        (d)[2] = (vec).z;                                                                                                \
+        (d)[3] = (vec).w;                                                                                                \
+    }
+#define LOAD4(r, s)                                                                                                    \
+    {                                                                                                                  \
+        (void)rot;                                                                                                     \
+        (r)[0] = (s)[0];                                                                                               \
+        (r)[1] = (s)[1];                                                                                               \
+        (r)[2] = (s)[2];                                                                                               \
+        (r)[3] = (s)[3];                                                                                               \
+    }
+#endif
 
     template<int W, int FMT>
     __global__ void __launch_bounds__(256) k_rec_pack(const __grid_constant__ RecPackParams q)
@@ -469,12 +505,7 @@ namespace lamk
                 {
                     const uint32_t w0 = 4 * (threadIdx.x + 256 * k);
                     uint32_t* d = psm + w0 + pad_of(q, w0);
-#pragma unroll
-                    for(uint32_t j = 0; j < 4; ++j)
-                    {
-                        const uint32_t c = (j + rot) & 3;
-                        d[c] = comp(x[k], c);
-                    }
+                    STORE4(d, x[k]);
                 }
         }
         else
@@ -483,12 +514,7 @@ namespace lamk
                 const uint4 x = __ldcs(src + ch);
                 const uint32_t w0 = 4 * ch;
                 uint32_t* d = psm + w0 + pad_of(q, w0);
-#pragma unroll
-                for(uint32_t j = 0; j < 4; ++j)
-                {
-                    const uint32_t c = (j + rot) & 3;
-                    d[c] = comp(x, c);
-                }
+                STORE4(d, x);
             }
         __syncthreads();
         const bool live = wp < q.nl && lane < ng;
@@ -674,12 +700,7 @@ namespace lamk
             const uint32_t w0 = 4 * ch;
             const uint32_t* s = psm + w0 + pad_of(q, w0);
             uint32_t r[4];
-#pragma unroll
-            for(uint32_t j = 0; j < 4; ++j)
-            {
-                const uint32_t c = (j + rot) & 3;
-                r[c] = s[c];
-            }
+            LOAD4(r, s);
             __stcs(dst + ch, make_uint4(r[0], r[1], r[2], r[3]));
         }
     }
