@@ -28,10 +28,11 @@ namespace lamhost
             && b.isFullyPhysical();
     }
 
-    // Bit-packed <-> record-contiguous (AoS / AoSoA) copies of 32-bit leaves have no one-pass
-    // kernel: stage through an SoA multi-blob scratch view so both halves run on the specialised
-    // kernels (k_vec_transpose, k_pack32 / k_unpack32).  Every element is still read once from
-    // the source view and written once to the destination view (counters unchanged).
+    // Bit-packed <-> record-contiguous copies of 32-bit leaves that the one-pass kernels do not
+    // take (k_rec_pack: AoS / AoSoA<L | 32> with one bit width; k_pack32: SoA / AoSoA<32k>) are
+    // staged through an SoA multi-blob scratch view so both halves run on specialised kernels
+    // (k_vec_transpose, k_pack32 / k_unpack32).  Every element is still read once from the source
+    // view and written once to the destination view (counters unchanged).
     static bool hasBits(const Lowered& L)
     {
         for(const auto& st : L.streams)
@@ -68,7 +69,7 @@ namespace lamhost
     static bool recordSide32(const Lowered& L)
     {
         const size_t nl = L.roots.size();
-        if(nl < 1 || nl > 8)
+        if(nl < 2 || nl > 8)
             return false;
         const uint16_t s0 = L.nodes[L.roots[0]].stream;
         const lamp_stream& st = L.streams[s0];

@@ -260,10 +260,21 @@ namespace lamk
         return a >= 0 ? a / b : -((-a + b - 1) / b);
     }
 
+    // floor(a / b) for b > 0 without the 64-bit division subroutine: a double-precision quotient
+    // estimate (|a| < 2^53, so it is off by at most one) corrected with one integer multiply
+    __device__ __forceinline__ int64_t floor_div_r(int64_t a, int64_t b, double invb)
+    {
+        int64_t q = static_cast<int64_t>(floor(static_cast<double>(a) * invb));
+        const int64_t r = a - q * b;
+        q += r < 0 ? -1 : (r >= b ? 1 : 0);
+        return q;
+    }
+
     __global__ void __launch_bounds__(256) k_heat_closed(const __grid_constant__ HeatParams p)
     {
         const HeatStream& st = p.st[blockIdx.y];
         const int64_t g = static_cast<int64_t>(p.gran), bs = static_cast<int64_t>(st.bs), b0 = static_cast<int64_t>(st.base0);
+        const double invbs = 1.0 / static_cast<double>(bs);
         const int64_t first = (b0 + static_cast<int64_t>(p.begin) * bs) / g;
         const int64_t last = (b0 + static_cast<int64_t>(p.end) * bs - 1) / g;
         const int64_t eb = static_cast<int64_t>(p.begin), ee = static_cast<int64_t>(p.end) - 1;
@@ -277,8 +288,8 @@ namespace lamk
                 const HeatTerm& ht = p.term[t];
                 const int64_t off = b0 + ht.inblock;
                 // overlap: off + e*bs < (b+1)g  and  off + e*bs + size > b*g
-                int64_t lo = floor_div(b * g - off - static_cast<int64_t>(ht.size), bs) + 1;
-                int64_t hi = floor_div((b + 1) * g - off - 1, bs);
+                int64_t lo = floor_div_r(b * g - off - static_cast<int64_t>(ht.size), bs, invbs) + 1;
+                int64_t hi = floor_div_r((b + 1) * g - off - 1, bs, invbs);
                 lo = lo < eb ? eb : lo;
                 hi = hi > ee ? ee : hi;
                 if(hi >= lo)

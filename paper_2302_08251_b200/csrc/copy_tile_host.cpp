@@ -683,7 +683,8 @@ namespace lamhost
     static bool tryRecPack(const lamt_params& p, uint64_t begin, uint64_t groups, cudaStream_t s)
     {
         const uint32_t nl = p.nleaves;
-        if(nl < 1 || nl > 8 || envNum("LAMB_RECPACK", 1) == 0)
+        // one leaf: the record stream is an SoA array, which k_pack32 handles with every warp busy
+        if(nl < 2 || nl > 8 || envNum("LAMB_RECPACK", 1) == 0)
             return false;
         lamk::RecPackParams q{};
         bool packDir = false;
