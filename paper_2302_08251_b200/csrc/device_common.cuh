@@ -187,8 +187,9 @@ namespace lamd
     LAM_DEV uint32_t encode_e5m10_f32(uint32_t b)
     {
         const uint32_t a = b & 0x7FFFFFFFu;
-        const uint32_t h = __half_as_ushort(__float2half_rn(__uint_as_float(b)));
-        return a > 0x7F800000u ? (((b >> 31) << 15) | 0x7E00u) : h; // NaN: the reference's canonical quiet pattern
+        if(a > 0x7F800000u)
+            return ((b >> 31) << 15) | 0x7E00u;
+        return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__uint_as_float(b))));
     }
 
     // ---- raw byte access ----------------------------------------------------------------
