@@ -17,6 +17,9 @@ PAIRS = [
     (R64, "aos-packed", "changetype:f64=f32:bytesplit:soa-mb"), (R64, "changetype:f64=f32:bytesplit:soa-mb", "aos-packed"),
     (MIXED, "aos-packed", "soa-mb"), (MIXED, "soa-sb", "aos-aligned"),
     ("Record{v:u32,w:i32}", "soa-mb", "bitpack-int:7"), ("Record{v:u32,w:i32}", "bitpack-int:13", "soa-mb"),
+    # record-side one-pass packing (k_rec_pack / k_rec_unpack)
+    (R32, "bitpack-float:8,10", "aos-packed"), (R32, "bitpack-float:5,10", "aosoa:8"), (R32, "aosoa:16", "bitpack-float:8,10"),
+    ("Record{v:u32,w:i32}", "bitpack-int:7", "aos-packed"), ("Record{v:u32,w:i32}", "aosoa:4", "bitpack-int:29"),
 ]
 
 
