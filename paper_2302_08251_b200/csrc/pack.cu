@@ -206,7 +206,7 @@ namespace lamk
 
     // pack: 32 values -> W words per thread (W = 0: runtime width p.w)
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, FMT == 1 ? 4 : 3) k_pack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, 3) k_pack32(const __grid_constant__ PackParams p)
     {
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
