@@ -205,8 +205,15 @@ namespace lamk
     }
 
     // pack: 32 values -> W words per thread (W = 0: runtime width p.w)
+    // register bound: 3 CTAs/SM (80 registers) except the integer widths that spill there (even
+    // W from 10 to 30 but 16); a (256, 4) bound on e8m10 had cost it 17% (profiles/README.md)
+    __host__ __device__ constexpr int pack_minb(int W, int FMT)
+    {
+        return (FMT == 0 && W >= 10 && W % 2 == 0 && W != 16 && W != 32) ? 2 : 3;
+    }
+
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, 3) k_pack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackParams p)
     {
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
