@@ -11,12 +11,15 @@ Algorithmic bytes = source leaf bytes read + destination leaf bytes written
   value  : whole-job GB/s, device-resident views, CUDA events, max over ranks
   e2e    : same metric through lam_copy_host (host pinned blobs in and out, H2D/D2H
            inside the timed region)
-  roofline: dominant kernel k_tile_copy, algorithmic bytes / mean launch time vs the
-           measured HBM copy peak (MEASURED_PEAKS.json)
+  roofline: dominant kernel k_vec_transpose<7,4>, algorithmic bytes / mean launch time vs
+           the measured HBM copy peak (MEASURED_PEAKS.json)
+  parity : after the timed region, every pair's destination is checked bit-exactly against the
+           reference copyView on three 2^20-record ranges (checker leg)
   cpu_baseline: the reference itself (oracle/_ref, compiled from /root/reference) on a
-           bounded sample, 1 host core
+           bounded sample (2^24 records x 25 pairs), all host threads
 
---impl reference : the reference's CPU copyView loop (oracle/_ref) on all host cores.
+--impl reference : the reference's copyView (oracle/_ref) on the SAME workload (2^26 records x
+                   25 pairs per step), all host threads over disjoint index ranges.
 --suite          : additionally time configs C1, C3, C5 and n-body (C4) on this GPU.
 """
 from __future__ import annotations
@@ -151,17 +154,27 @@ def sum_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def fill_source(L, view, layout_text, n, seed, stream):
-    """Synthetic source content: random u32 patterns per (i, f) including NaN/sNaN/±0/
-    denormal bit patterns — a layout copy is a byte permutation, so every pattern must
-    survive.  Generated once in aos-packed on the device, then copied into `view`."""
+SPECIAL_U32 = (0x7FC00000, 0xFFC00000, 0x7F800001, 0xFFA00001, 0x7F800000, 0xFF800000, 0x00000001, 0x80000001,
+               0x007FFFFF, 0x80000000, 0x00000000)
+
+
+def fill_source(L, view, n, seed):
+    """Synthetic source content: full-range random u32 patterns per (i, f), with about 1 in 50
+    values replaced by NaN / sNaN / +-0 / denormal / Inf patterns (a layout copy is a byte
+    permutation, so every pattern must survive).  Generated in aos-packed on the device, then
+    copied into `view` by the library; device-synchronised on both sides, so the zero-fill of
+    the view (lam_view_alloc), the generator and the copy never overlap."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(seed)
-    raw = torch.randint(0, 2**31 - 1, (n * 7,), device="cuda", dtype=torch.int32, generator=g)
+    raw = torch.randint(-2**31, 2**31, (n * 7,), device="cuda", dtype=torch.int32, generator=g)
+    pick = torch.randint(0, 50, (n * 7,), device="cuda", generator=g) == 0
+    special = torch.tensor([x - 2**32 if x >= 2**31 else x for x in SPECIAL_U32], device="cuda", dtype=torch.int32)
+    raw = torch.where(pick, special[torch.randint(0, len(SPECIAL_U32), (n * 7,), device="cuda", generator=g)], raw)
     raw = raw.view(torch.uint8)
     aos = L.Layout(R32, f"i32:[{n}]", "aos-packed")
+    torch.cuda.synchronize()
     tmp = L.View(aos, blobs=[raw.data_ptr()], blob_bytes=[raw.numel()])
-    L.copy_view(tmp, view, stream=stream)
+    L.copy_view(tmp, view)
     torch.cuda.synchronize()
     del tmp, raw
 
@@ -174,7 +187,7 @@ def run_c2(L, n, steps, warmup, world, local):
     srcs = {a: L.View(lays[a], device=local) for a in C2_LAYOUTS}
     dsts = {a: L.View(lays[a], device=local) for a in C2_LAYOUTS}
     for k, a in enumerate(C2_LAYOUTS):
-        fill_source(L, srcs[a], a, n, 1234 + k, stream)
+        fill_source(L, srcs[a], n, 1234 + k)
     pairs = [(a, b) for a in C2_LAYOUTS for b in C2_LAYOUTS]
     bytes_pair = 56 * n
     ev = [{p: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for p in pairs}
@@ -210,9 +223,7 @@ def run_c2(L, n, steps, warmup, world, local):
     per_pair = {f"{a}->{b}": round(bytes_pair / (pair_ms[(a, b)] / steps * 1e-3) / 1e9, 1) for a, b in pairs}
     out = {"ms_per_step": ms_max, "value": value, "launches": launches, "clocks": clk.summary(),
            "achieved_tile": achieved, "tile_ms": tile_ms, "per_pair_gbs": per_pair, "bytes_step": bytes_step,
-           "wall_ms_per_step": total_ms / steps}
-    del srcs, dsts
-    torch.cuda.synchronize()
+           "wall_ms_per_step": total_ms / steps, "views": (srcs, dsts)}
     return out
 
 
@@ -293,21 +304,68 @@ def pcie_bandwidth(local, nbytes=1 << 30):
     return {"h2d": nbytes / t_h2d / 1e9, "d2h": nbytes / t_d2h / 1e9, "bidirectional": 2 * nbytes / t_bi / 1e9}
 
 
-def cpu_reference_c2(n, nthreads, repeats=1):
-    """The reference's copyView (oracle/_ref) over the 25 pairs on n records."""
+class RefC2:
+    """The reference's copyView (oracle/_ref, the unmodified lamina library) over the 25 C2
+    pairs on resident reference views of n records: 5 sources (random u32 patterns, aos-packed
+    drawn once and copied into the other layouts by the reference) and 5 destinations.  One
+    step = 25 copyView calls; nthreads > 1 runs the loop body over disjoint index ranges
+    (SURVEY 8(d) variant ii; the same-layout pairs take the blob-memcpy path split by bytes)."""
+
+    def __init__(self, n, nthreads, seed=3):
+        from oracle import ref
+        ext = f"i32:[{n}]"
+        self.n, self.nthreads = n, nthreads
+        self.src = {a: ref.RefView(R32, ext, a) for a in C2_LAYOUTS}
+        self.dst = {a: ref.RefView(R32, ext, a) for a in C2_LAYOUTS}
+        rng = np.random.default_rng(seed)
+        blob = self.src["aos-packed"].blobs[0].view(np.uint32)
+        step = 1 << 24
+        for lo in range(0, blob.size, step):
+            blob[lo:lo + step] = rng.integers(0, 2**32, min(step, blob.size - lo), dtype=np.uint32)
+        for a in C2_LAYOUTS[1:]:
+            self.src[a].copy_from(self.src["aos-packed"], nthreads)
+
+    def step(self):
+        """Seconds of the 25 copyView calls (wall clock of each call, summed)."""
+        return sum(self.dst[b].copy_from(self.src[a], self.nthreads)[0] for a in C2_LAYOUTS for b in C2_LAYOUTS)
+
+
+def check_c2_parity(L, srcs, dsts, n, nthreads, chunk=1 << 20):
+    """Bit-exact check of the timed workload (checker leg, after the timed region).  For every
+    pair, the GPU copies the full 2^26-record view again; three record ranges [lo, lo+chunk)
+    (first, middle, last) of its destination are compared with the reference copyView of a
+    chunk view whose blobs are the same ranges of the GPU source (SURVEY 8(d) slice rules)."""
     from oracle import ref
-    ext = f"i32:[{n}]"
-    rng = np.random.default_rng(3)
-    total_s = 0.0
-    src = {}
+    cext = f"i32:[{chunk}]"
+    checked = 0
+    los = (0, (n // 2) // chunk * chunk, n - chunk)
     for a in C2_LAYOUTS:
-        src[a] = [rng.integers(0, 256, s, dtype=np.uint8) for s in ref.layout_info(R32, ext, a)["blob_sizes"]]
-    for a in C2_LAYOUTS:
+        chunk_src = {}
+        for lo in los:
+            ca = ref.RefView(R32, cext, a)
+            for g, glo, ghi, cbn, clo, chi in _c2_slices(a, n, lo, chunk):
+                ca.blobs[cbn][clo:chi] = srcs[a].download_range(g, glo, ghi - glo)
+            chunk_src[lo] = ca
         for b in C2_LAYOUTS:
-            dst = ref.zero_blobs(R32, ext, b)
-            r = ref.copy(R32, ext, a, src[a], b, dst, nthreads=nthreads, repeats=repeats)
-            total_s += r["seconds"]
-    return 56 * n * 25 / total_s / 1e9, total_s
+            L.copy_view(srcs[a], dsts[b])
+            for lo in los:
+                cb = ref.RefView(R32, cext, b)
+                cb.copy_from(chunk_src[lo], nthreads)
+                for g, glo, ghi, cbn, clo, chi in _c2_slices(b, n, lo, chunk):
+                    got = dsts[b].download_range(g, glo, ghi - glo)
+                    if not np.array_equal(got, cb.blobs[cbn][clo:chi]):
+                        raise AssertionError(f"bench parity: {a} -> {b} records [{lo}, {lo + chunk}) differ")
+                    checked += ghi - glo
+    return {"pairs": 25, "ranges_per_pair": len(los), "records_per_range": chunk, "bytes_compared": checked,
+            "bit_exact": True, "against": "reference copyView (oracle/_ref) of the same source bytes"}
+
+
+def _c2_slices(layout, n, a, c):
+    if layout == "aos-packed" or layout.startswith("aosoa:"):
+        return [(0, 28 * a, 28 * (a + c), 0, 0, 28 * c)]
+    if layout == "soa-mb":
+        return [(f, 4 * a, 4 * (a + c), f, 0, 4 * c) for f in range(7)]
+    return [(0, 4 * n * f + 4 * a, 4 * n * f + 4 * (a + c), 0, 4 * c * f, 4 * c * (f + 1)) for f in range(7)]
 
 
 def main():
@@ -317,7 +375,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--records", type=int, default=1 << 26)
-    ap.add_argument("--cpu-records", type=int, default=1 << 20)
+    ap.add_argument("--cpu-records", type=int, default=1 << 24)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -342,20 +400,22 @@ def main():
         if not ref.available():
             ref.build()
         threads = os.cpu_count() or 1
-        samples = []
+        t0 = time.perf_counter()
+        rc2 = RefC2(n, threads)
+        setup_s = time.perf_counter() - t0
         for _ in range(args.warmup):
-            cpu_reference_c2(args.cpu_records * 4, threads)
-        for _ in range(args.steps):
-            v, s = cpu_reference_c2(args.cpu_records * 4, threads)
-            samples.append(s)
-        total = float(np.median(samples))
-        value = 56 * args.cpu_records * 4 * 25 / total / 1e9
+            rc2.step()
+        samples = [rc2.step() for _ in range(args.steps)]
+        total = float(sum(samples))
+        value = 56 * n * 25 * args.steps / total / 1e9
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": total * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-                "config": dict(config, records_per_step=args.cpu_records * 4),
+                "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (random u32 bit patterns)",
+                "impl": "reference", "config": config,
                 "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
-                                 "sample": f"25 pairs x {args.cpu_records * 4} records per step (bounded sample of C2)"},
+                                 "sample": f"the full workload: 25 pairs x {n} records per step, reference copyView "
+                                           f"(oracle/_ref) on resident reference views, {threads} threads over "
+                                           f"disjoint index ranges; view setup {setup_s:.1f} s untimed"},
                 "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -379,25 +439,38 @@ def main():
     line["roofline"] = {"bound": "hbm", "kernel": "k_vec_transpose<7,4> (the 20 cross-layout pairs)",
                         "achieved": res["achieved_tile"], "peak": peak, "unit": "GB/s",
                         "frac": res["achieved_tile"] / peak, "traffic": traffic,
+                        "traffic_source": "committed ncu constant (profiles/vec_traffic.json: dram__bytes_read.sum + "
+                                          "dram__bytes_write.sum of one k_vec_transpose<7,4> launch at 2^26 records, "
+                                          "ncu --set full; re-captured whenever that kernel changes)",
                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                         "spec_peak_GBps": 8000.0, "frac_of_spec": res["achieved_tile"] / 8000.0,
                         "algorithmic_bytes_per_launch": 56 * n}
     line["per_pair_gbs"] = res["per_pair_gbs"]
+    srcs, dsts = res.pop("views")
+    if rank == 0 and not args.no_cpu:
+        from oracle import ref
+        if ref.available():
+            # checker: the timed workload's bytes against the reference (first / middle / last ranges)
+            line["parity"] = check_c2_parity(L, srcs, dsts, n, os.cpu_count() or 1)
+            # cpu_baseline: the reference on a bounded sample of the workload, every host thread
+            threads = os.cpu_count() or 1
+            rc2 = RefC2(args.cpu_records, threads)
+            s = rc2.step()
+            line["cpu_baseline"] = {"value": 56 * args.cpu_records * 25 / s / 1e9, "unit": "GB/s", "cores": threads,
+                                    "kind": "reference",
+                                    "sample": f"25 pairs x {args.cpu_records} records (bounded sample of C2), reference "
+                                              f"copyView (oracle/_ref), {threads} threads, {s:.1f} s"}
+            del rc2
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
+                                    "sample": "oracle/_ref not built"}
+    del srcs, dsts
+    torch.cuda.synchronize()
     if not args.no_e2e:
         # N>1: 2^24 records per GPU for the host leg (5 x 470 MB pinned per rank instead of 9.4 GB)
         e2e = run_c2_e2e(L, n if world == 1 else min(n, 1 << 24), args.e2e_steps, local, world)
         if rank == 0:
             line["e2e"] = e2e
-    if rank == 0 and not args.no_cpu:
-        from oracle import ref
-        if ref.available():
-            v, s = cpu_reference_c2(args.cpu_records, 1)
-            line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": 1, "kind": "reference",
-                                    "sample": f"25 pairs x {args.cpu_records} records (bounded sample of C2), "
-                                              f"reference copyView single-threaded, {s:.1f} s"}
-        else:
-            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
-                                    "sample": "oracle/_ref not built"}
     if args.suite and rank == 0:
         from bench_suite import run_suite
         line["suite"] = run_suite(L, local)

@@ -139,6 +139,12 @@ const void* lam_view_device_plan(const lam_view* view);
 /* Stream-ordered host<->device blob transfer (pinned host memory makes them async). */
 int lam_view_upload(lam_view* view, size_t nr, const void* host, void* stream);
 int lam_view_download(const lam_view* view, size_t nr, void* host, void* stream);
+/* Byte sub-range [offset, offset + nbytes) of blob nr (the reference exposes blobs as spans,
+ * View::blobs(), view.hpp:133-141); out-of-bounds ranges fail with "index out of range". */
+int lam_view_upload_range(lam_view* view, size_t nr, uint64_t offset, uint64_t nbytes, const void* host,
+                          void* stream);
+int lam_view_download_range(const lam_view* view, size_t nr, uint64_t offset, uint64_t nbytes, void* host,
+                            void* stream);
 
 /* ---- view dump / restore (core/include/lamina/view_io.hpp; core/src/view_io.cpp:28-129) ----
  * The reference's on-disk format: <stem>.meta (schema=, extents=, extent-values=, mapping=,

@@ -61,6 +61,14 @@ def lib():
         L.ref_nbody.argtypes = [cp, u64, u64, i32, u64, i32, i32, P(vp), P(dbl), P(dbl), P(dbl)]
         L.ref_nbody_cli.argtypes = [cp, u64, u64, i32, u64, i32]
         L.ref_nbody_trace.argtypes = [cp, u64, u64, i32, u64, i32, u64, cp, cp]
+        L.ref_view_new.restype = vp
+        L.ref_view_new.argtypes = [cp, cp, P(u64), sz, cp, i32, u64]
+        L.ref_view_free.argtypes = [vp]
+        L.ref_view_blob_count.restype = sz
+        L.ref_view_blob_count.argtypes = [vp]
+        L.ref_view_blob.restype = vp
+        L.ref_view_blob.argtypes = [vp, sz, P(u64)]
+        L.ref_view_copy.argtypes = [vp, vp, i32, P(dbl), P(u64)]
         L.ref_contiguous_run.argtypes = [cp, cp, P(u64), C.c_size_t, cp, i32, u64, u64, C.c_size_t, u64, P(C.c_int),
                                          P(C.c_size_t), P(u64)]
         _lib = L
@@ -209,3 +217,37 @@ def contiguous_run(schema, extents, layout, linear, leaf, n, dyn=(), wrap=0, gra
     _check(lib().ref_contiguous_run(schema.encode(), extents.encode(), d, nd, layout.encode(), wrap, gran, linear, leaf,
                                     n, C.byref(has), C.byref(nr), C.byref(off)))
     return (nr.value, off.value) if has.value else None
+
+
+class RefView:
+    """A resident lamina::View (zeroed Blobs owned by the reference) whose blobs are exposed
+    as writable numpy arrays; copy_from runs the reference copyView into it."""
+
+    def __init__(self, schema, extents, layout, dyn=(), wrap=0, gran=0):
+        d, nd = _dyn(dyn)
+        self._h = lib().ref_view_new(schema.encode(), extents.encode(), d, nd, layout.encode(), wrap, gran)
+        if not self._h:
+            _check(lib().ref_last_kind() or 5)
+        self.leaves = layout_info(schema, extents, layout, dyn, wrap, gran)["leaves"]
+        self.blobs = []
+        for nr in range(lib().ref_view_blob_count(self._h)):
+            size = C.c_uint64()
+            ptr = lib().ref_view_blob(self._h, nr, C.byref(size))
+            if size.value == 0:
+                self.blobs.append(np.zeros(0, np.uint8))
+            else:
+                self.blobs.append(np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(size.value,)))
+
+    def copy_from(self, src: "RefView", nthreads=1):
+        """copyView(src, self); returns (seconds, dst FieldAccessCount [reads..., writes...])."""
+        secs = C.c_double()
+        fac = np.zeros(max(1, 2 * self.leaves), np.uint64)
+        _check(lib().ref_view_copy(src._h, self._h, nthreads, C.byref(secs),
+                                   fac.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return secs.value, fac[: 2 * self.leaves]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self.blobs = []
+            lib().ref_view_free(self._h)
+            self._h = None

@@ -168,6 +168,61 @@ namespace
     {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     }
+
+    /// lamina::copyView(src, dst) (view.cpp:168-189) for nthreads <= 1; otherwise the same
+    /// dispatch with the fieldwise loop body dst.write(i,f,src.read(i,f)) (view.cpp:186-188)
+    /// over disjoint 64-element-aligned index ranges, and the blob memcpy path split by bytes.
+    void copyThreaded(const View& src, View& dst, int nthreads)
+    {
+        if(nthreads <= 1)
+            copyView(src, dst);
+        else
+        {
+            const Mapping& a = src.mapping();
+            const Mapping& b = dst.mapping();
+            if(!(a.schema() == b.schema()) || !(a.extents() == b.extents()))
+                throw std::invalid_argument("incompatible views");
+            const bool sameLayout = a.name() == b.name() && !a.hasMutableState()
+                && !b.hasMutableState() && a.isFullyPhysical() && b.isFullyPhysical();
+            std::vector<std::thread> pool;
+            if(sameLayout)
+            {
+                for(int t = 0; t < nthreads; ++t)
+                    pool.emplace_back(
+                        [&, t]
+                        {
+                            for(std::size_t nr = 0; nr < a.blobCount(); ++nr)
+                            {
+                                const std::size_t sz = a.blobSize(nr);
+                                const std::size_t lo = sz * t / nthreads;
+                                const std::size_t hi = sz * (t + 1) / nthreads;
+                                std::memcpy(
+                                    dst.blobs()[nr].data() + lo,
+                                    src.blobs()[nr].data() + lo,
+                                    hi - lo);
+                            }
+                        });
+            }
+            else
+            {
+                const std::uint64_t n = a.elementCount();
+                const std::size_t leaves = a.schema().leafCount();
+                const std::uint64_t units = (n + 63) / 64;
+                for(int t = 0; t < nthreads; ++t)
+                    pool.emplace_back(
+                        [&, t]
+                        {
+                            const std::uint64_t lo = std::min(n, units * t / nthreads * 64);
+                            const std::uint64_t hi = std::min(n, units * (t + 1) / nthreads * 64);
+                            for(std::uint64_t i = lo; i < hi; ++i)
+                                for(std::size_t f = 0; f < leaves; ++f)
+                                    dst.write(i, f, src.read(i, f));
+                        });
+            }
+            for(auto& th : pool)
+                th.join();
+        }
+    }
 } // namespace
 
 extern "C"
@@ -263,54 +318,7 @@ extern "C"
                     if(auto h = heatOf(&dst.mapping()))
                         h->reset();
                     const double t0 = now();
-                    if(nthreads <= 1)
-                        copyView(src, dst);
-                    else
-                    {
-                        const Mapping& a = src.mapping();
-                        const Mapping& b = dst.mapping();
-                        if(!(a.schema() == b.schema()) || !(a.extents() == b.extents()))
-                            throw std::invalid_argument("incompatible views");
-                        const bool sameLayout = a.name() == b.name() && !a.hasMutableState()
-                            && !b.hasMutableState() && a.isFullyPhysical() && b.isFullyPhysical();
-                        std::vector<std::thread> pool;
-                        if(sameLayout)
-                        {
-                            for(int t = 0; t < nthreads; ++t)
-                                pool.emplace_back(
-                                    [&, t]
-                                    {
-                                        for(std::size_t nr = 0; nr < a.blobCount(); ++nr)
-                                        {
-                                            const std::size_t sz = a.blobSize(nr);
-                                            const std::size_t lo = sz * t / nthreads;
-                                            const std::size_t hi = sz * (t + 1) / nthreads;
-                                            std::memcpy(
-                                                dst.blobs()[nr].data() + lo,
-                                                src.blobs()[nr].data() + lo,
-                                                hi - lo);
-                                        }
-                                    });
-                        }
-                        else
-                        {
-                            const std::uint64_t n = a.elementCount();
-                            const std::size_t leaves = a.schema().leafCount();
-                            const std::uint64_t units = (n + 63) / 64;
-                            for(int t = 0; t < nthreads; ++t)
-                                pool.emplace_back(
-                                    [&, t]
-                                    {
-                                        const std::uint64_t lo = std::min(n, units * t / nthreads * 64);
-                                        const std::uint64_t hi = std::min(n, units * (t + 1) / nthreads * 64);
-                                        for(std::uint64_t i = lo; i < hi; ++i)
-                                            for(std::size_t f = 0; f < leaves; ++f)
-                                                dst.write(i, f, src.read(i, f));
-                                    });
-                        }
-                        for(auto& th : pool)
-                            th.join();
-                    }
+                    copyThreaded(src, dst, nthreads);
                     best = std::min(best, now() - t0);
                 }
                 if(seconds != nullptr)
@@ -318,6 +326,51 @@ extern "C"
                 giveBack(dst, dstBlobs);
                 exportCounters(src.mapping(), srcFac, srcHeat);
                 exportCounters(dst.mapping(), dstFac, dstHeat);
+            });
+    }
+
+    /// Resident reference views (for timing loops and chunked checks without the per-call
+    /// blob adoption copies of ref_copy): a lamina::View owning zeroed Blobs
+    /// (view.hpp:108-111, blob.hpp:18-29), its blob pointers, copyView between two of them.
+    void* ref_view_new(const char* schema, const char* extents, const std::uint64_t* dyn, std::size_t ndyn,
+                       const char* layout, int wrap, std::uint64_t gran)
+    {
+        View* out = nullptr;
+        guarded([&] { out = new View(makeMapping(schema, extents, dyn, ndyn, layout, wrap, gran)); });
+        return out;
+    }
+
+    void ref_view_free(void* h)
+    {
+        delete static_cast<View*>(h);
+    }
+
+    std::size_t ref_view_blob_count(void* h)
+    {
+        return static_cast<View*>(h)->blobs().size();
+    }
+
+    void* ref_view_blob(void* h, std::size_t nr, std::uint64_t* size)
+    {
+        auto& b = static_cast<View*>(h)->blobs()[nr];
+        *size = b.size();
+        return b.data();
+    }
+
+    int ref_view_copy(void* src, void* dst, int nthreads, double* seconds, std::uint64_t* dstFac)
+    {
+        return guarded(
+            [&]
+            {
+                View& s = *static_cast<View*>(src);
+                View& d = *static_cast<View*>(dst);
+                if(auto f = facOf(&d.mapping()))
+                    f->reset();
+                const double t0 = now();
+                copyThreaded(s, d, nthreads);
+                if(seconds != nullptr)
+                    *seconds = now() - t0;
+                exportCounters(d.mapping(), dstFac, nullptr);
             });
     }
 

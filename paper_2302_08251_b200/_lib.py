@@ -48,6 +48,8 @@ _SIGS = {
     "lam_view_blob": (vp, [vp, sz]),
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
+    "lam_view_upload_range": (i32, [vp, sz, u64, u64, vp, vp]),
+    "lam_view_download_range": (i32, [vp, sz, u64, u64, vp, vp]),
     "lam_view_device_plan": (vp, [vp]),
     "lam_copy_sharded": (i32, [C.POINTER(vp), C.POINTER(vp), sz]),
     "lam_nbody_step": (i32, [vp, i32, u64, u64, vp]),

@@ -533,6 +533,48 @@ extern "C"
             });
     }
 
+    // byte sub-range [offset, offset + nbytes) of one blob (View::blobs() spans, view.hpp:133-141)
+    static void checkRange(const lam_view* v, size_t nr, uint64_t offset, uint64_t nbytes)
+    {
+        if(nr >= v->blobs.size())
+            throw std::out_of_range("index out of range: blob " + std::to_string(nr));
+        const uint64_t sz = v->L->map->blobSize(nr);
+        if(offset > sz || nbytes > sz - offset)
+            throw std::out_of_range("index out of range: bytes [" + std::to_string(offset) + ", "
+                                    + std::to_string(offset + nbytes) + ") of blob " + std::to_string(nr)
+                                    + " (size " + std::to_string(sz) + ")");
+    }
+
+    int lam_view_upload_range(lam_view* v, size_t nr, uint64_t offset, uint64_t nbytes, const void* host,
+                              void* stream)
+    {
+        return guard(
+            [&]
+            {
+                checkRange(v, nr, offset, nbytes);
+                DeviceGuard g(v->device);
+                if(nbytes)
+                    lam_cuda_check(cudaMemcpyAsync(static_cast<char*>(v->blobs[nr]) + offset, host, nbytes,
+                                                   cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
+                                   "cudaMemcpyAsync(upload_range)");
+            });
+    }
+
+    int lam_view_download_range(const lam_view* v, size_t nr, uint64_t offset, uint64_t nbytes, void* host,
+                                void* stream)
+    {
+        return guard(
+            [&]
+            {
+                checkRange(v, nr, offset, nbytes);
+                DeviceGuard g(v->device);
+                if(nbytes)
+                    lam_cuda_check(cudaMemcpyAsync(host, static_cast<const char*>(v->blobs[nr]) + offset, nbytes,
+                                                   cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)),
+                                   "cudaMemcpyAsync(download_range)");
+            });
+    }
+
     // ---- view dump / restore (core/src/view_io.cpp:28-129) -------------------------------------
     // Same files as lamina::writeViewDump / readViewDump: <stem>.meta (key=value sidecar) and
     // <stem>.blob<nr>.bin (raw blob bytes), same error messages (std::runtime_error ->

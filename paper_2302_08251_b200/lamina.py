@@ -287,6 +287,21 @@ class View:
             self.sync()
         return out
 
+    def upload_range(self, nr: int, offset: int, host: np.ndarray, stream=None) -> None:
+        host = np.ascontiguousarray(host)
+        _check(lib().lam_view_upload_range(self._h, nr, offset, host.nbytes, host.ctypes.data_as(C.c_void_p),
+                                           _stream_handle(stream)))
+        if stream is None:
+            self.sync()
+
+    def download_range(self, nr: int, offset: int, nbytes: int, stream=None) -> np.ndarray:
+        out = np.empty(nbytes, dtype=np.uint8)
+        _check(lib().lam_view_download_range(self._h, nr, offset, nbytes, out.ctypes.data_as(C.c_void_p),
+                                             _stream_handle(stream)))
+        if stream is None:
+            self.sync()
+        return out
+
     def upload_all(self, blobs: Sequence[np.ndarray]) -> None:
         for nr, b in enumerate(blobs):
             if self.layout.blob_size(nr):
