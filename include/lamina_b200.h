@@ -124,9 +124,9 @@ int lam_layout_stream_region(const lam_layout* layout, size_t stream, uint64_t b
  * device memory and start at zero. */
 int lam_view_alloc(const lam_layout* layout, int device, void* stream, lam_view** out);
 /* Replaces lamina::View(MappingPtr, std::vector<Blob>) (core/src/view.cpp:105-118): adopts
- * caller-owned device blobs (not freed by lam_view_free).  `blob_bytes` (optional) is
- * checked like the reference ("blob count mismatch" / "blob size mismatch").  Blob
- * pointers must be 16-byte aligned. */
+ * caller-owned device blobs (not freed by lam_view_free).  `blob_bytes` (required: a Blob
+ * always knows its size) is checked like the reference ("blob count mismatch" / "blob size
+ * mismatch"); NULL fails with "blob size mismatch".  Blob pointers must be 16-byte aligned. */
 int lam_view_wrap(const lam_layout* layout, int device, void* const* device_blobs, const uint64_t* blob_bytes,
                   size_t n_blobs, lam_view** out);
 void lam_view_free(lam_view* view);

@@ -133,10 +133,17 @@ namespace lamina_b200
             check(lam_view_alloc(m_->handle(), device, stream, &v));
             v_.reset(v, lam_view_free);
         }
-        View(MappingPtr m, const std::vector<void*>& deviceBlobs, int device = 0) : m_(std::move(m))
+        /// View(MappingPtr, std::vector<Blob>) (view.cpp:105-118): adopts device blobs of the
+        /// given sizes ("blob count mismatch" / "blob size mismatch" as the reference).
+        View(MappingPtr m, const std::vector<void*>& deviceBlobs, const std::vector<uint64_t>& blobBytes,
+             int device = 0)
+            : m_(std::move(m))
         {
+            if(blobBytes.size() != deviceBlobs.size())
+                throw std::invalid_argument("blob count mismatch: " + std::to_string(deviceBlobs.size())
+                                            + " blobs, " + std::to_string(blobBytes.size()) + " sizes");
             lam_view* v = nullptr;
-            check(lam_view_wrap(m_->handle(), device, deviceBlobs.data(), nullptr, deviceBlobs.size(), &v));
+            check(lam_view_wrap(m_->handle(), device, deviceBlobs.data(), blobBytes.data(), deviceBlobs.size(), &v));
             v_.reset(v, lam_view_free);
         }
         const Mapping& mapping() const

@@ -450,9 +450,11 @@ extern "C"
                     throw std::invalid_argument(
                         "blob count mismatch: mapping declares " + std::to_string(m.blobCount()) + ", got "
                         + std::to_string(n));
+                if(bytes == nullptr && n > 0)
+                    throw std::invalid_argument("blob size mismatch: the sizes of the adopted blobs are required");
                 for(size_t nr = 0; nr < n; ++nr)
                 {
-                    if(bytes && bytes[nr] != m.blobSize(nr))
+                    if(bytes[nr] != m.blobSize(nr))
                         throw std::invalid_argument(
                             "blob size mismatch: blob " + std::to_string(nr) + " declares "
                             + std::to_string(m.blobSize(nr)) + ", got " + std::to_string(bytes[nr]));
@@ -612,6 +614,9 @@ extern "C"
                         throw std::runtime_error("cannot write " + metaPath);
                 }
                 DeviceGuard g(v->device);
+                // no stream argument (writeViewDump's signature): wait for every stream of the
+                // device, non-blocking ones included, before reading the blobs back
+                lam_cuda_check(cudaDeviceSynchronize(), "sync");
                 const Map& m = *v->L->map;
                 std::vector<char> host;
                 for(size_t nr = 0; nr < m.blobCount(); ++nr)

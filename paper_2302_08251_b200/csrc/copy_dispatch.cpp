@@ -117,13 +117,18 @@ namespace lamhost
         return !leafContig32(phys);
     }
 
-    // scratch SoA views, cached per (device, stream, schema+extents): allocation and plan lowering happen
-    // once, not per copy (a 2^26-record scratch is 1.9 GB; at most 4 are kept)
+    // Scratch SoA views for staged copies, cached per (device, schema+extents): allocation and
+    // plan lowering happen once, not per copy (a 2^26-record scratch is 1.9 GB; at most 4 are
+    // kept).  Users hold a shared_ptr, so an evicted scratch lives until its last user is done;
+    // `use` serialises the enqueueing of the two staged copies, and `done` (recorded after
+    // them) orders the next use on any stream after the previous one on the device.
     struct ScratchSoA
     {
         std::shared_ptr<Lowered> L;
         lam_view v;
         std::string key;
+        std::mutex use;
+        cudaEvent_t done = nullptr;
         ScratchSoA(const lam_view& like, std::string k) : key(std::move(k))
         {
             const Map& m = *like.L->map;
@@ -132,6 +137,7 @@ namespace lamhost
             v.device = like.device;
             v.owned = false;
             DeviceGuard g(like.device);
+            lam_cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "scratch event");
             for(size_t nr = 0; nr < L->map->blobCount(); ++nr)
             {
                 void* p = nullptr;
@@ -143,29 +149,31 @@ namespace lamhost
         ~ScratchSoA()
         {
             DeviceGuard g(v.device);
-            cudaDeviceSynchronize();
+            if(done)
+            {
+                cudaEventSynchronize(done); // the last staged copy through this scratch
+                cudaEventDestroy(done);
+            }
             v.img.release();
             for(void* p : v.blobs)
                 cudaFree(p);
         }
     };
 
-    static lam_view& scratchFor(const lam_view& like, cudaStream_t s)
+    static std::shared_ptr<ScratchSoA> scratchFor(const lam_view& like)
     {
         static std::mutex mu;
-        static std::vector<std::unique_ptr<ScratchSoA>> cache;
+        static std::vector<std::shared_ptr<ScratchSoA>> cache;
         const Map& m = *like.L->map;
-        // one scratch per stream: copies on different streams may run concurrently
-        const std::string key = std::to_string(like.device) + "|" + std::to_string(reinterpret_cast<uintptr_t>(s)) + "|"
-            + m.schema().toString() + "|" + m.extents().toString();
+        const std::string key = std::to_string(like.device) + "|" + m.schema().toString() + "|" + m.extents().toString();
         std::lock_guard<std::mutex> lk(mu);
         for(auto& c : cache)
             if(c->key == key)
-                return c->v;
+                return c;
         if(cache.size() >= 4)
             cache.erase(cache.begin());
-        cache.push_back(std::make_unique<ScratchSoA>(like, key));
-        return cache.back()->v;
+        cache.push_back(std::make_shared<ScratchSoA>(like, key));
+        return cache.back();
     }
 
     void copyViews(const lam_view& src, lam_view& dst, uint64_t begin, uint64_t end, cudaStream_t s)
@@ -204,9 +212,12 @@ namespace lamhost
         const char* fg = std::getenv("LAMB_FORCE_GENERIC");
         if(full && !(fg && fg[0] == '1') && stagingHelps(*src.L, *dst.L))
         {
-            lam_view& tmp = scratchFor(src, s);
-            copyViews(src, tmp, begin, end, s);
-            copyViews(tmp, dst, begin, end, s);
+            const std::shared_ptr<ScratchSoA> sc = scratchFor(src);
+            std::lock_guard<std::mutex> lk(sc->use);
+            lam_cuda_check(cudaStreamWaitEvent(s, sc->done, 0), "scratch wait");
+            copyViews(src, sc->v, begin, end, s); // never staged again: the scratch side is plain SoA
+            copyViews(sc->v, dst, begin, end, s);
+            lam_cuda_check(cudaEventRecord(sc->done, s), "scratch record");
             return;
         }
         if(!(fg && fg[0] == '1') && tileCopy(src, dst, begin, end, s))

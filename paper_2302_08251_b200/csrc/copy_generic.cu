@@ -11,6 +11,9 @@
 #include <cstdlib>
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace lamk
 {
@@ -22,6 +25,26 @@ namespace lamk
     uint64_t launch_count()
     {
         return g_launches.load(std::memory_order_relaxed);
+    }
+
+    cudaError_t opt_in_smem(const void* func, size_t smem)
+    {
+        if(smem <= 48 * 1024)
+            return cudaSuccess;
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if(e != cudaSuccess)
+            return e;
+        static std::mutex mu;
+        static std::map<std::pair<const void*, int>, size_t> done; // (kernel, device) -> bytes set
+        std::lock_guard<std::mutex> g(mu);
+        size_t& have = done[{func, dev}];
+        if(have >= smem)
+            return cudaSuccess;
+        e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if(e == cudaSuccess)
+            have = smem;
+        return e;
     }
 
     int sm_count(int device)
@@ -349,12 +372,8 @@ namespace lamk
             return cudaSuccess;
         const uint64_t ctas = (p.end - p.begin + p.E - 1) / p.E; // E is sized on the host
         const size_t smem = static_cast<size_t>(p.maxWindow) * sizeof(unsigned long long);
-        static size_t attr = 0;
-        if(attr < smem)
-        {
-            cudaFuncSetAttribute(k_heat_phys, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            attr = smem;
-        }
+        if(cudaError_t e = opt_in_smem(reinterpret_cast<const void*>(k_heat_phys), smem); e != cudaSuccess)
+            return e;
         k_heat_phys<<<static_cast<unsigned>(ctas), 256, smem, s>>>(p);
         count_launch();
         return cudaGetLastError();

@@ -1044,12 +1044,8 @@ namespace lamk
     {
         const uint32_t warps = 8;
         const size_t smem = static_cast<size_t>(warps) * (p.src_bytes + p.dst_bytes);
-        static size_t attr = 0;
-        if(attr < smem)
-        {
-            cudaFuncSetAttribute(k_warp_tile<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            attr = smem;
-        }
+        if(cudaError_t e = opt_in_smem(reinterpret_cast<const void*>(k_warp_tile<8>), smem); e != cudaSuccess)
+            return e;
         const unsigned grid = stream_grid((uint64_t(ntiles) + warps - 1) / warps, "LAMB_WT_CTAS", 8);
         k_warp_tile<8><<<grid, warps * 32, smem, s>>>(p, ntiles);
         count_launch();
@@ -1063,16 +1059,9 @@ namespace lamk
         const uint32_t perWarp = p.src_bytes + p.dst_bytes;
         const uint32_t warps = 8;
         const size_t smem = static_cast<size_t>(warps) * perWarp;
-        static size_t attr[64] = {0};
         auto kern = p.usize == 4 ? k_uniform_warp<uint32_t, 4> : k_uniform_warp<unsigned long long, 4>;
-        if(dev < 64 && attr[dev] < smem)
-        {
-            cudaFuncSetAttribute(k_uniform_warp<uint32_t, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            cudaFuncSetAttribute(k_uniform_warp<unsigned long long, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            attr[dev] = smem;
-        }
+        if(cudaError_t e = opt_in_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess)
+            return e;
         int occ = 0;
         if(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem) != cudaSuccess || occ < 1)
             occ = 1;
@@ -1102,18 +1091,10 @@ namespace lamk
     {
         if(p.ntiles == 0)
             return cudaSuccess;
-        static uint32_t attrSet[64] = {0};
         int dev = 0;
         cudaGetDevice(&dev);
-        if(dev >= 64 || attrSet[dev] < smemBytes)
-        {
-            cudaError_t e = cudaFuncSetAttribute(k_tile_copy, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smemBytes));
-            if(e != cudaSuccess)
-                return e;
-            if(dev < 64)
-                attrSet[dev] = smemBytes;
-        }
+        if(cudaError_t e = opt_in_smem(reinterpret_cast<const void*>(k_tile_copy), smemBytes); e != cudaSuccess)
+            return e;
         const uint32_t sms = static_cast<uint32_t>(sm_count(dev));
         // persistent grid: exactly the CTAs that are co-resident (a second wave would serialise)
         int occ = 0;

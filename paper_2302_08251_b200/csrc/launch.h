@@ -18,6 +18,10 @@ namespace lamk
 
     int sm_count(int device);
 
+    // Opt `func` in to `smem` bytes of dynamic shared memory on the CURRENT device.  The
+    // attribute is per device, so it is tracked per (kernel, device); no-op up to 48 KB.
+    cudaError_t opt_in_smem(const void* func, size_t smem);
+
     // Grid for a grid-stride streaming kernel: `want` CTAs (one pass of the data), capped at
     // `perSm` x SMs, with the cap overridable by the environment variable `env`; a cap of 0
     // means uncapped.  Uncapped one-pass grids measured best for streaming copies on B200: the

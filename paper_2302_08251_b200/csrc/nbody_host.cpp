@@ -268,9 +268,13 @@ extern "C"
             {
                 const bool f64 = particleF64(v);
                 DeviceGuard g(v->device);
+                // checksumView takes no stream: order after all work on the device (non-blocking
+                // streams included), then copy on the legacy stream and read back
+                lam_cuda_check(cudaDeviceSynchronize(), "sync");
                 const uint64_t n = v->L->map->elementCount();
                 TempView tmp(*v, v->device);
                 copyViews(*v, tmp.v, 0, n, nullptr);
+                lam_cuda_check(cudaDeviceSynchronize(), "sync");
                 const size_t T = f64 ? 8 : 4;
                 std::vector<uint8_t> host(n * 7 * T);
                 if(!host.empty())

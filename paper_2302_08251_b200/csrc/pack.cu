@@ -715,24 +715,14 @@ namespace lamk
     template<int W, int FMT>
     static void launch_rec(const RecPackParams& q, bool pack, unsigned grid, size_t smem, cudaStream_t s)
     {
-        static size_t setPack = 0, setUnpack = 0;
         if(pack)
         {
-            if(setPack < smem)
-            {
-                cudaFuncSetAttribute(k_rec_pack<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-                setPack = smem;
-            }
+            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_rec_pack<W, FMT>), smem), "opt_in_smem");
             k_rec_pack<W, FMT><<<grid, 256, smem, s>>>(q);
         }
         else
         {
-            if(setUnpack < smem)
-            {
-                cudaFuncSetAttribute(k_rec_unpack<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-                setUnpack = smem;
-            }
+            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_rec_unpack<W, FMT>), smem), "opt_in_smem");
             k_rec_unpack<W, FMT><<<grid, 256, smem, s>>>(q);
         }
     }
@@ -784,26 +774,15 @@ namespace lamk
     template<int W, int FMT>
     static void launch_pack(const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s)
     {
-        // opt in to > 48 KB of dynamic shared memory once per instantiation and size
-        static size_t setPack = 0, setUnpack = 0;
+        // opt in to > 48 KB of dynamic shared memory once per instantiation, size and device
         if(pack)
         {
-            if(setPack < smem)
-            {
-                cudaFuncSetAttribute(k_pack32<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-                setPack = smem;
-            }
+            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_pack32<W, FMT>), smem), "opt_in_smem");
             k_pack32<W, FMT><<<resident_grid(k_pack32<W, FMT>, grid, smem, p.facS || p.facD), 256, smem, s>>>(p);
         }
         else
         {
-            if(setUnpack < smem)
-            {
-                cudaFuncSetAttribute(k_unpack32<W, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-                setUnpack = smem;
-            }
+            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_unpack32<W, FMT>), smem), "opt_in_smem");
             k_unpack32<W, FMT><<<resident_grid(k_unpack32<W, FMT>, grid, smem, p.facS || p.facD), 256, smem, s>>>(p);
         }
     }

@@ -140,13 +140,8 @@ namespace lamk
         else
         {
             const size_t smem = 8 * 32 * NV * sizeof(uint4);
-            static bool attr = false;
-            if(!attr)
-            {
-                cudaFuncSetAttribute(k_planes_to_rec<NL, SB, CVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-                attr = true;
-            }
+            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_planes_to_rec<NL, SB, CVT>), smem),
+                           "opt_in_smem");
             k_planes_to_rec<NL, SB, CVT><<<stream_grid((p.groups + 255) / 256, "LAMB_PLANES_CTAS", 0), 256, smem, s>>>(p);
         }
     }

@@ -368,12 +368,7 @@ namespace lamk
     static void launch_convert(const VecParams& p, cudaStream_t s)
     {
         const size_t smem = p.d.recordContig ? 8 * 32 * (NL * DS / 4) * 16 : 0;
-        static bool attr = false;
-        if(!attr)
-        {
-            cudaFuncSetAttribute(k_vec_convert<NL, SS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-            attr = true;
-        }
+        lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_vec_convert<NL, SS, DS>), smem), "opt_in_smem");
         k_vec_convert<NL, SS, DS><<<stream_grid((p.groups + 255) / 256, "LAMB_VEC_CTAS", 0), 256, smem, s>>>(p);
     }
 

@@ -71,7 +71,7 @@ def nbody_distributed(layout_text: str, n: int, steps: int, mode: int = 0, seed:
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     dev = torch.cuda.current_device()
     blobs = [torch.zeros(max(16, s), dtype=torch.uint8, device="cuda") for s in lay.blob_sizes]
-    view = L.View(lay, device=dev, blobs=[b.data_ptr() for b in blobs], blob_bytes=None)
+    view = L.View(lay, device=dev, blobs=[b.data_ptr() for b in blobs], blob_bytes=lay.blob_sizes)
     view.nbody_init(seed)
     lo, hi = shard_range(n, lay.shard_unit, rank, world)
     stream = torch.cuda.current_stream()

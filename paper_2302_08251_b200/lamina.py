@@ -238,10 +238,10 @@ class View:
             _check(L.lam_view_alloc(layout.handle, device, _stream_handle(stream), C.byref(h)))
         else:
             n = len(blobs)
+            if blob_bytes is None or len(blob_bytes) != n:
+                raise InvalidArgument("blob size mismatch: pass blob_bytes (one size per adopted blob)")
             ptrs = (C.c_void_p * max(1, n))(*[C.c_void_p(int(p)) for p in blobs])
-            sizes = None
-            if blob_bytes is not None:
-                sizes = (C.c_uint64 * max(1, n))(*blob_bytes)
+            sizes = (C.c_uint64 * max(1, n))(*blob_bytes)
             _check(L.lam_view_wrap(layout.handle, device, ptrs, sizes, n, C.byref(h)))
         self._h = h
 

@@ -34,11 +34,11 @@ def test_all_f32_patterns_fast_equals_generic(fmt):
     back_f = torch.empty(CHUNK, dtype=torch.int32, device="cuda")
     back_g = torch.empty(CHUNK, dtype=torch.int32, device="cuda")
     v32 = torch.empty(CHUNK, dtype=torch.int32, device="cuda")
-    vs = L.View(ls, blobs=[v32.data_ptr()])
-    vf = L.View(ld, blobs=[fast.data_ptr()])
-    vg = L.View(ld, blobs=[gen.data_ptr()])
-    bf = L.View(ls, blobs=[back_f.data_ptr()])
-    bg = L.View(ls, blobs=[back_g.data_ptr()])
+    vs = L.View(ls, blobs=[v32.data_ptr()], blob_bytes=[v32.numel() * 4])
+    vf = L.View(ld, blobs=[fast.data_ptr()], blob_bytes=[fast.numel() * 4])
+    vg = L.View(ld, blobs=[gen.data_ptr()], blob_bytes=[gen.numel() * 4])
+    bf = L.View(ls, blobs=[back_f.data_ptr()], blob_bytes=[back_f.numel() * 4])
+    bg = L.View(ls, blobs=[back_g.data_ptr()], blob_bytes=[back_g.numel() * 4])
     for c in range((1 << 32) // CHUNK):
         torch.arange(c * CHUNK, (c + 1) * CHUNK, dtype=torch.int64, device="cuda", out=vals)
         v32.copy_((vals - (vals >= 2**31).to(torch.int64) * 2**32).to(torch.int32))
