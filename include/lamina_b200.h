@@ -96,6 +96,10 @@ size_t lam_layout_leaf_path(const lam_layout* layout, size_t flat_leaf, char* bu
 int lam_layout_is_computed(const lam_layout* layout, size_t flat_leaf);
 int lam_layout_is_fully_physical(const lam_layout* layout);
 int lam_layout_has_mutable_state(const lam_layout* layout);
+/* ArrayExtents::isFullyStatic (extents.hpp:127-130) and Mapping::runtimeStateBytes
+ * (mapping.hpp:145-148; wrappers add inner mappings and counters, instrument.cpp:79-82,197-200). */
+int lam_layout_is_fully_static(const lam_layout* layout);
+uint64_t lam_layout_runtime_state_bytes(const lam_layout* layout);
 /* Mapping::physicalOffset (mapping.hpp:109); LAM_ELOGIC for computed leaves. */
 int lam_layout_physical_offset(const lam_layout* layout, uint64_t linear, size_t flat_leaf, size_t* nr,
                                uint64_t* offset);
@@ -130,6 +134,12 @@ int lam_view_alloc(const lam_layout* layout, int device, void* stream, lam_view*
 int lam_view_wrap(const lam_layout* layout, int device, void* const* device_blobs, const uint64_t* blob_bytes,
                   size_t n_blobs, lam_view** out);
 void lam_view_free(lam_view* view);
+/* View::isTriviallyRelocatable / blobBytes / stateBytes (core/src/view.cpp:145-162):
+ * relocatable = fully static extents, no mutable state, no runtime state; state = blob bytes
+ * + runtime state bytes (acceptance criterion 10, acceptance.cpp:772-790). */
+int lam_view_is_trivially_relocatable(const lam_view* view);
+uint64_t lam_view_blob_bytes(const lam_view* view);
+uint64_t lam_view_state_bytes(const lam_view* view);
 const lam_layout* lam_view_layout(const lam_view* view);
 void* lam_view_blob(const lam_view* view, size_t nr);
 /* Device pointer to the view's lowered plan (struct lamp_view): the argument user kernels pass
@@ -210,6 +220,18 @@ int lam_nbody_move(lam_view* view, uint64_t i_begin, uint64_t i_end, void* strea
 /* One runner step (runner.cpp:387-421): lam_nbody_update then lam_nbody_move over [i_begin, i_end). */
 int lam_nbody_step(lam_view* view, int mode, uint64_t i_begin, uint64_t i_end, void* stream);
 int lam_nbody_checksum(const lam_view* view, double* out);
+
+/* The reference's hand-written baselines (tools/nbody/steps.hpp:124-230, runner.cpp:239-323:
+ * layouts "manual-aos" = ManualParticle[], "manual-soa" = ManualSoA) as plain device kernels
+ * without mappings: state drawn by drawInitValues(seed), update (mode EXACT | FAST), move,
+ * checksum as runManual.  They measure the library-vs-hand-written ratio (paper Fig. 3). */
+typedef struct lam_nbody_manual lam_nbody_manual;
+int lam_nbody_manual_create(const char* kind, uint64_t n, int f64, uint64_t seed, int device, void* stream,
+                            lam_nbody_manual** out);
+int lam_nbody_manual_update(lam_nbody_manual* m, int mode, void* stream);
+int lam_nbody_manual_move(lam_nbody_manual* m, void* stream);
+int lam_nbody_manual_checksum(const lam_nbody_manual* m, double* out);
+void lam_nbody_manual_free(lam_nbody_manual* m);
 /* The fused multi-GPU update step: elements [i_begin, i_end) of `view` against j-sources read
  * directly from other views -- view k supplies particles [j_begin[k], j_end[k]) (global indices,
  * visited in the given order, so exact mode matches the single-view update when the ranges tile

@@ -158,6 +158,19 @@ namespace lamina_b200
         {
             return v_.get();
         }
+        /// View::isTriviallyRelocatable / blobBytes / stateBytes (view.cpp:145-162)
+        bool isTriviallyRelocatable() const noexcept
+        {
+            return lam_view_is_trivially_relocatable(v_.get()) != 0;
+        }
+        std::size_t blobBytes() const noexcept
+        {
+            return static_cast<std::size_t>(lam_view_blob_bytes(v_.get()));
+        }
+        std::size_t stateBytes() const noexcept
+        {
+            return static_cast<std::size_t>(lam_view_state_bytes(v_.get()));
+        }
 
         /// FieldAccessCount::counters() of an instrumented view: (reads, writes) per leaf
         std::pair<std::vector<std::uint64_t>, std::vector<std::uint64_t>> counters(std::size_t leaves) const

@@ -69,6 +69,7 @@ def lib():
         L.ref_view_blob.restype = vp
         L.ref_view_blob.argtypes = [vp, sz, P(u64)]
         L.ref_view_copy.argtypes = [vp, vp, i32, P(dbl), P(u64)]
+        L.ref_state_info.argtypes = [cp, cp, P(u64), sz, cp, i32, u64, P(i32), P(u64), P(i32), P(u64), P(u64)]
         L.ref_contiguous_run.argtypes = [cp, cp, P(u64), C.c_size_t, cp, i32, u64, u64, C.c_size_t, u64, P(C.c_int),
                                          P(C.c_size_t), P(u64)]
         _lib = L
@@ -208,6 +209,15 @@ def nbody_trace(layout, n, steps, report_dir, trace=True, heat_gran=0, f64=False
                                str(report_dir).encode(), csv_path.encode() if csv_path else None)
     if rc != 0:
         raise RefError(5, f"ref_nbody_trace exit code {rc}")
+
+
+def state_info(schema, extents, layout, dyn=(), wrap=0, gran=1):
+    """(isFullyStatic, runtimeStateBytes, isTriviallyRelocatable, stateBytes, blobBytes)."""
+    d, nd = _dyn(dyn)
+    fs, rs, tr, sb, bb = C.c_int(), C.c_uint64(), C.c_int(), C.c_uint64(), C.c_uint64()
+    _check(lib().ref_state_info(schema.encode(), extents.encode(), d, nd, layout.encode(), wrap, gran, C.byref(fs),
+                                C.byref(rs), C.byref(tr), C.byref(sb), C.byref(bb)))
+    return bool(fs.value), rs.value, bool(tr.value), sb.value, bb.value
 
 
 def contiguous_run(schema, extents, layout, linear, leaf, n, dyn=(), wrap=0, gran=1):

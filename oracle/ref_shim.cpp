@@ -374,6 +374,24 @@ extern "C"
             });
     }
 
+    /// View::isTriviallyRelocatable / stateBytes / blobBytes (view.cpp:145-162) of a fresh view,
+    /// ArrayExtents::isFullyStatic and Mapping::runtimeStateBytes of its mapping.
+    int ref_state_info(const char* schema, const char* extents, const std::uint64_t* dyn, std::size_t ndyn,
+                       const char* layout, int wrap, std::uint64_t gran, int* fullyStatic, std::uint64_t* runtimeState,
+                       int* relocatable, std::uint64_t* stateBytes, std::uint64_t* blobBytes)
+    {
+        return guarded(
+            [&]
+            {
+                View v(makeMapping(schema, extents, dyn, ndyn, layout, wrap, gran));
+                *fullyStatic = v.mapping().extents().isFullyStatic() ? 1 : 0;
+                *runtimeState = v.mapping().runtimeStateBytes();
+                *relocatable = v.isTriviallyRelocatable() ? 1 : 0;
+                *stateBytes = v.stateBytes();
+                *blobBytes = v.blobBytes();
+            });
+    }
+
     /// Writes logical values (storage bits of the leaf's own type, one u64 per
     /// (i, f), i-major) through View::write into a zero-initialised view.
     int ref_write_values(

@@ -48,6 +48,11 @@ _SIGS = {
     "lam_view_blob": (vp, [vp, sz]),
     "lam_view_upload": (i32, [vp, sz, vp, vp]),
     "lam_view_download": (i32, [vp, sz, vp, vp]),
+    "lam_layout_is_fully_static": (i32, [vp]),
+    "lam_layout_runtime_state_bytes": (u64, [vp]),
+    "lam_view_is_trivially_relocatable": (i32, [vp]),
+    "lam_view_blob_bytes": (u64, [vp]),
+    "lam_view_state_bytes": (u64, [vp]),
     "lam_view_upload_range": (i32, [vp, sz, u64, u64, vp, vp]),
     "lam_view_download_range": (i32, [vp, sz, u64, u64, vp, vp]),
     "lam_view_device_plan": (vp, [vp]),
@@ -73,6 +78,11 @@ _SIGS = {
     "lam_nbody_update": (i32, [vp, i32, u64, u64, vp]),
     "lam_nbody_move": (i32, [vp, u64, u64, vp]),
     "lam_nbody_checksum": (i32, [vp, C.POINTER(C.c_double)]),
+    "lam_nbody_manual_create": (i32, [cp, u64, i32, u64, i32, vp, C.POINTER(vp)]),
+    "lam_nbody_manual_update": (i32, [vp, i32, vp]),
+    "lam_nbody_manual_move": (i32, [vp, vp]),
+    "lam_nbody_manual_checksum": (i32, [vp, C.POINTER(C.c_double)]),
+    "lam_nbody_manual_free": (None, [vp]),
     "lam_launch_count": (u64, []),
     "lam_bench_fma_peak": (i32, [i32, C.c_double, C.POINTER(C.c_double)]),
     "lam_device_sync": (i32, [i32]),

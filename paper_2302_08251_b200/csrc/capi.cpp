@@ -307,6 +307,36 @@ extern "C"
         return l->L->map->hasMutableState() ? 1 : 0;
     }
 
+    int lam_layout_is_fully_static(const lam_layout* l)
+    {
+        return l->L->map->extents().isFullyStatic() ? 1 : 0;
+    }
+
+    uint64_t lam_layout_runtime_state_bytes(const lam_layout* l)
+    {
+        return l->L->map->runtimeStateBytes();
+    }
+
+    // View::isTriviallyRelocatable / blobBytes / stateBytes (view.cpp:145-162)
+    int lam_view_is_trivially_relocatable(const lam_view* v)
+    {
+        const Map& m = *v->L->map;
+        return m.extents().isFullyStatic() && !m.hasMutableState() && m.runtimeStateBytes() == 0 ? 1 : 0;
+    }
+
+    uint64_t lam_view_blob_bytes(const lam_view* v)
+    {
+        uint64_t total = 0;
+        for(size_t nr = 0; nr < v->L->map->blobCount(); ++nr)
+            total += v->L->map->blobSize(nr);
+        return total;
+    }
+
+    uint64_t lam_view_state_bytes(const lam_view* v)
+    {
+        return lam_view_blob_bytes(v) + v->L->map->runtimeStateBytes();
+    }
+
     int lam_layout_physical_offset(const lam_layout* l, uint64_t i, size_t f, size_t* nr, uint64_t* off)
     {
         return guard(

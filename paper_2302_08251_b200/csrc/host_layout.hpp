@@ -224,6 +224,13 @@ namespace lamb
         {
             return false;
         }
+        // Mapping::runtimeStateBytes (mapping.hpp:145-148): dynamic extents' slots, plus inner
+        // mappings' and counters' bytes in the wrappers (computed.cpp:396-399,499-502,
+        // mappings.cpp:386-389, instrument.cpp:79-82,197-200)
+        virtual size_t runtimeStateBytes() const
+        {
+            return extents_.runtimeStateBytes();
+        }
         // physicalOffset without bounds checks; throws logic_error for computed leaves
         virtual std::pair<size_t, uint64_t> offsetOf(uint64_t i, size_t f) const;
         // lower leaf f into plan nodes; blob numbers shifted by `blobShift`
@@ -355,6 +362,10 @@ namespace lamb
         {
             return a_->hasMutableState() || b_->hasMutableState();
         }
+        size_t runtimeStateBytes() const override
+        {
+            return extents_.runtimeStateBytes() + a_->runtimeStateBytes() + b_->runtimeStateBytes();
+        }
         std::pair<size_t, uint64_t> offsetOf(uint64_t i, size_t f) const override;
         uint16_t lower(size_t f, uint32_t blobShift, PlanBuilder& pb) const override;
         int depth() const override
@@ -462,6 +473,10 @@ namespace lamb
         {
             return inner_->hasMutableState();
         }
+        size_t runtimeStateBytes() const override
+        {
+            return extents_.runtimeStateBytes() + inner_->runtimeStateBytes();
+        }
         std::pair<size_t, uint64_t> offsetOf(uint64_t i, size_t f) const override;
         uint16_t lower(size_t f, uint32_t blobShift, PlanBuilder& pb) const override;
         const Map* inner() const override
@@ -503,6 +518,10 @@ namespace lamb
         {
             return inner_->hasMutableState();
         }
+        size_t runtimeStateBytes() const override
+        {
+            return extents_.runtimeStateBytes() + inner_->runtimeStateBytes();
+        }
         uint16_t lower(size_t f, uint32_t blobShift, PlanBuilder& pb) const override;
         const Map* inner() const override
         {
@@ -525,6 +544,10 @@ namespace lamb
         std::string name() const override
         {
             return "field-access-count(" + inner_->name() + ")";
+        }
+        size_t runtimeStateBytes() const override
+        {
+            return extents_.runtimeStateBytes() + inner_->runtimeStateBytes() + 2 * schema_.leafCount() * 8;
         }
         size_t blobCount() const override
         {
@@ -570,6 +593,13 @@ namespace lamb
         std::string name() const override
         {
             return "heatmap:" + std::to_string(gran_) + "(" + inner_->name() + ")";
+        }
+        size_t runtimeStateBytes() const override
+        {
+            size_t blocks = 0;
+            for(size_t nr = 0; nr < blobCount(); ++nr)
+                blocks += blockCount(nr);
+            return extents_.runtimeStateBytes() + inner_->runtimeStateBytes() + blocks * 8;
         }
         size_t blobCount() const override
         {

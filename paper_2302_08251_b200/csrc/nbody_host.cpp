@@ -2,6 +2,8 @@
 #include "capi_internal.hpp"
 
 #include <cstring>
+#include <memory>
+#include <string>
 #include <random>
 #include <vector>
 
@@ -14,7 +16,18 @@ namespace lamk
     cudaError_t nbody_update_multi(const lamp_view* v, bool f64, bool exact, bool phys, const lamp_view* const* jv,
                                    const uint64_t* jb, const uint64_t* je, size_t nj, uint64_t ib, uint64_t ie,
                                    cudaStream_t s);
+    cudaError_t nbody_manual_update(bool soa, bool f64, bool exact, void* base, uint64_t n, cudaStream_t s);
+    cudaError_t nbody_manual_move(bool soa, bool f64, void* base, uint64_t n, cudaStream_t s);
 } // namespace lamk
+
+// the hand-written baselines' state: one device buffer, AoS records or 7 arrays
+struct lam_nbody_manual
+{
+    bool soa = false, f64 = false;
+    uint64_t n = 0;
+    int device = 0;
+    void* buf = nullptr;
+};
 
 using namespace lamb;
 using namespace lamhost;
@@ -147,6 +160,124 @@ extern "C"
                 copyViews(tmp.v, *v, 0, n, s);
                 lam_cuda_check(cudaStreamSynchronize(s), "sync");
             });
+    }
+
+    // ---- hand-written baselines (steps.hpp:124-230, runner.cpp:239-323) -------------------
+    int lam_nbody_manual_create(const char* kind, uint64_t n, int f64, uint64_t seed, int device, void* stream,
+                                lam_nbody_manual** out)
+    {
+        return guard2(
+            [&]
+            {
+                const std::string k = kind ? kind : "";
+                if(k != "manual-aos" && k != "manual-soa")
+                    throw std::invalid_argument("unknown manual baseline: '" + k + "' (manual-aos | manual-soa)");
+                auto m = std::make_unique<lam_nbody_manual>();
+                m->soa = k == "manual-soa";
+                m->f64 = f64 != 0;
+                m->n = n;
+                m->device = device;
+                DeviceGuard g(device);
+                const size_t T = m->f64 ? 8 : 4;
+                // drawInitValues (runner.cpp:30-43), laid out as ManualParticle[] or ManualSoA
+                std::mt19937_64 gen(seed);
+                std::vector<uint8_t> host(n * 7 * T);
+                for(uint64_t i = 0; i < n; ++i)
+                {
+                    double d[7];
+                    d[0] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[1] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[2] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[6] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+                    d[3] = d[4] = d[5] = 0.0;
+                    for(int f = 0; f < 7; ++f)
+                    {
+                        const uint64_t at = m->soa ? (f * n + i) * T : (i * 7 + f) * T;
+                        if(m->f64)
+                            std::memcpy(&host[at], &d[f], 8);
+                        else
+                        {
+                            const float x = static_cast<float>(d[f]);
+                            std::memcpy(&host[at], &x, 4);
+                        }
+                    }
+                }
+                lam_cuda_check(cudaMalloc(&m->buf, host.empty() ? 16 : host.size()), "cudaMalloc(manual)");
+                auto s = static_cast<cudaStream_t>(stream);
+                if(!host.empty())
+                    lam_cuda_check(cudaMemcpyAsync(m->buf, host.data(), host.size(), cudaMemcpyHostToDevice, s), "h2d");
+                lam_cuda_check(cudaStreamSynchronize(s), "sync");
+                *out = m.release();
+            });
+    }
+
+    int lam_nbody_manual_update(lam_nbody_manual* m, int mode, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                DeviceGuard g(m->device);
+                lam_cuda_check(lamk::nbody_manual_update(m->soa, m->f64, mode == LAM_NBODY_EXACT, m->buf, m->n,
+                                                         static_cast<cudaStream_t>(stream)),
+                               "nbody_manual_update");
+            });
+    }
+
+    int lam_nbody_manual_move(lam_nbody_manual* m, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                DeviceGuard g(m->device);
+                lam_cuda_check(lamk::nbody_manual_move(m->soa, m->f64, m->buf, m->n, static_cast<cudaStream_t>(stream)),
+                               "nbody_manual_move");
+            });
+    }
+
+    // the checksum of runManual (runner.cpp:303-318): Σ (x, y, z) in double, index order
+    int lam_nbody_manual_checksum(const lam_nbody_manual* m, double* out)
+    {
+        return guard2(
+            [&]
+            {
+                DeviceGuard g(m->device);
+                lam_cuda_check(cudaDeviceSynchronize(), "sync");
+                const size_t T = m->f64 ? 8 : 4;
+                std::vector<uint8_t> host(m->n * 7 * T);
+                if(!host.empty())
+                    lam_cuda_check(cudaMemcpy(host.data(), m->buf, host.size(), cudaMemcpyDeviceToHost), "d2h");
+                double sum = 0;
+                for(uint64_t i = 0; i < m->n; ++i)
+                    for(int f = 0; f < 3; ++f)
+                    {
+                        const uint64_t at = m->soa ? (f * m->n + i) * T : (i * 7 + f) * T;
+                        if(m->f64)
+                        {
+                            double x;
+                            std::memcpy(&x, &host[at], 8);
+                            sum += x;
+                        }
+                        else
+                        {
+                            float x;
+                            std::memcpy(&x, &host[at], 4);
+                            sum += static_cast<double>(x);
+                        }
+                    }
+                *out = sum;
+            });
+    }
+
+    void lam_nbody_manual_free(lam_nbody_manual* m)
+    {
+        if(!m)
+            return;
+        if(m->buf)
+        {
+            DeviceGuard g(m->device);
+            cudaFree(m->buf);
+        }
+        delete m;
     }
 
     int lam_nbody_update(lam_view* v, int mode, uint64_t ib, uint64_t ie, void* stream)

@@ -189,6 +189,14 @@ class Layout:
     def has_mutable_state(self) -> bool:
         return bool(lib().lam_layout_has_mutable_state(self._h))
 
+    @property
+    def is_fully_static(self) -> bool:
+        return bool(lib().lam_layout_is_fully_static(self._h))
+
+    @property
+    def runtime_state_bytes(self) -> int:
+        return int(lib().lam_layout_runtime_state_bytes(self._h))
+
     def physical_offset(self, linear: int, f: int) -> tuple[int, int]:
         nr, off = C.c_size_t(), C.c_uint64()
         _check(lib().lam_layout_physical_offset(self._h, linear, f, C.byref(nr), C.byref(off)))
@@ -266,6 +274,15 @@ class View:
     def dump(self, stem: str) -> None:
         """lamina::writeViewDump (view_io.cpp:28-59): <stem>.meta + <stem>.blob<nr>.bin."""
         _check(lib().lam_view_dump(self._h, str(stem).encode()))
+
+    def is_trivially_relocatable(self) -> bool:
+        return bool(lib().lam_view_is_trivially_relocatable(self._h))
+
+    def blob_bytes(self) -> int:
+        return int(lib().lam_view_blob_bytes(self._h))
+
+    def state_bytes(self) -> int:
+        return int(lib().lam_view_state_bytes(self._h))
 
     def blob_ptr(self, nr: int) -> int:
         return lib().lam_view_blob(self._h, nr) or 0
@@ -378,6 +395,37 @@ class View:
         out = C.c_double()
         _check(lib().lam_nbody_checksum(self._h, C.byref(out)))
         return out.value
+
+
+class ManualNbody:
+    """The reference's hand-written n-body baselines (steps.hpp:124-230) on the device:
+    kind "manual-aos" (ManualParticle[]) or "manual-soa" (ManualSoA), no mapping involved."""
+
+    def __init__(self, kind: str, n: int, f64: bool = False, seed: int = 42, device: int = 0, stream=None):
+        h = C.c_void_p()
+        _check(lib().lam_nbody_manual_create(kind.encode(), n, 1 if f64 else 0, seed, device, _stream_handle(stream),
+                                             C.byref(h)))
+        self._h, self.kind, self.n = h, kind, n
+
+    def update(self, mode: int = NBODY_EXACT, stream=None) -> None:
+        _check(lib().lam_nbody_manual_update(self._h, mode, _stream_handle(stream)))
+
+    def move(self, stream=None) -> None:
+        _check(lib().lam_nbody_manual_move(self._h, _stream_handle(stream)))
+
+    def checksum(self) -> float:
+        out = C.c_double()
+        _check(lib().lam_nbody_manual_checksum(self._h, C.byref(out)))
+        return out.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().lam_nbody_manual_free(h)
+            except TypeError:
+                pass
+            self._h = None
 
 
 def write_view_dump(view: View, stem: str) -> None:

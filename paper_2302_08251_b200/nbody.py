@@ -8,9 +8,11 @@ validation messages (runner.cpp:441-466), same CSV rows on stdout
 accumulated per phase over the steps.  The arithmetic runs in the sm_100a n-body kernels
 (exact mode by default: bit-identical to the reference, so the checksum text matches).
 
-`manual-aos` / `manual-soa` (the reference's hand-written baselines, steps.hpp:124-230) map to
-the same kernels over aos-packed / soa-mb: on the device the "hand-written" loop *is* the
-mapping-specialised kernel, so their checksums equal the library layouts' by construction.
+`manual-aos` / `manual-soa` (the reference's hand-written baselines, steps.hpp:124-230,
+runner.cpp:239-323) run separate hand-written device kernels over a plain struct array /
+seven plain arrays (csrc/nbody_manual.cu, no mapping, no accessor), so the
+library-vs-hand-written ratio of paper Fig. 3 is measured; in exact mode their checksum text
+equals the library layouts' (acceptance.cpp:744-766).
 """
 from __future__ import annotations
 
@@ -20,14 +22,14 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .lamina import (NBODY_EXACT, WRAP_FIELD_ACCESS_COUNT, WRAP_HEATMAP, Layout, View, field_access_csv,
-                     heatmap_csv)
+from .lamina import (NBODY_EXACT, WRAP_FIELD_ACCESS_COUNT, WRAP_HEATMAP, Layout, ManualNbody, View,
+                     field_access_csv, heatmap_csv)
 
 SCHEMA = {
     "f32": "Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}",
     "f64": "Record{Pos:Record{x:f64,y:f64,z:f64},Vel:Record{x:f64,y:f64,z:f64},Mass:f64}",
 }
-MANUAL = {"manual-aos": "aos-packed", "manual-soa": "soa-mb"}
+MANUAL = ("manual-aos", "manual-soa")
 
 
 @dataclass
@@ -78,6 +80,26 @@ def _g17(x: float) -> str:
     return f"{x:.17g}"
 
 
+def _run_manual(cfg: BenchConfig) -> int:
+    """runManual (runner.cpp:239-323): warm-up on a copy, then the measured steps, checksum."""
+    try:
+        f64 = cfg.precision == "f64"
+        warm = ManualNbody(cfg.layout, cfg.n, f64, cfg.seed, cfg.device)
+        warm.update(cfg.mode)
+        warm.move()
+        del warm
+        m = ManualNbody(cfg.layout, cfg.n, f64, cfg.seed, cfg.device)
+        upd_t, mov_t = [], []
+        for _ in range(cfg.steps):
+            upd_t.append(_time_ms(lambda: m.update(cfg.mode)) * 1e-3)
+            mov_t.append(_time_ms(lambda: m.move()) * 1e-3)
+        _write_csv(cfg, float(np.median(upd_t)), float(np.median(mov_t)), m.checksum())
+        return 0
+    except Exception as e:  # noqa: BLE001 - runner.cpp:458-462
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+
+
 def run_benchmark(cfg: BenchConfig) -> int:
     """runner.cpp:440-466 + runView/runManual on the device; returns the process exit code."""
     if cfg.n < 1:
@@ -96,7 +118,7 @@ def run_benchmark(cfg: BenchConfig) -> int:
             return _usage("manual baselines support --simd-width 1 only")
         if cfg.trace_fields or cfg.heatmap_granularity != 0:
             return _usage("manual baselines have no mapping to instrument")
-        layout = MANUAL[layout]
+        return _run_manual(cfg)
     wrap = (WRAP_FIELD_ACCESS_COUNT if cfg.trace_fields else 0) | (WRAP_HEATMAP if cfg.heatmap_granularity else 0)
     if cfg.aosoa_nested and (wrap or not layout.startswith("aosoa:")):
         return _usage("--aosoa-nested requires an uninstrumented aosoa:<L> layout")

@@ -196,3 +196,17 @@ def test_contiguous_run_matches_reference(layout, schema, ref):
             for n in (0, 1, 2, 3, 8, 37 - linear):
                 want = ref.contiguous_run(sch, ext, layout, linear, f, n, wrap=wrap, gran=8)
                 assert lay.contiguous_run(linear, f, n) == want, (layout, linear, f, n)
+
+
+@pytest.mark.parametrize("extents,dyn", [("i32:[16]", ()), ("i64:[dyn]", (16,)), ("u16:[4,dyn]", (5,)),
+                                         ("i64:[dyn,dyn]", (3, 7))])
+@pytest.mark.parametrize("layout,wrap", [("aos-packed", 0), ("soa-mb", 0), ("aosoa:4", 0), ("bitpack-float:5,10", 0),
+                                         ("split:Pos:soa-mb:aos-packed", 0), ("changetype:f32=f64:bytesplit:soa-sb", 0),
+                                         ("soa-sb", 1), ("aos-packed", 2), ("aosoa:2", 3)])
+def test_state_accounting_matches_reference(ref, extents, dyn, layout, wrap):
+    """isFullyStatic / runtimeStateBytes of the lowered layout equal the reference's
+    (extents.hpp:127-143, mapping.hpp:145-148, wrappers instrument.cpp:79-82,197-200)."""
+    from paper_2302_08251_b200 import lamina as L
+    fs, rs, _, _, _ = ref.state_info(R32, extents, layout, dyn, wrap, 5)
+    lay = L.Layout(R32, extents, layout, dyn=dyn, wrap=wrap, granularity=5)
+    assert (lay.is_fully_static, lay.runtime_state_bytes) == (fs, rs)

@@ -327,3 +327,19 @@ def test_record_side_bitpack_one_pass(rec, n):
         O.write_all(pm, pb, vals)
         back = O.read_all(pm, pb)
         run_pair(schema, n, packed, rec, back, src_wrap=1 if "8,10" in packed else 0)
+
+
+def test_acceptance_criterion_10_relocatable_state(ref):
+    """acceptance.cpp:772-790 through the C ABI: a static-extent aos-packed view of 16 particles
+    is trivially relocatable with stateBytes == blobBytes == 16 * 28; a dyn-extent one is not
+    and carries one i64 slot of runtime state (view.cpp:145-162)."""
+    L = lm()
+    fixed = L.View(L.Layout(R32, "i32:[16]", "aos-packed"))
+    assert fixed.is_trivially_relocatable() and fixed.state_bytes() == fixed.blob_bytes() == 16 * 28
+    dyn = L.View(L.Layout(R32, "i64:[dyn]", "aos-packed", dyn=(16,)))
+    assert not dyn.is_trivially_relocatable() and dyn.state_bytes() == dyn.blob_bytes() + 8
+    for text, wrap, dv, ext in (("soa-mb", 1, (), "i32:[16]"), ("aosoa:4", 2, (), "i32:[16]"),
+                                ("bitpack-float:5,10", 0, (9,), "i64:[dyn]")):
+        v = L.View(L.Layout(R32, ext, text, dyn=dv, wrap=wrap, granularity=5))
+        _, _, tr, sb, bb = ref.state_info(R32, ext, text, dv, wrap, 5)
+        assert (v.is_trivially_relocatable(), v.state_bytes(), v.blob_bytes()) == (tr, sb, bb)

@@ -190,3 +190,46 @@ def test_fused_p2p_transport_two_processes(layout):
                         "3"], cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     assert "OK" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+# ---- hand-written baselines (steps.hpp:124-230): separate kernels, no mapping -----------------
+@pytest.mark.parametrize("kind", ["manual-aos", "manual-soa"])
+@pytest.mark.parametrize("f64", [False, True], ids=["f32", "f64"])
+def test_manual_baseline_checksum_equals_library(kind, f64):
+    """acceptance.cpp:744-766: the hand-written baselines' checksum equals the library's
+    (exact mode: both bit-identical to the reference)."""
+    from paper_2302_08251_b200 import lamina as L
+    n, steps = 1024, 5
+    m = L.ManualNbody(kind, n, f64=f64, seed=42)
+    for _ in range(steps):
+        m.update(L.NBODY_EXACT)
+        m.move()
+    lib_view = run_gpu("aos-packed" if kind == "manual-aos" else "soa-mb", n, steps, f64=f64)
+    _, _, _, cs = O.nbody_run(n, steps, seed=42, dtype=np.float64 if f64 else np.float32)
+    assert m.checksum() == lib_view.nbody_checksum() == cs
+
+
+@pytest.mark.parametrize("kind", ["manual-aos", "manual-soa"])
+def test_manual_baseline_fast_within_tolerance(kind):
+    from paper_2302_08251_b200 import lamina as L
+    n, steps = 4096, 5
+    m = L.ManualNbody(kind, n, seed=42)
+    for _ in range(steps):
+        m.update(L.NBODY_FAST)
+        m.move()
+    _, _, _, cs = O.nbody_run(n, steps, seed=42, dtype=np.float64)
+    assert abs(m.checksum() - cs) <= FAST_TOL * abs(cs)
+
+
+def test_manual_runner_csv(capsys):
+    """runManual's CSV rows (runner.cpp:88-103) with the library layout's checksum text."""
+    from paper_2302_08251_b200.nbody import BenchConfig, run_benchmark
+    outs = {}
+    for lay in ("manual-soa", "soa-mb"):
+        assert run_benchmark(BenchConfig(layout=lay, n=512, steps=2, precision="f32")) == 0
+        rows = capsys.readouterr().out.strip().splitlines()
+        assert rows[0] == "layout,phase,simd_width,seconds_per_step,checksum"
+        assert [r.split(",")[:3] for r in rows[1:]] == [[lay, "update", "1"], [lay, "move", "1"]]
+        outs[lay] = rows[1].split(",")[-1]
+    assert outs["manual-soa"] == outs["soa-mb"]
+    assert run_benchmark(BenchConfig(layout="manual-aos", n=64, steps=1, simd_width=2)) == 2
