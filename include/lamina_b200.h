@@ -178,12 +178,14 @@ int lam_copy(const lam_view* src, lam_view* dst, void* stream);
 /* Same, over the element range [begin, end) only (both multiples of lam_layout_shard_unit
  * of src and dst, or end == element count): the per-shard call of a multi-GPU copy. */
 int lam_copy_range(const lam_view* src, lam_view* dst, uint64_t begin, uint64_t end, void* stream);
-/* copyView over HOST views: host blobs in, host blobs out (dst blobs are in/out so that
- * bytes the copy never writes keep their values).  Streams chunks through the GPU with
- * overlapped H2D / kernel / D2H.  Synchronous.  Host memory should be pinned. */
 /* lam_copy for n (src[k], dst[k]) pairs, each on its own device (SURVEY 8(b) lam_copy_sharded):
  * all copies in flight at once on per-device streams, returns when all are done. */
 int lam_copy_sharded(const lam_view* const* src, lam_view* const* dst, size_t n);
+/* copyView over HOST views: host blobs in, host blobs out (dst blobs are in/out so that
+ * bytes the copy never writes keep their values).  Streams chunks through the GPU with
+ * overlapped H2D / kernel / D2H.  Synchronous.  Host memory should be pinned.  The counter
+ * outputs (optional) receive per side the FieldAccessCount deltas reads[leaves], writes[leaves]
+ * (if the side counts) followed by the Heatmap block counters of every blob (if it has one). */
 int lam_copy_host(const lam_layout* src_layout, const void* const* src_host_blobs, const lam_layout* dst_layout,
                   void* const* dst_host_blobs, int device, uint64_t* src_counters, uint64_t* dst_counters);
 

@@ -1,12 +1,18 @@
 // Header-only C++ host mirror of the reference's hot-path API over the C ABI
 // (include/lamina_b200.h).  Same names, argument meaning and exception types as
 // lamina (/root/reference/proj/core/include/lamina/{layout_spec,view,instrument}.hpp),
-// so reference-style host code switches by changing the namespace:
+// so reference-style host code switches by changing the namespace for the calls below:
 //
-//   auto m = lamina_b200::parseLayout("aosoa:32", schemaText, "i32:[1048576]");
-//   lamina_b200::View src(lamina_b200::parseLayout("aos-packed", schemaText, "i32:[1048576]"));
-//   lamina_b200::View dst(m);
+//   const auto schema = lamina_b200::RecordSchema::parse(schemaText);
+//   const auto ext = lamina_b200::ArrayExtents::parse("i32:[1048576]", {});
+//   lamina_b200::View src(lamina_b200::parseLayout("aos-packed", schema, ext));
+//   lamina_b200::View dst(lamina_b200::parseLayout("aosoa:32", schema, ext));
 //   lamina_b200::copyView(src, dst);          // sm_100a kernels, stream-ordered
+//
+// Not mirrored: user-defined Mapping subclasses (mapping.hpp:44-155) -- a device view needs a
+// mapping the layout grammar can name; RecordSchema / ArrayExtents here are validated,
+// canonical text (no leaf-table or coordinate API).  Views the reference already owns go
+// through lamina::copyViewB200 (include/lamina_b200_binding.hpp).
 //
 // Errors are rethrown as std::invalid_argument / std::out_of_range / std::overflow_error /
 // std::logic_error with the reference's messages; CUDA failures as std::runtime_error.
@@ -116,11 +122,86 @@ namespace lamina_b200
 
     using MappingPtr = std::shared_ptr<const Mapping>;
 
+    /// lamina::RecordSchema::parse (record.cpp:364-479): validated, held as canonical text.
+    class RecordSchema
+    {
+    public:
+        static RecordSchema parse(const std::string& text)
+        {
+            lam_layout* h = nullptr;
+            check(lam_layout_create(text.c_str(), "i32:[1]", nullptr, 0, "aos-packed", 0, 0, &h));
+            RecordSchema s;
+            s.text_.resize(lam_layout_schema(h, nullptr, 0));
+            lam_layout_schema(h, s.text_.data(), s.text_.size() + 1);
+            lam_layout_destroy(h);
+            return s;
+        }
+        const std::string& toString() const noexcept
+        {
+            return text_;
+        }
+        bool operator==(const RecordSchema& o) const noexcept
+        {
+            return text_ == o.text_;
+        }
+
+    private:
+        std::string text_;
+    };
+
+    /// lamina::ArrayExtents::parse(text, dynamicValues) (extents.cpp:118-177): validated
+    /// ("index type overflow", ...), canonical text plus the dynamic values.
+    class ArrayExtents
+    {
+    public:
+        static ArrayExtents parse(const std::string& text, const std::vector<std::uint64_t>& dynamicValues)
+        {
+            lam_layout* h = nullptr;
+            check(lam_layout_create("Record{v:u8}", text.c_str(), dynamicValues.data(), dynamicValues.size(),
+                                    "aos-packed", 0, 0, &h));
+            ArrayExtents e;
+            e.text_.resize(lam_layout_extents(h, nullptr, 0));
+            lam_layout_extents(h, e.text_.data(), e.text_.size() + 1);
+            e.count_ = lam_layout_element_count(h);
+            lam_layout_destroy(h);
+            e.dyn_ = dynamicValues;
+            return e;
+        }
+        const std::string& toString() const noexcept
+        {
+            return text_;
+        }
+        const std::vector<std::uint64_t>& dynamicValues() const noexcept
+        {
+            return dyn_;
+        }
+        bool isFullyStatic() const noexcept
+        {
+            return dyn_.empty();
+        }
+        std::uint64_t elementCount() const noexcept
+        {
+            return count_;
+        }
+
+    private:
+        std::string text_;
+        std::vector<std::uint64_t> dyn_;
+        std::uint64_t count_ = 0;
+    };
+
     /// lamina::parseLayout(text, schema, extents) (layout_spec.hpp:19), schema/extents as text.
     inline MappingPtr parseLayout(const std::string& text, const std::string& schema, const std::string& extents,
                                   const std::vector<std::uint64_t>& dyn = {})
     {
         return std::make_shared<const Mapping>(schema, extents, text, dyn);
+    }
+
+    /// lamina::parseLayout(std::string_view, const RecordSchema&, const ArrayExtents&)
+    /// (layout_spec.hpp:19), the reference's own signature.
+    inline MappingPtr parseLayout(const std::string& text, const RecordSchema& schema, const ArrayExtents& extents)
+    {
+        return std::make_shared<const Mapping>(schema.toString(), extents.toString(), text, extents.dynamicValues());
     }
 
     /// lamina::View on a device: zero-filled blobs in HBM (or adopted device pointers).

@@ -9,7 +9,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import MIXED, R32, R64, ROOT, random_values
+from conftest import MIXED, R32, R64, ROOT, leaf_types, random_values
 from oracle import lamina_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -343,3 +343,89 @@ def test_acceptance_criterion_10_relocatable_state(ref):
         v = L.View(L.Layout(R32, ext, text, dyn=dv, wrap=wrap, granularity=5))
         _, _, tr, sb, bb = ref.state_info(R32, ext, text, dv, wrap, 5)
         assert (v.is_trivially_relocatable(), v.state_bytes(), v.blob_bytes()) == (tr, sb, bb)
+
+
+# ---- edge cases the reference's own tests pin -------------------------------------------------
+def test_bitpack_int16_equals_soa_u16():
+    """acceptance.cpp:389-404: bitpack-int:16 over u16 leaves is byte-identical to soa-mb u16
+    (the packed blob is the soa blob padded to whole 32-bit words)."""
+    L = lm()
+    schema, n = "Record{v:u16,w:u16}", 4099
+    rng = np.random.default_rng(16)
+    vals = random_values(rng, [5, 5], n)
+    run_pair(schema, n, "aos-packed", "bitpack-int:16", vals)
+    soa = L.View(L.Layout(schema, f"i32:[{n}]", "soa-mb"))
+    ms = O.make(schema, f"i32:[{n}]", "soa-mb")
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    soa.upload_all(sb)
+    pk = L.View(L.Layout(schema, f"i32:[{n}]", "bitpack-int:16"))
+    L.copy_view(soa, pk)
+    for nr, blob in enumerate(pk.download_all()):
+        assert blob.nbytes == (n * 16 + 31) // 32 * 4
+        assert np.array_equal(blob[: 2 * n], sb[nr]) and not blob[2 * n:].any()
+
+
+@pytest.mark.parametrize("schema,bits", [("Record{a:i8,b:u8}", 3), ("Record{a:i8,b:u8}", 8),
+                                         ("Record{a:i16,b:u16}", 11), ("Record{v:u64}", 33),
+                                         ("Record{v:u64,w:i64}", 47), ("Record{v:i64}", 64),
+                                         ("Record{a:i8,b:u64,c:i16}", 5)])
+def test_bitpack_int_other_widths(schema, bits):
+    """BitpackIntSoA on 8/16/64-bit leaves (computed.cpp:59-67,101-122): pack truncates to the
+    low b bits, unpack zero/sign-extends; 1 <= b <= 8 * leaf size."""
+    n = 4099
+    rng = np.random.default_rng(bits)
+    vals = random_values(rng, leaf_types(schema), n)
+    for phys in ("soa-mb", "aos-packed", "aosoa:8"):
+        run_pair(schema, n, phys, f"bitpack-int:{bits}", vals)
+    packed = O.make(schema, f"i32:[{n}]", f"bitpack-int:{bits}")
+    pb = O.zero_blobs(packed)
+    O.write_all(packed, pb, vals)
+    back = O.read_all(packed, pb)
+    for phys in ("soa-mb", "aos-packed"):
+        run_pair(schema, n, f"bitpack-int:{bits}", phys, back)
+
+
+@pytest.mark.parametrize("fmt", ["11,52", "8,23", "5,10", "8,10", "4,3", "15,40"])
+def test_bitpack_float_f64_leaves(fmt):
+    """BitpackFloatSoA on f64 leaves (computed.cpp:133-222; bitpack.cpp:96-188): e11m52 is
+    binary64 itself, the rest round through floatEncode(double)."""
+    n = 4099
+    rng = np.random.default_rng(52)
+    vals = random_values(rng, [9] * 7, n)
+    for phys in ("aos-packed", "soa-mb"):
+        run_pair(R64, n, phys, f"bitpack-float:{fmt}", vals)
+    packed = O.make(R64, f"i32:[{n}]", f"bitpack-float:{fmt}")
+    pb = O.zero_blobs(packed)
+    O.write_all(packed, pb, vals)
+    run_pair(R64, n, f"bitpack-float:{fmt}", "soa-mb", O.read_all(packed, pb))
+
+
+BOOLREC = "Record{a:bool,b:u8,c:bool,d:f32,e:bool}"
+
+
+@pytest.mark.parametrize("generic", [False, True], ids=["specialised", "generic"])
+@pytest.mark.parametrize("a,b", [("aos-packed", "soa-mb"), ("soa-mb", "aosoa:4"), ("aos-aligned", "soa-sb"),
+                                 ("aos-packed", "bytesplit:soa-mb"), ("aosoa:3", "aos-packed"),
+                                 ("soa-sb", "changetype:f32=f64:aos-packed")])
+def test_bool_bytes_canonicalise_on_read(a, b, generic, monkeypatch):
+    """ScalarValue::fromStorageBits(Bool) = bits != 0 (scalar.hpp:259-261): a bool byte 0x02..0xFF
+    in the source is written as 0x01 by every fieldwise copy path."""
+    L = lm()
+    n = 1031
+    ext = f"i32:[{n}]"
+    if generic:
+        monkeypatch.setenv("LAMB_FORCE_GENERIC", "1")
+    ms, md = O.make(BOOLREC, ext, a), O.make(BOOLREC, ext, b)
+    rng = np.random.default_rng(2)
+    sb = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(ms)]
+    assert any((x > 1).any() for x in sb)
+    db = O.zero_blobs(md)
+    O.copy_view(ms, sb, md, db)
+    gs, gd = L.View(L.Layout(BOOLREC, ext, a)), L.View(L.Layout(BOOLREC, ext, b))
+    gs.upload_all(sb)
+    L.copy_view(gs, gd)
+    for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
+        assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
+    vals = O.read_all(md, db)
+    assert set(np.unique(vals[:, [0, 2, 4]])) <= {0, 1}
