@@ -104,8 +104,11 @@ def cpu_reference(parts):
     return out
 
 
-def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")):
+def run_suite(L, device=0, peak_gbs=None, parts=("C1", "C3", "C4", "C5", "C6")):
     import torch
+    if peak_gbs is None:
+        from bench import peaks
+        peak_gbs = peaks()[0]  # MEASURED_PEAKS.json hbm_gbs
     out = {}
     # ---- C1 ------------------------------------------------------------------------------
     if "C1" in parts:
@@ -173,6 +176,20 @@ def run_suite(L, device=0, peak_gbs=6550.7, parts=("C1", "C3", "C4", "C5", "C6")
                 row["move_ms"] = _time(lambda: v.nbody_move(), reps=3)
                 c4[lay] = row
                 del v
+            # the reference's hand-written baselines (steps.hpp:124-230) as plain device kernels:
+            # library / hand-written = paper Fig. 3's ratio
+            for kind, lib_lay in (("manual-aos", "aos-packed"), ("manual-soa", "soa-mb")):
+                m = L.ManualNbody(kind, n, seed=42)
+                row = {}
+                for mode, name in ((1, "fast"), (0, "exact")):
+                    ms = _time(lambda: m.update(mode), reps=5, warm=2)
+                    ips = n * n / (ms * 1e-3)
+                    row[name] = {"ms_per_update": ms, "interactions/s": ips,
+                                 "frac_measured_fp32_peak": ips * 20 / 1e12 / measured,
+                                 "library_over_handwritten": c4[lib_lay][name]["interactions/s"] / ips}
+                row["move_ms"] = _time(lambda: m.move(), reps=3)
+                c4[kind] = row
+                del m
         out["C4_nbody_128K_f32"] = dict(
             c4, fp32_peak_measured_tflops=measured, fp32_peak_nominal_tflops=nominal,
             clocks_during_peak=clk_peak.summary(), clocks_during_nbody=clk.summary(),

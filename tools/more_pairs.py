@@ -3,6 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from bench_suite import _time, _fill, R32, R64
 from paper_2302_08251_b200 import lamina as L
+from bench import peaks
+PEAK = peaks()[0]  # MEASURED_PEAKS.json hbm_gbs
 MIXED = "Record{a:f64,b:u16,c:i8,d:f32}"
 n = 1 << 26
 for schema, a, b in [("Record{v:u16,w:u16}", "soa-mb", "bitpack-int:5"), ("Record{v:u16,w:u16}", "bitpack-int:5", "soa-mb"),
@@ -15,5 +17,5 @@ for schema, a, b in [("Record{v:u16,w:u16}", "soa-mb", "bitpack-int:5"), ("Recor
     _fill(L, s, 1)
     ms = _time(lambda: L.copy_view(s, d), reps=3, warm=1)
     byt = sum(la.blob_sizes) + sum(lb.blob_sizes)
-    print(f"{schema[:22]:22} {a:>32} -> {b:<32} {byt / ms / 1e6:7.0f} GB/s  {byt / ms / 1e6 / 6550.7:.2f}", flush=True)
+    print(f"{schema[:22]:22} {a:>32} -> {b:<32} {byt / ms / 1e6:7.0f} GB/s  {byt / ms / 1e6 / PEAK:.2f}", flush=True)
     del s, d
