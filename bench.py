@@ -368,6 +368,72 @@ def _c2_slices(layout, n, a, c):
     return [(0, 4 * n * f + 4 * a, 4 * n * f + 4 * (a + c), 0, 4 * c * f, 4 * c * (f + 1)) for f in range(7)]
 
 
+def run_c4_strong(L, world, rank, local, steps=5, warmup=2, n=128 * 1024, layout="soa-mb"):
+    """C4 strong scaling: 128K particles TOTAL split over the ranks (i-range shards), per step
+    update + move + the positions-only all-gather (distributed.py; one collective of 12 B per
+    particle, Mass once).  Step time = max over ranks of the per-step CUDA-event time."""
+    from paper_2302_08251_b200.distributed import nbody_distributed
+    out = {"particles_total": n, "layout": layout, "steps": steps,
+           "exchange": "one all-gather of packed x,y,z per step (NCCL); Mass gathered once"}
+    for mode, name in ((1, "fast"), (0, "exact")):
+        nbody_distributed(layout, n, warmup, mode=mode)  # warm-up: allocation, NCCL rings, caches
+        barrier(world)
+        t = {}
+        nbody_distributed(layout, n, steps, mode=mode, timing=t)
+        step = max_over_ranks(t["step_ms"], world)
+        exch = max_over_ranks(t["exchange_ms"], world)
+        upd = max_over_ranks(t["update_ms"], world)
+        out[name] = {"ms_per_step": step, "update_ms": upd, "exchange_ms": exch, "move_ms": t["move_ms"],
+                     "interactions_per_s": n * n / (step * 1e-3),
+                     "exchange_bytes_per_step": t["exchange_bytes_per_step"]}
+    return out
+
+
+def run_c5_sharded(L, world, rank, local, total=1_000_000_000, reps=3):
+    """C5: 1e9 R64 records TOTAL, sharded by index over the ranks (no collective on the data
+    path): aos-packed f64 -> FieldAccessCount(changetype:f64=f32:bytesplit:soa-mb), source =
+    scalarSample(F64, i*7+f) of the GLOBAL index, generated on each device.  GB/s = 84 B x 1e9
+    over the max-over-ranks copy time; write counters summed over ranks must be 1e9 per leaf."""
+    import torch
+    import torch.distributed as dist
+    per = total // world
+    lo = rank * per
+    n = total - lo if rank == world - 1 else per
+    ext = f"i32:[{n}]"
+    src_t = torch.empty(n * 7, dtype=torch.float64, device="cuda")
+    step = 1 << 26
+    for a in range(0, n * 7, step):
+        b = min(n * 7, a + step)
+        s = torch.arange(lo * 7 + a, lo * 7 + b, dtype=torch.int64, device="cuda")
+        h = s * (0x9E3779B97F4A7C15 - 2**64) + 0x2545F4914F6CDD1D
+        src_t[a:b] = ((h >> 11) & ((1 << 53) - 1)).to(torch.float64) * 2.0 ** -53 * 4.0 - 2.0
+    torch.cuda.synchronize()
+    src = L.View(L.Layout(R64, ext, "aos-packed"), device=local, blobs=[src_t.data_ptr()], blob_bytes=[n * 56])
+    dst = L.View(L.Layout(R64, ext, "changetype:f64=f32:bytesplit:soa-mb", wrap=1), device=local)
+    torch.cuda.synchronize()
+    L.copy_view(src, dst)
+    torch.cuda.synchronize()
+    dst.reset_counters()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    e0.record()
+    for _ in range(reps):
+        L.copy_view(src, dst)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / reps, world)
+    _, w = dst.counters()
+    wt = torch.tensor([int(x) for x in w], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(wt)
+    writes = [int(x) // reps for x in wt.tolist()]
+    del src, dst, src_t
+    torch.cuda.synchronize()
+    return {"records_total": total, "records_per_gpu": per, "ms": ms, "GB/s": 84 * total / (ms * 1e-3) / 1e9,
+            "GB/s_per_gpu": 84 * total / world / (ms * 1e-3) / 1e9, "writes_per_leaf_total": writes,
+            "counters_ok": writes == [total] * 7, "layout": "aos-packed(R64) -> FAC(changetype:f64=f32:bytesplit:soa-mb)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -380,6 +446,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C4 strong / C5 sharded keys")
     args = ap.parse_args()
     if args.impl == "reference":
         # the reference arm is CPU-only: no process group, rank 0 alone works and prints
@@ -471,6 +538,10 @@ def main():
         e2e = run_c2_e2e(L, n if world == 1 else min(n, 1 << 24), args.e2e_steps, local, world)
         if rank == 0:
             line["e2e"] = e2e
+    if not args.no_extra:
+        # configs that shard / communicate at N GPUs (informative keys beside the C2 headline)
+        line["c4_strong"] = run_c4_strong(L, world, rank, local)
+        line["c5_sharded"] = run_c5_sharded(L, world, rank, local)
     if args.suite and rank == 0:
         from bench_suite import run_suite
         line["suite"] = run_suite(L, local)

@@ -244,6 +244,11 @@ int lam_nbody_update_multi(lam_view* view, const lam_view* const* j_views, const
                            const uint64_t* j_end, size_t n_sources, int mode, uint64_t i_begin, uint64_t i_end,
                            void* stream);
 /* CUDA IPC of device allocations (64-byte handles) for the fused multi-GPU step. */
+/* Positions-only exchange of the multi-GPU step: particles [i_begin, i_end) of the
+ * view packed into `out` (device) as SoA x[cnt], y[cnt], z[cnt] (and m[cnt] with with_mass),
+ * cnt = i_end - i_begin, in the view's float type; read through the view's mapping. */
+int lam_nbody_pack_positions(const lam_view* view, uint64_t i_begin, uint64_t i_end, int with_mass, void* out,
+                             void* stream);
 int lam_ipc_get_handle(const void* device_ptr, void* handle64_out);
 int lam_ipc_open(const void* handle64, int device, void** device_ptr);
 int lam_ipc_close(void* device_ptr);

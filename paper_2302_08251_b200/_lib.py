@@ -78,6 +78,7 @@ _SIGS = {
     "lam_nbody_update": (i32, [vp, i32, u64, u64, vp]),
     "lam_nbody_move": (i32, [vp, u64, u64, vp]),
     "lam_nbody_checksum": (i32, [vp, C.POINTER(C.c_double)]),
+    "lam_nbody_pack_positions": (i32, [vp, u64, u64, i32, vp, vp]),
     "lam_nbody_manual_create": (i32, [cp, u64, i32, u64, i32, vp, C.POINTER(vp)]),
     "lam_nbody_manual_update": (i32, [vp, i32, vp]),
     "lam_nbody_manual_move": (i32, [vp, vp]),

@@ -16,6 +16,8 @@ namespace lamk
     cudaError_t nbody_update_multi(const lamp_view* v, bool f64, bool exact, bool phys, const lamp_view* const* jv,
                                    const uint64_t* jb, const uint64_t* je, size_t nj, uint64_t ib, uint64_t ie,
                                    cudaStream_t s);
+    cudaError_t nbody_pack(const lamp_view* v, bool f64, bool phys, uint64_t ib, uint64_t ie, bool withMass, void* out,
+                           cudaStream_t s);
     cudaError_t nbody_manual_update(bool soa, bool f64, bool exact, void* base, uint64_t n, cudaStream_t s);
     cudaError_t nbody_manual_move(bool soa, bool f64, void* base, uint64_t n, cudaStream_t s);
 } // namespace lamk
@@ -389,6 +391,24 @@ extern "C"
                 if(v->L->fac || v->L->heat)
                     lam_cuda_check(lamk::nbody_account(v->img.hdr, true, n, ib, ie, static_cast<cudaStream_t>(stream)),
                                    "nbody_account");
+            });
+    }
+
+    int lam_nbody_pack_positions(const lam_view* v, uint64_t ib, uint64_t ie, int with_mass, void* out, void* stream)
+    {
+        return guard2(
+            [&]
+            {
+                const bool f64 = particleF64(v);
+                const uint64_t n = v->L->map->elementCount();
+                if(ib > ie || ie > n)
+                    throw std::out_of_range("index out of range: particles");
+                if(!out && ie > ib)
+                    throw std::invalid_argument("n-body pack: null output buffer");
+                DeviceGuard g(v->device);
+                lam_cuda_check(lamk::nbody_pack(v->img.hdr, f64, particlePhys(v), ib, ie, with_mass != 0, out,
+                                                static_cast<cudaStream_t>(stream)),
+                               "nbody_pack");
             });
     }
 

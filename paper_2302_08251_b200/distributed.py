@@ -2,12 +2,20 @@
 
 * copy / pack / instrument: every rank owns the element range `shard_range(...)` of every blob;
   no collective (weak scaling, `lam_copy_range`).
-* n-body: every rank holds the whole view, updates Vel / moves Pos of its own i-range, then the
-  ranks all-gather the byte regions their ranges occupy in each blob stream (NCCL over NVLink on
-  GPUs, gloo in the CPU tests).  Per-i arithmetic is independent of the sharding, so the result
-  is bit-identical to one GPU in exact mode.
+* n-body (transport "allgather", the SURVEY §8e plan): every rank owns the i-range
+  [r*S, (r+1)*S) of the particles in the chosen mapping.  Per step it updates Vel of its
+  i-range against all j, moves its Pos, packs its positions as SoA x,y,z (12 B/particle for
+  f32) into its slot of a replicated exchange buffer G[world][3][S], and ONE all-gather
+  (NCCL over NVLink) refreshes G everywhere.  Mass is constant: gathered once at init into
+  M[n].  The update reads j from G and M through one soa-mb view per rank slot (blob
+  pointers into G, `exchange_pointers`), visited in global j order, so exact mode is
+  bit-identical to one GPU.
+* transport "p2p": the fused step -- peers' blobs are mapped with CUDA IPC and read over
+  NVLink inside the update kernel (`lam_nbody_update_multi`), no gathered copy.
 """
 from __future__ import annotations
+
+import math
 
 
 def shard_range(n: int, unit: int, rank: int, world: int) -> tuple[int, int]:
@@ -18,69 +26,121 @@ def shard_range(n: int, unit: int, rank: int, world: int) -> tuple[int, int]:
     return lo, hi
 
 
-def stream_regions(layout, lo: int, hi: int):
-    """[(nr, byte_lo, byte_hi)] per blob stream for elements [lo, hi)."""
-    return [layout.stream_region(s, lo, hi) for s in range(layout.stream_count)]
+def exchange_shape(n: int, unit: int, world: int) -> int:
+    """Particles per rank S of the positions-only exchange (equal shards, S a multiple of the
+    layout's shard unit and of 4 so every slot pointer stays 16-byte aligned)."""
+    u = unit * 4 // math.gcd(unit, 4)
+    if n % (world * u):
+        raise ValueError(f"n-body all-gather needs n ({n}) to be a multiple of world*unit ({world * u})")
+    return n // world
 
 
-def allgather_regions(layout, blobs, world: int, group=None):
-    """All-gather every rank's shard regions into the replicated blobs (torch uint8 tensors).
+def exchange_pointers(base: int, n: int, world: int, elem: int, mass_base: int):
+    """Blob pointers of the soa-mb j-view of rank slot r of G[world][3][S] (S = n/world):
+    x_r = G + (3rS - rS)*elem, so x_r + j*elem addresses G[r][0][j - rS] for j in [rS, (r+1)S);
+    y_r = x_r + S*elem, z_r = x_r + 2S*elem.  Vel (never read by the update) and Mass point
+    at M[n].  Every pointer stays inside G."""
+    S = n // world
+    out = []
+    for r in range(world):
+        x = base + 2 * r * S * elem
+        out.append([x, x + S * elem, x + 2 * S * elem, mass_base, mass_base, mass_base, mass_base])
+    return out
 
-    Needs equal shards: element count a multiple of world * shard_unit.
-    """
+
+def world_rank(group=None) -> tuple[int, int]:
+    """(world size, rank) of the group; (1, 0) without an initialised process group."""
     import torch.distributed as dist
-    n = layout.element_count
-    unit = layout.shard_unit
-    if n % (world * unit):
-        raise ValueError(f"n-body all-gather needs n ({n}) to be a multiple of world*shard_unit ({world * unit})")
-    per = n // world
-    rank = dist.get_rank(group)
-    for s in range(layout.stream_count):
-        nr, a0, _ = layout.stream_region(s, 0, per)
-        _, _, b_last = layout.stream_region(s, (world - 1) * per, n)
-        _, lo, hi = layout.stream_region(s, rank * per, (rank + 1) * per)
-        if hi <= lo:
-            continue
-        out = blobs[nr][a0:b_last]
-        piece = blobs[nr][lo:hi]
-        if out.numel() != world * piece.numel():
-            raise ValueError("stream regions are not equal per rank")
-        dist.all_gather_into_tensor(out, piece.clone() if out.device.type == "cpu" else piece, group=group)
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def all_gather_slot(buf, rank: int, world: int, group=None):
+    """In-place all-gather of rank's equal slot of `buf` (1-D tensor) into every slot: NCCL
+    all-gather on CUDA tensors; staged through host memory for gloo (CPU tests)."""
+    import torch.distributed as dist
+    if world == 1:
+        return
+    per = buf.numel() // world
+    slot = buf[rank * per:(rank + 1) * per]
+    if buf.device.type == "cuda" and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, slot, group=group)
+        return
+    host = buf.cpu()
+    dist.all_gather_into_tensor(host, host[rank * per:(rank + 1) * per].clone(), group=group)
+    buf.copy_(host)
 
 
 def nbody_distributed(layout_text: str, n: int, steps: int, mode: int = 0, seed: int = 42, f64: bool = False,
-                      group=None, transport: str = "allgather"):
+                      group=None, transport: str = "allgather", timing: dict | None = None):
     """Run the n-body benchmark with the particles sharded over the process group.
 
-    transport "allgather": every rank updates and moves its i-shard, then the shards' blob
-    regions are all-gathered (NCCL over NVLink).  transport "p2p": the fused step -- every
-    rank maps its peers' views (CUDA IPC) and the update kernel reads their positions over
-    NVLink directly (lam_nbody_update_multi); a barrier separates update and move.
+    transport "allgather": positions-only exchange (module docstring), one all-gather per step.
+    transport "p2p": the fused step over CUDA IPC (see `_nbody_p2p`).
+    With `timing` (a dict), per-step CUDA-event times are recorded: update_ms, move_ms,
+    exchange_ms (pack + all-gather), step_ms.
 
-    Returns (view, blobs): the view holds the whole replicated state after the last step.
+    Returns (view, exchange): the view's own i-range [r*S, (r+1)*S) holds the rank's final
+    state; for "allgather" exchange = (G, M), the replicated final positions and masses.
     """
     if transport == "p2p":
         return _nbody_p2p(layout_text, n, steps, mode, seed, f64, group)
     import torch
-    import torch.distributed as dist
 
     from . import lamina as L
     t = "f64" if f64 else "f32"
     schema = f"Record{{Pos:Record{{x:{t},y:{t},z:{t}}},Vel:Record{{x:{t},y:{t},z:{t}}},Mass:{t}}}"
     lay = L.Layout(schema, f"i64:[{n}]", layout_text)
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    world, rank = world_rank(group)
     dev = torch.cuda.current_device()
-    blobs = [torch.zeros(max(16, s), dtype=torch.uint8, device="cuda") for s in lay.blob_sizes]
-    view = L.View(lay, device=dev, blobs=[b.data_ptr() for b in blobs], blob_bytes=lay.blob_sizes)
+    S = exchange_shape(n, lay.shard_unit, world)
+    lo, hi = rank * S, (rank + 1) * S
+    dtype = torch.float64 if f64 else torch.float32
+    elem = 8 if f64 else 4
+    view = L.View(lay, device=dev)
     view.nbody_init(seed)
-    lo, hi = shard_range(n, lay.shard_unit, rank, world)
     stream = torch.cuda.current_stream()
+    G = torch.empty(world * 3 * S, dtype=dtype, device="cuda")
+    M = torch.empty(n, dtype=dtype, device="cuda")
+    tmp = torch.empty(4 * S, dtype=dtype, device="cuda")
+    view.nbody_pack_positions(lo, hi, tmp.data_ptr(), with_mass=True, stream=stream)
+    G[rank * 3 * S:(rank + 1) * 3 * S].copy_(tmp[:3 * S])
+    M[lo:hi].copy_(tmp[3 * S:])
+    del tmp
+    all_gather_slot(M, rank, world, group)  # Mass once
+    all_gather_slot(G, rank, world, group)
+    soa = L.Layout(schema, f"i64:[{n}]", "soa-mb")
+    jviews = [L.View(soa, device=dev, blobs=p, blob_bytes=[n * elem] * 7)
+              for p in exchange_pointers(G.data_ptr(), n, world, elem, M.data_ptr())]
+    sources = [(jviews[r], r * S, (r + 1) * S) for r in range(world)]
+    slot = G[rank * 3 * S:(rank + 1) * 3 * S]
+    ev = []
     for _ in range(steps):
-        view.nbody_update(mode, lo, hi, stream=stream)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing is not None else None
+        if e:
+            e[0].record(stream)
+        view.nbody_update_from(sources, mode, lo, hi, stream=stream)
+        if e:
+            e[1].record(stream)
         view.nbody_move(lo, hi, stream=stream)
-        allgather_regions(lay, blobs, world, group)
+        if e:
+            e[2].record(stream)
+        view.nbody_pack_positions(lo, hi, slot.data_ptr(), stream=stream)
+        all_gather_slot(G, rank, world, group)
+        if e:
+            e[3].record(stream)
+            ev.append(e)
     torch.cuda.synchronize()
-    return view, blobs
+    if timing is not None and ev:
+        k = len(ev)
+        timing["update_ms"] = sum(e[0].elapsed_time(e[1]) for e in ev) / k
+        timing["move_ms"] = sum(e[1].elapsed_time(e[2]) for e in ev) / k
+        timing["exchange_ms"] = sum(e[2].elapsed_time(e[3]) for e in ev) / k
+        timing["step_ms"] = sum(e[0].elapsed_time(e[3]) for e in ev) / k
+        timing["exchange_bytes_per_step"] = 3 * n * elem
+    del jviews
+    return view, (G, M)
 
 
 def _nbody_p2p(layout_text, n, steps, mode, seed, f64, group):

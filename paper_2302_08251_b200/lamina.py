@@ -391,6 +391,11 @@ class View:
         je = (C.c_uint64 * k)(*[int(e) for _, _, e in sources])
         _check(lib().lam_nbody_update_multi(self._h, hv, jb, je, k, mode, begin, end, _stream_handle(stream)))
 
+    def nbody_pack_positions(self, begin: int, end: int, out_ptr: int, with_mass: bool = False, stream=None) -> None:
+        """SoA x, y, z (, m) of particles [begin, end) into the device buffer at out_ptr."""
+        _check(lib().lam_nbody_pack_positions(self._h, begin, end, 1 if with_mass else 0, C.c_void_p(out_ptr),
+                                              _stream_handle(stream)))
+
     def nbody_checksum(self) -> float:
         out = C.c_double()
         _check(lib().lam_nbody_checksum(self._h, C.byref(out)))

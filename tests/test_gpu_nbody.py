@@ -233,3 +233,17 @@ def test_manual_runner_csv(capsys):
         outs[lay] = rows[1].split(",")[-1]
     assert outs["manual-soa"] == outs["soa-mb"]
     assert run_benchmark(BenchConfig(layout="manual-aos", n=64, steps=1, simd_width=2)) == 2
+
+
+@pytest.mark.parametrize("layout,mode", [("soa-mb", 0), ("aosoa:8", 0), ("aos-packed", 1)])
+def test_allgather_transport_two_processes(layout, mode):
+    """nbody_distributed(transport="allgather"): the positions-only exchange (one all-gather of
+    12 B/particle per step, Mass once) with the real kernels in two processes (here sharing one
+    GPU, gloo) equals the single-view run: bit-identical in exact mode."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29543", "tools/allgather_check.py", layout,
+                        "4096", "3", str(mode)], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "OK" in r.stdout, r.stdout + r.stderr[-2000:]
