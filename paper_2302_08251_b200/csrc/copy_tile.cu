@@ -227,6 +227,8 @@ namespace lamk
                         return ((pp >> 15) << 31) | 0x7FC00000u;
                     return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pp))));
                 }
+                if(L.stype == lamd::F32 && L.sE <= 8 && L.sM <= 23)
+                    return lamd::float_decode_f32(static_cast<uint32_t>(pat), L.sE, L.sM);
                 const uint64_t d = lamd::float_decode(pat, L.sE, L.sM);
                 return L.stype == lamd::F32 ? lamd::f64_to_f32_bits(d) : d;
             }
@@ -273,11 +275,10 @@ namespace lamk
                     pat = lamd::encode_e8m10_f32(static_cast<uint32_t>(v));
                 else if(L.dtype == lamd::F32 && L.dE == 5 && L.dM == 10)
                     pat = lamd::encode_e5m10_f32(static_cast<uint32_t>(v));
+                else if(L.dtype == lamd::F32)
+                    pat = lamd::float_encode_f32(static_cast<uint32_t>(v), L.dE, L.dM);
                 else
-                {
-                    const uint64_t d = L.dtype == lamd::F32 ? lamd::f32_to_f64_bits(static_cast<uint32_t>(v)) : v;
-                    pat = lamd::float_encode(d, L.dE, L.dM);
-                }
+                    pat = lamd::float_encode(v, L.dE, L.dM);
                 if(s.scratch64)
                     reinterpret_cast<unsigned long long*>(dbuf + s.scratch_off)[e] = pat;
                 else

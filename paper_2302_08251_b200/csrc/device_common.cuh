@@ -170,6 +170,94 @@ namespace lamd
         return mag | (sign << 63);
     }
 
+    // RNE of x / 2^s for 0 < s < 32 (rneShift, bitpack.cpp:57-69, on 32-bit significands)
+    LAM_DEV uint32_t rne32(uint32_t x, uint32_t s)
+    {
+        const uint32_t q = x >> s;
+        const uint32_t rem = x & ((1u << s) - 1u);
+        const uint32_t half = 1u << (s - 1);
+        return (rem > half || (rem == half && (q & 1u))) ? q + 1 : q;
+    }
+
+    // floatEncode((double)f, E, M) for an f32 input f, in 32-bit integer arithmetic.  The f32
+    // significand has 24 bits, so the reference's RNE of the 53-bit double significand (whose
+    // low 29 bits are zero) by 52 - M is the RNE of the 24-bit one by 23 - M; M > 23 shifts
+    // left exactly.  Every E >= 1 and width 1 + E + M <= 64; checked against float_encode on
+    // all 2^32 inputs for a set of formats (tests/test_gpu_codec.py).
+    LAM_DEV uint64_t float_encode_f32(uint32_t b, uint32_t E, uint32_t M)
+    {
+        const uint64_t signBit = uint64_t(b >> 31) << (E + M);
+        const uint64_t expMask = low_mask(E);
+        const uint64_t inf = signBit | (expMask << M);
+        const uint32_t a = b & 0x7FFFFFFFu;
+        if(a >= 0x7F800000u)
+            return (a == 0x7F800000u || M == 0) ? inf : (inf | (1ull << (M - 1)));
+        if(a == 0)
+            return signBit;
+        uint32_t frac = a & 0x7FFFFFu;
+        int e2; // value = frac * 2^e2, frac in [2^23, 2^24)
+        if((a >> 23) == 0)
+        {
+            const int sh = __clz(frac) - 8;
+            frac <<= sh;
+            e2 = 1 - 127 - 23 - sh;
+        }
+        else
+        {
+            frac |= 1u << 23;
+            e2 = static_cast<int>(a >> 23) - 127 - 23;
+        }
+        const int64_t bias = (int64_t(1) << (E - 1)) - 1;
+        int64_t biasedExp = e2 + 23 + bias;
+        const int64_t maxExpField = static_cast<int64_t>(expMask);
+        if(biasedExp >= 1)
+        {
+            uint64_t q = M <= 23 ? (M == 23 ? frac : rne32(frac, 23 - M)) : (uint64_t(frac) << (M - 23));
+            if((q >> (M + 1)) != 0)
+            {
+                q >>= 1;
+                ++biasedExp;
+            }
+            if(biasedExp >= maxExpField)
+                return inf;
+            return signBit | (static_cast<uint64_t>(biasedExp) << M) | (q - (1ull << M));
+        }
+        const int64_t shift = (1 - bias - static_cast<int64_t>(M)) - e2;
+        const uint64_t q = shift <= 0 ? (uint64_t(frac) << (-shift)) : (shift >= 32 ? 0 : rne32(frac, uint32_t(shift)));
+        if((q >> M) != 0)
+        {
+            if(1 >= maxExpField)
+                return inf;
+            return signBit | (1ull << M);
+        }
+        return signBit | q;
+    }
+
+    // (float)floatDecode(p, E, M) (bitpack.cpp:165-188, scalar.hpp:151-152) for E <= 8, M <= 23:
+    // every such minifloat is exactly an f32, so the bits are assembled directly; NaN -> the
+    // f32 quiet NaN with the sign, as the double quiet_NaN converts
+    LAM_DEV uint32_t float_decode_f32(uint32_t p, uint32_t E, uint32_t M)
+    {
+        const uint32_t sign = ((p >> (E + M)) & 1u) << 31;
+        const uint32_t allOnes = (1u << E) - 1u;
+        const uint32_t ef = (p >> M) & allOnes;
+        const uint32_t man = p & ((1u << M) - 1u);
+        const int bias = (1 << (E - 1)) - 1;
+        if(ef == allOnes)
+            return sign | (man ? 0x7FC00000u : 0x7F800000u);
+        if(ef == 0)
+        {
+            if(man == 0)
+                return sign;
+            const int top = 31 - __clz(man);              // man in [2^top, 2^(top + 1))
+            const int e = top + 1 - bias - static_cast<int>(M); // exponent of the leading bit
+            if(e >= -126)
+                return sign | (static_cast<uint32_t>(e + 127) << 23) | ((man << (23 - top)) & 0x7FFFFFu);
+            return sign | (man << (1 - bias - static_cast<int>(M) + 149)); // f32 subnormal, units of 2^-149
+        }
+        return sign | (static_cast<uint32_t>(static_cast<int>(ef) - bias + 127) << 23) | (man << (23 - M));
+    }
+
     // Fast f32 encoders, equal to floatEncode((double)f, E, M) on every f32 input
     // (checked exhaustively against the reference on the GPU, tests/test_gpu_codec.py).
     LAM_DEV uint32_t encode_e8m10_f32(uint32_t b)

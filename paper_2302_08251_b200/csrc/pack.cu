@@ -46,7 +46,7 @@ namespace lamk
             return lamd::encode_e8m10_f32(v);
         if(p.E == 5 && p.M == 10)
             return lamd::encode_e5m10_f32(v);
-        return static_cast<uint32_t>(lamd::float_encode(lamd::f32_to_f64_bits(v), p.E, p.M));
+        return static_cast<uint32_t>(lamd::float_encode_f32(v, p.E, p.M));
     }
 
     __device__ __forceinline__ uint32_t decode_value(const PackParams& p, uint32_t pat)
@@ -73,6 +73,8 @@ namespace lamk
                 return ((pat >> 15) << 31) | 0x7FC00000u;
             return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
         }
+        if(p.E <= 8 && p.M <= 23)
+            return lamd::float_decode_f32(pat, p.E, p.M);
         return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
     }
 
@@ -104,7 +106,7 @@ namespace lamk
         else if constexpr(FMT == 2)
             return lamd::encode_e5m10_f32(v);
         else
-            return static_cast<uint32_t>(lamd::float_encode(lamd::f32_to_f64_bits(v), p.E, p.M));
+            return static_cast<uint32_t>(lamd::float_encode_f32(v, p.E, p.M));
     }
 
     template<int FMT>
@@ -132,6 +134,8 @@ namespace lamk
                 return ((pat >> 15) << 31) | 0x7FC00000u;
             return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
         }
+        else if(p.E <= 8 && p.M <= 23)
+            return lamd::float_decode_f32(pat, p.E, p.M);
         else
             return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
     }

@@ -1,7 +1,8 @@
 """Exhaustive minifloat codec check on the GPU (SURVEY §7 "floatEncode parity").
 
-Every one of the 2^32 f32 bit patterns is packed to e8m10 and e5m10 through the fast path
-(register pack kernel, integer/half encoders) and through the generic interpreter
+Every one of the 2^32 f32 bit patterns is packed to e8m10, e5m10 and eight other (E, M)
+formats through the fast path (register pack kernel: TF32/half encoders for e8m10/e5m10, the
+32-bit float_encode_f32 / float_decode_f32 for the rest) and through the generic interpreter
 (integer-exact floatEncode restatement, bitpack.cpp:96-163); the packed streams must be
 identical, and so must the unpacked values.  A 2M-value random subset is compared with
 the reference library itself (oracle/_ref).
@@ -23,7 +24,7 @@ def _pair(fmt, n):
     return L, src, dst
 
 
-@pytest.mark.parametrize("fmt", ["8,10", "5,10"])
+@pytest.mark.parametrize("fmt", ["8,10", "5,10", "4,3", "5,2", "8,7", "6,9", "8,23", "3,0", "2,5", "11,20"])
 def test_all_f32_patterns_fast_equals_generic(fmt):
     import torch
     L, ls, ld = _pair(fmt, CHUNK)
