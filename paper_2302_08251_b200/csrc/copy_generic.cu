@@ -29,8 +29,8 @@ namespace lamk
 
     cudaError_t opt_in_smem(const void* func, size_t smem)
     {
-        if(smem <= 48 * 1024)
-            return cudaSuccess;
+        // set even below 48 KB: a kernel with static shared memory needs the attribute once
+        // static + dynamic passes 48 KB
         int dev = 0;
         cudaError_t e = cudaGetDevice(&dev);
         if(e != cudaSuccess)
@@ -39,7 +39,7 @@ namespace lamk
         static std::map<std::pair<const void*, int>, size_t> done; // (kernel, device) -> bytes set
         std::lock_guard<std::mutex> g(mu);
         size_t& have = done[{func, dev}];
-        if(have >= smem)
+        if(have >= smem && have != 0)
             return cudaSuccess;
         e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if(e == cudaSuccess)

@@ -745,7 +745,8 @@ namespace lamhost
         return lamk::rec_pack(q, kind, packDir, s);
     }
 
-    // K3/K4: every leaf 4-byte physical (SoA or AoSoA with 32 | L) <-> bit stream of width <= 32
+    // K3/K4: every leaf physical (SoA or AoSoA with 32 | L) <-> bit stream: 4-byte leaves with fields
+    // <= 32 bits through k_pack32/k_unpack32, 1/2/8-byte leaves and wider fields through packv.cu
     static bool tryPack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
                         const Lowered& S, const Lowered& D, cudaStream_t s)
     {
@@ -765,6 +766,7 @@ namespace lamhost
             return true;
         }
         std::vector<lamk::PackParams> jobs;
+        std::vector<std::pair<lamk::PackVParams, uint32_t>> vjobs; // other value sizes / wide fields
         bool packDir = false;
         for(uint32_t f = 0; f < p.nleaves; ++f)
         {
@@ -777,34 +779,57 @@ namespace lamhost
             const lamt_term& vt = pk ? L.s[0] : L.d[0];
             const lamt_stream& vs = p.st[vt.stream];
             const lamt_stream& bs = p.st[pk ? L.d[0].stream : L.s[0].stream];
-            if(vt.size != 4 || L.stype != L.ltype || L.dtype != L.ltype || L.ltype == Bool)
+            const uint32_t vsz = vt.size;
+            if((vsz != 1 && vsz != 2 && vsz != 4 && vsz != 8) || L.stype != L.ltype || L.dtype != L.ltype
+               || L.ltype == Bool)
                 return false;
-            const bool soa = vs.lanes == 1 && vs.bs == 4;
-            const bool aosoa = vs.lanes % 32 == 0 && vs.lshift != 0xFFFFFFFFu && vt.ls == 4;
+            const bool soa = vs.lanes == 1 && vs.bs == vsz;
+            const bool aosoa = vs.lanes % 32 == 0 && vs.lshift != 0xFFFFFFFFu && vt.ls == vsz;
             if(!(soa || aosoa))
                 return false;
-            lamk::PackParams j{};
             const uint8_t kind = pk ? L.dkind : L.skind;
-            j.kind = kind == LAMT_K_BITS_FLT ? 1 : 0;
-            j.E = pk ? L.dE : L.sE;
-            j.M = pk ? L.dM : L.sM;
-            j.w = j.kind ? 1 + j.E + j.M : j.E;
-            if(j.w < 1 || j.w > 32 || bs.bs != j.w)
+            const uint32_t kd = kind == LAMT_K_BITS_FLT ? 1 : 0;
+            const uint32_t E = pk ? L.dE : L.sE, M = pk ? L.dM : L.sM;
+            const uint32_t w = kd ? 1 + E + M : E;
+            if(w < 1 || w > 64 || bs.bs != w || (kd == 0 && w > 8 * vsz))
                 return false;
-            if(j.kind == 1 && L.ltype != F32)
+            if(kd == 1 && !((L.ltype == F32 && vsz == 4) || (L.ltype == F64 && vsz == 8)))
                 return false;
+            const uint64_t vals = vs.gptr + (soa ? vt.inblock : 0);
+            if((vals + (soa ? 0 : vt.inblock)) % 16 || bs.gptr % 16)
+                return false;
+            if(vsz != 4 || w > 32)
+            {
+                lamk::PackVParams v{};
+                v.vals = vals;
+                v.bits = bs.gptr;
+                v.begin = begin;
+                v.groups = groups;
+                v.w = w;
+                v.kind = kd;
+                v.sgn = pk ? 0 : L.ssigned;
+                v.E = E;
+                v.M = M;
+                v.vbs = vs.bs;
+                v.vl = vs.lanes;
+                v.vsh = soa ? 0 : vs.lshift;
+                v.vinb = soa ? 0 : vt.inblock;
+                vjobs.emplace_back(v, vsz);
+                continue;
+            }
+            lamk::PackParams j{};
+            j.kind = kd;
+            j.E = E;
+            j.M = M;
+            j.w = w;
             j.sgn = pk ? 0 : L.ssigned;
             j.valType = L.ltype;
-            j.vals = vs.gptr + (soa ? 0 : 0);
+            j.vals = vals;
             j.vinb = soa ? 0 : vt.inblock;
             j.vbs = vs.bs;
             j.vl = vs.lanes;
             j.vsh = soa ? 0 : vs.lshift;
-            if(soa)
-                j.vals += vt.inblock;
             j.bits = bs.gptr;
-            if((j.vals + (soa ? 0 : j.vinb)) % 16 || j.bits % 16)
-                return false;
             j.begin = begin;
             j.groups = groups;
             j.facS = 0; // counted in closed form below (fac_add)
@@ -815,6 +840,9 @@ namespace lamhost
             j.nleaves = p.nleaves;
             jobs.push_back(j);
         }
+        for(const auto& [v, vsz] : vjobs)
+            if(!lamk::packv(v, vsz, packDir, s))
+                throw std::runtime_error(std::string("packv launch failed: ") + cudaGetErrorString(cudaGetLastError()));
         for(const auto& j : jobs)
             if(!lamk::pack32(j, packDir, s))
                 throw std::runtime_error(std::string("pack32 launch failed: ") + cudaGetErrorString(cudaGetLastError()));

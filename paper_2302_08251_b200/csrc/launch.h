@@ -16,10 +16,26 @@ namespace lamk
     void count_launch(uint64_t n = 1);
     uint64_t launch_count();
 
+    // bit packing for 1/2/8-byte leaves and fields wider than 32 bits (packv.cu)
+    struct PackVParams
+    {
+        unsigned long long vals;   // value stream (element 0's value, SoA) or AoSoA block base
+        unsigned long long bits;   // bit stream (word 0 = element 0)
+        unsigned long long begin;  // first element (multiple of 32)
+        unsigned long long groups; // groups of 32 elements
+        uint32_t w;                // field width, 1..64
+        uint32_t kind;             // 0 int, 1 float
+        uint32_t sgn;              // int: sign-extend on unpack
+        uint32_t E, M;             // float format
+        uint32_t vbs, vl, vsh, vinb; // value stream geometry: SoA (vl == 1) or AoSoA (vl % 32 == 0)
+    };
+
+    bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s);
+
     int sm_count(int device);
 
     // Opt `func` in to `smem` bytes of dynamic shared memory on the CURRENT device.  The
-    // attribute is per device, so it is tracked per (kernel, device); no-op up to 48 KB.
+    // attribute is per device, so it is tracked per (kernel, device).
     cudaError_t opt_in_smem(const void* func, size_t smem);
 
     // Grid for a grid-stride streaming kernel: `want` CTAs (one pass of the data), capped at

@@ -1,0 +1,315 @@
+// Bit packing for value sizes other than the 32-bit fast path (pack.cu k_pack32 /
+// k_unpack32): 1-, 2- and 8-byte leaves (BitpackIntSoA on i8/u8/i16/u16/i64/u64 leaves,
+// BitpackFloatSoA on f64 leaves, computed.cpp:48-222) and 4-byte leaves whose field is wider
+// than 32 bits (e.g. bitpack-float:11,30 on f32).  Same ownership rule as k_pack32: a thread
+// owns 32 consecutive values = w whole 32-bit words of the stream (w = field width, 1..64), so
+// no word is shared and no read-modify-write is needed (bitpack.hpp:16-17).  The warp's 1024
+// values move as coalesced 16-byte chunks through a padded shared-memory row per lane (row
+// stride 2*VS+1 chunks: conflict-free both ways), the words through an odd-stride word slice
+// that aliases it, then leave as coalesced 32-bit stores.
+//   encode: integers keep the low w bits (packInt, bitpack.cpp:72-80); f32 -> float_encode_f32,
+//           f64 -> float_encode (floatEncode, bitpack.cpp:96-163)
+//   decode: zero/sign extension to the leaf width (unpackUnsigned/Signed, bitpack.cpp:82-94);
+//           floatDecode -> the leaf's float type (bitpack.cpp:165-188)
+#include "device_common.cuh"
+#include "launch.h"
+
+namespace lamk
+{
+    namespace
+    {
+        template<int VS>
+        __device__ __forceinline__ uint64_t vaddr(const PackVParams& p, uint64_t e)
+        {
+            if(p.vl == 1)
+                return p.vals + e * VS;
+            return p.vals + (e >> p.vsh) * p.vbs + p.vinb + (e & (p.vl - 1)) * VS;
+        }
+
+        template<int VS>
+        __device__ __forceinline__ uint64_t enc(const PackVParams& p, uint64_t v)
+        {
+            if(p.kind == 0)
+                return v & lamd::low_mask(p.w);
+            if constexpr(VS == 4)
+                return lamd::float_encode_f32(static_cast<uint32_t>(v), p.E, p.M);
+            else
+                return lamd::float_encode(v, p.E, p.M);
+        }
+
+        template<int VS>
+        __device__ __forceinline__ uint64_t dec(const PackVParams& p, uint64_t pat)
+        {
+            if(p.kind == 0)
+            {
+                if(p.sgn && p.w < 64)
+                {
+                    const uint64_t s = 1ull << (p.w - 1);
+                    pat = (pat ^ s) - s;
+                }
+                return pat & lamd::low_mask(8 * VS);
+            }
+            if constexpr(VS == 4)
+            {
+                if(p.E <= 8 && p.M <= 23)
+                    return lamd::float_decode_f32(static_cast<uint32_t>(pat), p.E, p.M);
+                return lamd::f64_to_f32_bits(lamd::float_decode(pat, p.E, p.M));
+            }
+            else
+                return lamd::float_decode(pat, p.E, p.M);
+        }
+
+        // row of lane r: 32 values (32*VS bytes) + 16 bytes of padding
+        template<int VS>
+        __host__ __device__ constexpr uint32_t row_words()
+        {
+            return 8 * VS + 4;
+        }
+        template<int VS>
+        __host__ __device__ constexpr uint32_t warp_words()
+        {
+            return 32 * row_words<VS>() > 32 * 65 ? 32 * row_words<VS>() : 32 * 65;
+        }
+
+        // value chunks (16 B) of the warp's span <-> rows: chunk c = row c / (2VS), column c % (2VS)
+        template<int VS>
+        __device__ __forceinline__ void g2s(const PackVParams& p, uint32_t* sm, uint64_t e0, uint32_t lane, uint32_t live)
+        {
+            constexpr uint32_t CPR = 2 * VS; // chunks per row
+            const uint32_t chunks = live * CPR;
+            if(live == 32)
+            {
+                uint4 x[CPR];
+#pragma unroll
+                for(uint32_t k = 0; k < CPR; ++k)
+                    x[k] = __ldcs(reinterpret_cast<const uint4*>(vaddr<VS>(p, e0 + (lane + 32 * k) * 16 / VS)));
+#pragma unroll
+                for(uint32_t k = 0; k < CPR; ++k)
+                {
+                    const uint32_t c = lane + 32 * k;
+                    *reinterpret_cast<uint4*>(sm + (c / CPR) * row_words<VS>() + (c % CPR) * 4) = x[k];
+                }
+                return;
+            }
+            for(uint32_t c = lane; c < chunks; c += 32)
+                *reinterpret_cast<uint4*>(sm + (c / CPR) * row_words<VS>() + (c % CPR) * 4)
+                    = __ldcs(reinterpret_cast<const uint4*>(vaddr<VS>(p, e0 + c * 16 / VS)));
+        }
+
+        template<int VS>
+        __device__ __forceinline__ void s2g(const PackVParams& p, const uint32_t* sm, uint64_t e0, uint32_t lane,
+                                            uint32_t live)
+        {
+            constexpr uint32_t CPR = 2 * VS;
+            const uint32_t chunks = live * CPR;
+            for(uint32_t c = lane; c < chunks; c += 32)
+                __stcs(reinterpret_cast<uint4*>(vaddr<VS>(p, e0 + c * 16 / VS)),
+                       *reinterpret_cast<const uint4*>(sm + (c / CPR) * row_words<VS>() + (c % CPR) * 4));
+        }
+
+        // value i of a row held as 8*VS words
+        template<int VS>
+        __device__ __forceinline__ uint64_t value_of(const uint32_t* wd, int i)
+        {
+            if constexpr(VS == 1)
+                return (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+            else if constexpr(VS == 2)
+                return (wd[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+            else if constexpr(VS == 4)
+                return wd[i];
+            else
+                return static_cast<uint64_t>(wd[2 * i]) | (static_cast<uint64_t>(wd[2 * i + 1]) << 32);
+        }
+    } // namespace
+
+    template<int VS>
+    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_packv(const __grid_constant__ PackVParams p)
+    {
+        extern __shared__ __align__(16) uint32_t vsm[];
+        const uint32_t lane = threadIdx.x & 31, w = p.w, ws = w | 1u;
+        uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32;
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const uint64_t warpG = g - lane;
+            const uint32_t live =
+                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint64_t e0 = p.begin + warpG * 32;
+            g2s<VS>(p, sm, e0, lane, live);
+            __syncwarp();
+            uint32_t wd[8 * VS];
+            const bool mine = g < p.groups;
+            if(mine)
+            {
+#pragma unroll
+                for(int q = 0; q < 2 * VS; ++q)
+                {
+                    const uint4 x = *reinterpret_cast<const uint4*>(sm + lane * row_words<VS>() + 4 * q);
+                    wd[4 * q] = x.x;
+                    wd[4 * q + 1] = x.y;
+                    wd[4 * q + 2] = x.z;
+                    wd[4 * q + 3] = x.w;
+                }
+            }
+            __syncwarp(); // rows consumed: the word slice (aliasing them) may be written
+            if(mine)
+            {
+                uint32_t* my = sm + lane * ws;
+                unsigned long long acc = 0;
+                uint32_t nb = 0, k = 0;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    const uint64_t e = enc<VS>(p, value_of<VS>(wd, i));
+                    if(w <= 32)
+                    {
+                        acc |= e << nb;
+                        nb += w;
+                        if(nb >= 32)
+                        {
+                            my[k++] = static_cast<uint32_t>(acc);
+                            acc >>= 32;
+                            nb -= 32;
+                        }
+                    }
+                    else
+                    {
+                        acc |= (e & 0xFFFFFFFFull) << nb;
+                        my[k++] = static_cast<uint32_t>(acc);
+                        acc >>= 32;
+                        acc |= (e >> 32) << nb;
+                        nb += w - 32;
+                        if(nb >= 32)
+                        {
+                            my[k++] = static_cast<uint32_t>(acc);
+                            acc >>= 32;
+                            nb -= 32;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + e0 / 32 * w;
+            for(uint32_t q = lane; q < live * w; q += 32)
+                __stcs(dst + q, sm[(q / w) * ws + (q % w)]);
+            __syncwarp();
+        }
+    }
+
+    template<int VS>
+    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_unpackv(const __grid_constant__ PackVParams p)
+    {
+        extern __shared__ __align__(16) uint32_t vsm[];
+        const uint32_t lane = threadIdx.x & 31, w = p.w, ws = w | 1u;
+        uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32;
+        const uint64_t mask = lamd::low_mask(w);
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const uint64_t warpG = g - lane;
+            const uint32_t live =
+                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint64_t e0 = p.begin + warpG * 32;
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bits) + e0 / 32 * w;
+            for(uint32_t q = lane; q < live * w; q += 32)
+                sm[(q / w) * ws + (q % w)] = __ldcs(src + q);
+            __syncwarp();
+            uint32_t wd[8 * VS];
+            const bool mine = g < p.groups;
+            if(mine)
+            {
+                const uint32_t* my = sm + lane * ws;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    const uint32_t bit = static_cast<uint32_t>(i) * w, k = bit >> 5, sh = bit & 31;
+                    uint64_t pat = static_cast<uint64_t>(my[k]) >> sh;
+                    if(sh + w > 32)
+                        pat |= static_cast<uint64_t>(my[k + 1]) << (32 - sh);
+                    if(sh + w > 64)
+                        pat |= static_cast<uint64_t>(my[k + 2]) << (64 - sh);
+                    const uint64_t v = dec<VS>(p, pat & mask);
+                    if constexpr(VS == 1)
+                    {
+                        if((i & 3) == 0)
+                            wd[i >> 2] = 0;
+                        wd[i >> 2] |= static_cast<uint32_t>(v) << (8 * (i & 3));
+                    }
+                    else if constexpr(VS == 2)
+                    {
+                        if((i & 1) == 0)
+                            wd[i >> 1] = 0;
+                        wd[i >> 1] |= static_cast<uint32_t>(v) << (16 * (i & 1));
+                    }
+                    else if constexpr(VS == 4)
+                        wd[i] = static_cast<uint32_t>(v);
+                    else
+                    {
+                        wd[2 * i] = static_cast<uint32_t>(v);
+                        wd[2 * i + 1] = static_cast<uint32_t>(v >> 32);
+                    }
+                }
+            }
+            __syncwarp(); // words consumed: rows (aliasing them) may be written
+            if(mine)
+            {
+#pragma unroll
+                for(int q = 0; q < 2 * VS; ++q)
+                    *reinterpret_cast<uint4*>(sm + lane * row_words<VS>() + 4 * q)
+                        = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
+            }
+            __syncwarp();
+            s2g<VS>(p, sm, e0, lane, live);
+            __syncwarp();
+        }
+    }
+
+    template<int VS>
+    static void launch_v(const PackVParams& p, bool pack, cudaStream_t s)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const size_t smem = 8 * warp_words<VS>() * sizeof(uint32_t);
+        const void* fn = pack ? reinterpret_cast<const void*>(k_packv<VS>) : reinterpret_cast<const void*>(k_unpackv<VS>);
+        lam_cuda_check(opt_in_smem(fn, smem), "opt_in_smem");
+        int occ = 0;
+        if(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pack ? k_packv<VS> : k_unpackv<VS>, 256, smem) != cudaSuccess
+           || occ < 1)
+            occ = 1;
+        const uint64_t want = (p.groups + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * occ * 4;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        if(pack)
+            k_packv<VS><<<grid, 256, smem, s>>>(p);
+        else
+            k_unpackv<VS><<<grid, 256, smem, s>>>(p);
+    }
+
+    bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s)
+    {
+        if(p.groups == 0 || p.w < 1 || p.w > 64 || (p.kind == 0 && p.w > 8 * vsize))
+            return false;
+        switch(vsize)
+        {
+        case 1:
+            launch_v<1>(p, pack, s);
+            break;
+        case 2:
+            launch_v<2>(p, pack, s);
+            break;
+        case 4:
+            launch_v<4>(p, pack, s);
+            break;
+        case 8:
+            launch_v<8>(p, pack, s);
+            break;
+        default:
+            return false;
+        }
+        count_launch();
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
+    }
+} // namespace lamk
