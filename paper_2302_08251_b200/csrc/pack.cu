@@ -213,7 +213,7 @@ namespace lamk
     // W from 10 to 30 but 16); a (256, 4) bound on e8m10 had cost it 17% (profiles/README.md)
     __host__ __device__ constexpr int pack_minb(int W, int FMT)
     {
-        return (FMT == 0 && W >= 10 && W % 2 == 0 && W != 16 && W != 32) ? 2 : 3;
+        return (FMT == 0 && W >= 10 && W % 2 == 0 && W != 16 && W != 32) || (FMT == 3 && W != 0) ? 2 : 3;
     }
 
     template<int W, int FMT>
@@ -800,6 +800,16 @@ namespace lamk
         return hit;
     }
 
+    // any other (E, M) with 1 + E + M <= 32: compile-time width, runtime format
+    template<int... Ws>
+    static bool dispatch_flt(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+                             std::integer_sequence<int, Ws...>)
+    {
+        bool hit = false;
+        ((w == Ws + 2 ? (launch_pack<Ws + 2, 3>(p, pack, grid, smem, s), hit = true) : false), ...);
+        return hit;
+    }
+
     bool pack32(const PackParams& p, bool pack, cudaStream_t s)
     {
         if(p.groups == 0 || p.w < 1 || p.w > 32)
@@ -815,7 +825,7 @@ namespace lamk
             launch_pack<19, 1>(p, pack, grid, smem, s);
         else if(p.E == 5 && p.M == 10)
             launch_pack<16, 2>(p, pack, grid, smem, s);
-        else
+        else if(!dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
             launch_pack<0, 3>(p, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");

@@ -107,6 +107,30 @@ namespace lamk
                        *reinterpret_cast<const uint4*>(sm + (c / CPR) * row_words<VS>() + (c % CPR) * 4));
         }
 
+        // word q = lane + 32k of the warp's span lives in row q / w, column q % w of the word
+        // slice (row stride ws); walked incrementally, no division in the loop
+        struct WordWalk
+        {
+            uint32_t r, c, dr, dc, w;
+            __device__ __forceinline__ WordWalk(uint32_t lane, uint32_t w_) : w(w_)
+            {
+                r = lane / w;
+                c = lane - r * w;
+                dr = 32 / w;
+                dc = 32 - dr * w;
+            }
+            __device__ __forceinline__ void next()
+            {
+                r += dr;
+                c += dc;
+                if(c >= w)
+                {
+                    c -= w;
+                    ++r;
+                }
+            }
+        };
+
         // value i of a row held as 8*VS words
         template<int VS>
         __device__ __forceinline__ uint64_t value_of(const uint32_t* wd, int i)
@@ -162,7 +186,7 @@ namespace lamk
                 for(int i = 0; i < 32; ++i)
                 {
                     const uint64_t e = enc<VS>(p, value_of<VS>(wd, i));
-                    if(w <= 32)
+                    if(VS <= 2 || w <= 32)
                     {
                         acc |= e << nb;
                         nb += w;
@@ -191,8 +215,9 @@ namespace lamk
             }
             __syncwarp();
             uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + e0 / 32 * w;
-            for(uint32_t q = lane; q < live * w; q += 32)
-                __stcs(dst + q, sm[(q / w) * ws + (q % w)]);
+            WordWalk ww(lane, w);
+            for(uint32_t q = lane; q < live * w; q += 32, ww.next())
+                __stcs(dst + q, sm[ww.r * ws + ww.c]);
             __syncwarp();
         }
     }
@@ -213,24 +238,58 @@ namespace lamk
                 static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
             const uint64_t e0 = p.begin + warpG * 32;
             const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bits) + e0 / 32 * w;
-            for(uint32_t q = lane; q < live * w; q += 32)
-                sm[(q / w) * ws + (q % w)] = __ldcs(src + q);
+            {
+                WordWalk ww(lane, w);
+                for(uint32_t q = lane; q < live * w; q += 32, ww.next())
+                    sm[ww.r * ws + ww.c] = __ldcs(src + q);
+            }
             __syncwarp();
             uint32_t wd[8 * VS];
             const bool mine = g < p.groups;
             if(mine)
             {
                 const uint32_t* my = sm + lane * ws;
+                // stream the lane's words through a 64-bit window: at most one word refill per
+                // value for w <= 32, two for wider fields
+                unsigned long long acc = 0;
+                uint32_t nb = 0, k = 0;
 #pragma unroll
                 for(int i = 0; i < 32; ++i)
                 {
-                    const uint32_t bit = static_cast<uint32_t>(i) * w, k = bit >> 5, sh = bit & 31;
-                    uint64_t pat = static_cast<uint64_t>(my[k]) >> sh;
-                    if(sh + w > 32)
-                        pat |= static_cast<uint64_t>(my[k + 1]) << (32 - sh);
-                    if(sh + w > 64)
-                        pat |= static_cast<uint64_t>(my[k + 2]) << (64 - sh);
-                    const uint64_t v = dec<VS>(p, pat & mask);
+                    uint64_t pat;
+                    if(VS <= 2 || w <= 32)
+                    {
+                        if(nb < w)
+                        {
+                            acc |= static_cast<unsigned long long>(my[k++]) << nb;
+                            nb += 32;
+                        }
+                        pat = acc & mask;
+                        acc >>= w;
+                        nb -= w;
+                    }
+                    else
+                    {
+                        // w in (32, 64]: low 32 bits, then the remaining w - 32
+                        if(nb < 32)
+                        {
+                            acc |= static_cast<unsigned long long>(my[k++]) << nb;
+                            nb += 32;
+                        }
+                        pat = acc & 0xFFFFFFFFull;
+                        acc >>= 32;
+                        nb -= 32;
+                        const uint32_t hw = w - 32;
+                        if(nb < hw)
+                        {
+                            acc |= static_cast<unsigned long long>(my[k++]) << nb;
+                            nb += 32;
+                        }
+                        pat |= (acc & lamd::low_mask(hw)) << 32;
+                        acc >>= hw;
+                        nb -= hw;
+                    }
+                    const uint64_t v = dec<VS>(p, pat);
                     if constexpr(VS == 1)
                     {
                         if((i & 3) == 0)
