@@ -252,8 +252,11 @@ namespace lamd
         const int bias = (1 << (E - 1)) - 1;
         if(static_cast<int>(a >> 23) - 127 + bias >= 1)
         {
+            // the parity for ties-to-even is the LSB of the rounded significand: mantissa bit
+            // 23 - M, or -- at M = 0, where only the implicit 1 remains -- always odd
             const uint32_t sh = 23 - M;
-            const uint32_t r = sh ? a + ((1u << (sh - 1)) - 1u) + ((a >> sh) & 1u) : a;
+            const uint32_t lsb = M ? (a >> sh) & 1u : 1u;
+            const uint32_t r = sh ? a + ((1u << (sh - 1)) - 1u) + lsb : a;
             const int e = static_cast<int>(r >> 23) - 127 + bias;
             if(e >= static_cast<int>(maxExp))
                 return inf;
