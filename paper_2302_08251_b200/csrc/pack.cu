@@ -95,7 +95,8 @@ namespace lamk
 
     // Compile-time field width: the 32 values of a thread map to exactly W words, and the
     // word boundaries fall at compile-time positions, so packing is pure shift/or chains.
-    // FMT: 0 integer, 1 f32 e8m10 (W=19), 2 f32 e5m10 (W=16), 3 any float (runtime E, M).
+    // FMT: 0 integer, 1 f32 e8m10 (W=19), 2 f32 e5m10 (W=16), 3 any f32 format with E <= 8,
+    // M <= 23 (runtime E, M; the 32-bit codec), 4 any float format (runtime E, M).
     template<int FMT>
     __device__ __forceinline__ uint32_t enc_t(const PackParams& p, uint32_t v, uint32_t mask)
     {
@@ -105,6 +106,8 @@ namespace lamk
             return lamd::encode_e8m10_f32(v);
         else if constexpr(FMT == 2)
             return lamd::encode_e5m10_f32(v);
+        else if constexpr(FMT == 3)
+            return lamd::float_encode_f32_small(v, p.E, p.M);
         else
             return static_cast<uint32_t>(lamd::float_encode_f32(v, p.E, p.M));
     }
@@ -134,6 +137,8 @@ namespace lamk
                 return ((pat >> 15) << 31) | 0x7FC00000u;
             return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
         }
+        else if constexpr(FMT == 3)
+            return lamd::float_decode_f32(pat, p.E, p.M);
         else if(p.E <= 8 && p.M <= 23)
             return lamd::float_decode_f32(pat, p.E, p.M);
         else
@@ -759,7 +764,7 @@ namespace lamk
         else if(q.E == 5 && q.M == 10)
             launch_rec<16, 2>(q, pack, grid, smem, s);
         else
-            launch_rec<0, 3>(q, pack, grid, smem, s);
+            launch_rec<0, 4>(q, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");
         return true;
@@ -825,8 +830,9 @@ namespace lamk
             launch_pack<19, 1>(p, pack, grid, smem, s);
         else if(p.E == 5 && p.M == 10)
             launch_pack<16, 2>(p, pack, grid, smem, s);
-        else if(!dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
-            launch_pack<0, 3>(p, pack, grid, smem, s);
+        else if(p.E > 8 || p.M > 23
+                || !dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
+            launch_pack<0, 4>(p, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");
         return true;

@@ -14,6 +14,8 @@
 #include "device_common.cuh"
 #include "launch.h"
 
+#include <utility>
+
 namespace lamk
 {
     namespace
@@ -146,11 +148,13 @@ namespace lamk
         }
     } // namespace
 
-    template<int VS>
+    // W != 0: compile-time field width of an integer leaf of 1 or 2 bytes (word boundaries at
+    // compile-time positions: pure shift/or chains, as k_pack32); W == 0: runtime width / float
+    template<int VS, int W = 0>
     __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_packv(const __grid_constant__ PackVParams p)
     {
         extern __shared__ __align__(16) uint32_t vsm[];
-        const uint32_t lane = threadIdx.x & 31, w = p.w, ws = w | 1u;
+        const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
@@ -177,7 +181,29 @@ namespace lamk
                 }
             }
             __syncwarp(); // rows consumed: the word slice (aliasing them) may be written
-            if(mine)
+            if(mine && W != 0)
+            {
+                uint32_t* my = sm + lane * ws;
+                constexpr uint32_t mask = W >= 32 ? 0xFFFFFFFFu : (1u << (W ? W : 1)) - 1u;
+                uint32_t e[32];
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                    e[i] = static_cast<uint32_t>(value_of<VS>(wd, i)) & mask;
+                // word k = bits [32k, 32k+32): values floor(32k/W) .. floor((32k+31)/W)
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    uint32_t word = 0;
+#pragma unroll
+                    for(int i = (32 * k) / (W ? W : 1); i <= (32 * k + 31) / (W ? W : 1) && i < 32; ++i)
+                    {
+                        const int pos = i * W - 32 * k;
+                        word |= pos >= 0 ? e[i] << pos : e[i] >> (-pos);
+                    }
+                    my[k] = word;
+                }
+            }
+            else if(mine)
             {
                 uint32_t* my = sm + lane * ws;
                 unsigned long long acc = 0;
@@ -215,18 +241,30 @@ namespace lamk
             }
             __syncwarp();
             uint32_t* dst = reinterpret_cast<uint32_t*>(p.bits) + e0 / 32 * w;
-            WordWalk ww(lane, w);
-            for(uint32_t q = lane; q < live * w; q += 32, ww.next())
-                __stcs(dst + q, sm[ww.r * ws + ww.c]);
+            if(W != 0 && live == 32)
+            {
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t q = lane + 32 * k;
+                    __stcs(dst + q, sm[(q / w) * ws + (q % w)]);
+                }
+            }
+            else
+            {
+                WordWalk ww(lane, w);
+                for(uint32_t q = lane; q < live * w; q += 32, ww.next())
+                    __stcs(dst + q, sm[ww.r * ws + ww.c]);
+            }
             __syncwarp();
         }
     }
 
-    template<int VS>
+    template<int VS, int W = 0>
     __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_unpackv(const __grid_constant__ PackVParams p)
     {
         extern __shared__ __align__(16) uint32_t vsm[];
-        const uint32_t lane = threadIdx.x & 31, w = p.w, ws = w | 1u;
+        const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
@@ -238,6 +276,20 @@ namespace lamk
                 static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
             const uint64_t e0 = p.begin + warpG * 32;
             const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bits) + e0 / 32 * w;
+            if(W != 0 && live == 32)
+            {
+                uint32_t t[W ? W : 1];
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                    t[k] = __ldcs(src + lane + 32 * k);
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t q = lane + 32 * k;
+                    sm[(q / w) * ws + (q % w)] = t[k];
+                }
+            }
+            else
             {
                 WordWalk ww(lane, w);
                 for(uint32_t q = lane; q < live * w; q += 32, ww.next())
@@ -246,7 +298,43 @@ namespace lamk
             __syncwarp();
             uint32_t wd[8 * VS];
             const bool mine = g < p.groups;
-            if(mine)
+            if(mine && W != 0)
+            {
+                const uint32_t* my = sm + lane * ws;
+                uint32_t wds[W ? W : 1];
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                    wds[k] = my[k];
+                constexpr uint32_t mask = W >= 32 ? 0xFFFFFFFFu : (1u << (W ? W : 1)) - 1u;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                {
+                    const int bit = i * W, k = bit >> 5, sh = bit & 31;
+                    uint32_t pat = wds[k] >> sh;
+                    if(sh + W > 32)
+                        pat |= wds[k + 1] << (32 - sh);
+                    pat &= mask;
+                    if(p.sgn && W < 32)
+                    {
+                        const uint32_t sb = 1u << (W - 1);
+                        pat = (pat ^ sb) - sb;
+                    }
+                    const uint32_t v = VS == 1 ? pat & 0xFFu : pat & 0xFFFFu;
+                    if constexpr(VS == 1)
+                    {
+                        if((i & 3) == 0)
+                            wd[i >> 2] = 0;
+                        wd[i >> 2] |= v << (8 * (i & 3));
+                    }
+                    else
+                    {
+                        if((i & 1) == 0)
+                            wd[i >> 1] = 0;
+                        wd[i >> 1] |= v << (16 * (i & 1));
+                    }
+                }
+            }
+            else if(mine)
             {
                 const uint32_t* my = sm + lane * ws;
                 // stream the lane's words through a 64-bit window: at most one word refill per
@@ -325,25 +413,30 @@ namespace lamk
         }
     }
 
-    template<int VS>
+    template<int VS, int W = 0>
     static void launch_v(const PackVParams& p, bool pack, cudaStream_t s)
     {
         int dev = 0;
         cudaGetDevice(&dev);
         const size_t smem = 8 * warp_words<VS>() * sizeof(uint32_t);
-        const void* fn = pack ? reinterpret_cast<const void*>(k_packv<VS>) : reinterpret_cast<const void*>(k_unpackv<VS>);
-        lam_cuda_check(opt_in_smem(fn, smem), "opt_in_smem");
+        auto kern = pack ? k_packv<VS, W> : k_unpackv<VS, W>;
+        lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(kern), smem), "opt_in_smem");
         int occ = 0;
-        if(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pack ? k_packv<VS> : k_unpackv<VS>, 256, smem) != cudaSuccess
-           || occ < 1)
+        if(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem) != cudaSuccess || occ < 1)
             occ = 1;
         const uint64_t want = (p.groups + 255) / 256;
         const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * occ * 4;
         const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-        if(pack)
-            k_packv<VS><<<grid, 256, smem, s>>>(p);
-        else
-            k_unpackv<VS><<<grid, 256, smem, s>>>(p);
+        kern<<<grid, 256, smem, s>>>(p);
+    }
+
+    // integer leaves of 1 / 2 bytes: a compile-time width per kernel
+    template<int VS, int... Ws>
+    static bool dispatch_narrow(const PackVParams& p, bool pack, cudaStream_t s, std::integer_sequence<int, Ws...>)
+    {
+        bool hit = false;
+        ((static_cast<int>(p.w) == Ws + 1 ? (launch_v<VS, Ws + 1>(p, pack, s), hit = true) : false), ...);
+        return hit;
     }
 
     bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s)
@@ -353,10 +446,12 @@ namespace lamk
         switch(vsize)
         {
         case 1:
-            launch_v<1>(p, pack, s);
+            if(p.kind != 0 || !dispatch_narrow<1>(p, pack, s, std::make_integer_sequence<int, 8>{}))
+                launch_v<1>(p, pack, s);
             break;
         case 2:
-            launch_v<2>(p, pack, s);
+            if(p.kind != 0 || !dispatch_narrow<2>(p, pack, s, std::make_integer_sequence<int, 16>{}))
+                launch_v<2>(p, pack, s);
             break;
         case 4:
             launch_v<4>(p, pack, s);
