@@ -293,6 +293,12 @@ namespace lamk
         return q;
     }
 
+    // the same count on the host (pattern tables): exact integer floor division
+    static int64_t floor_div_h(int64_t a, int64_t b)
+    {
+        return a >= 0 ? a / b : -((-a + b - 1) / b);
+    }
+
     __global__ void __launch_bounds__(256) k_heat_closed(const __grid_constant__ HeatParams p)
     {
         const HeatStream& st = p.st[blockIdx.y];
@@ -302,6 +308,8 @@ namespace lamk
         const int64_t last = floor_div_r(b0 + static_cast<int64_t>(p.end) * bs - 1, g, invg);
         const int64_t eb = static_cast<int64_t>(p.begin), ee = static_cast<int64_t>(p.end) - 1;
         unsigned long long* heat = p.heat + p.heatOff[st.nr];
+        const int64_t P = st.period;
+        const double invP = P ? 1.0 / static_cast<double>(P) : 0.0;
         // HEAT_K consecutive counters per thread: their read-modify-writes are independent, so all
         // HEAT_K loads are in flight together (one 8-byte RMW per thread left the pass latency-bound
         // at ~2 TB/s of counter traffic)
@@ -310,6 +318,14 @@ namespace lamk
             bq += static_cast<int64_t>(gridDim.x) * blockDim.x * HEAT_K)
         {
             unsigned long long c[HEAT_K], h[HEAT_K];
+            // interior blocks: the periodic pattern (one modulo per thread, then increments)
+            int64_t m = 0;
+            const bool inner = P != 0 && bq >= st.pLo && bq + HEAT_K - 1 <= st.pHi;
+            if(inner)
+            {
+                m = bq - st.pb0;
+                m -= floor_div_r(m, P, invP) * P;
+            }
 #pragma unroll
             for(int k = 0; k < HEAT_K; ++k)
             {
@@ -317,6 +333,12 @@ namespace lamk
                 c[k] = 0;
                 if(b > last)
                     continue;
+                if(inner)
+                {
+                    c[k] = p.pattern[st.patOff + m];
+                    m = m + 1 == P ? 0 : m + 1;
+                    continue;
+                }
                 for(uint32_t t = st.t0; t < st.t1; ++t)
                 {
                     const HeatTerm& ht = p.term[t];
@@ -363,8 +385,54 @@ namespace lamk
         }
         if(closed && p.end > p.begin)
         {
+            // interior pattern per stream (P = bs / gcd(g, bs) blocks), computed with the kernel's
+            // formula; blocks within ceil(bs / g) + 2 of either end stay exact
+            HeatParams q = p;
+            uint32_t used = 0;
+            const int64_t g = static_cast<int64_t>(p.gran);
+            for(uint32_t k = 0; k < q.nstreams; ++k)
+            {
+                HeatStream& st = q.st[k];
+                st.period = 0;
+                const int64_t bs = static_cast<int64_t>(st.bs), b0 = static_cast<int64_t>(st.base0);
+                int64_t a = g, bb = bs;
+                while(bb)
+                {
+                    const int64_t t = a % bb;
+                    a = bb;
+                    bb = t;
+                }
+                const int64_t P = bs / a;
+                const int64_t first = floor_div_h(b0 + static_cast<int64_t>(p.begin) * bs, g);
+                const int64_t last = floor_div_h(b0 + static_cast<int64_t>(p.end) * bs - 1, g);
+                const int64_t D = (bs + g - 1) / g + 2;
+                if(P < 1 || used + P > sizeof(q.pattern) / sizeof(q.pattern[0]) || last - first + 1 < 2 * D + P
+                   || std::getenv("LAMB_HEAT_PATTERN") && std::getenv("LAMB_HEAT_PATTERN")[0] == '0')
+                    continue;
+                st.pb0 = first + D;
+                st.pLo = first + D;
+                st.pHi = last - D;
+                st.period = static_cast<uint32_t>(P);
+                st.patOff = used;
+                for(int64_t j = 0; j < P; ++j)
+                {
+                    const int64_t b = st.pb0 + j;
+                    uint64_t cnt = 0;
+                    for(uint32_t t = st.t0; t < st.t1; ++t)
+                    {
+                        const HeatTerm& ht = q.term[t];
+                        const int64_t off = b0 + ht.inblock;
+                        const int64_t lo = floor_div_h(b * g - off - static_cast<int64_t>(ht.size), bs) + 1;
+                        const int64_t hi = floor_div_h((b + 1) * g - off - 1, bs);
+                        if(hi >= lo)
+                            cnt += static_cast<uint64_t>(hi - lo + 1);
+                    }
+                    q.pattern[used + j] = static_cast<uint32_t>(cnt);
+                }
+                used += static_cast<uint32_t>(P);
+            }
             const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 0);
-            k_heat_closed<<<dim3(gx, p.nstreams), 256, 0, s>>>(p);
+            k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();
             return cudaGetLastError();
         }

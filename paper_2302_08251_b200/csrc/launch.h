@@ -62,6 +62,10 @@ namespace lamk
     {
         uint64_t base0, bs, lanes;
         uint32_t lshift, nr, t0, t1; // terms [t0, t1) live on this stream
+        // closed form, interior blocks: the counts repeat with period P = bs / gcd(g, bs) blocks;
+        // pattern[patOff + k] is the count of block pb0 + k (P = 0: no pattern, exact per block)
+        int64_t pb0, pLo, pHi;       // pattern origin and the interior block range [pLo, pHi]
+        uint32_t period, patOff;
     };
     struct HeatParams
     {
@@ -72,6 +76,7 @@ namespace lamk
         uint32_t nstreams, maxWindow;
         HeatStream st[64];
         HeatTerm term[256];
+        uint32_t pattern[2048];
     };
     cudaError_t heat_phys(const HeatParams& p, cudaStream_t s);
 

@@ -98,6 +98,26 @@ namespace lamk
                     = __ldcs(reinterpret_cast<const uint4*>(vaddr<VS>(p, e0 + c * 16 / VS)));
         }
 
+        // full-warp value span in two halves, so the next span's loads can be issued before the
+        // current one is processed: global -> registers, registers -> rows
+        template<int VS>
+        __device__ __forceinline__ void g2r(const PackVParams& p, uint4 (&x)[2 * VS], uint64_t e0, uint32_t lane)
+        {
+#pragma unroll
+            for(uint32_t k = 0; k < 2 * VS; ++k)
+                x[k] = __ldcs(reinterpret_cast<const uint4*>(vaddr<VS>(p, e0 + (lane + 32 * k) * 16 / VS)));
+        }
+        template<int VS>
+        __device__ __forceinline__ void r2s(uint32_t* sm, const uint4 (&x)[2 * VS], uint32_t lane)
+        {
+#pragma unroll
+            for(uint32_t k = 0; k < 2 * VS; ++k)
+            {
+                const uint32_t c = lane + 32 * k;
+                *reinterpret_cast<uint4*>(sm + (c / (2 * VS)) * row_words<VS>() + (c % (2 * VS)) * 4) = x[k];
+            }
+        }
+
         template<int VS>
         __device__ __forceinline__ void s2g(const PackVParams& p, const uint32_t* sm, uint64_t e0, uint32_t lane,
                                             uint32_t live)
@@ -158,13 +178,32 @@ namespace lamk
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
-        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        auto liveOf = [&](uint64_t warpG) -> uint32_t
+        {
+            return static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+        };
+        // software pipeline: the next full span's 16-byte loads are in flight while the current
+        // span is packed and stored (one span of loads per warp was latency-bound)
+        // (1- and 2-byte values only: a second span of 8-byte values would spill)
+        constexpr bool PF = VS <= 2;
+        uint4 xn[2 * VS];
+        const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        bool pre = PF && g0 - lane < gEnd && liveOf(g0 - lane) == 32;
+        if(pre)
+            g2r<VS>(p, xn, p.begin + (g0 - lane) * 32, lane);
+        for(uint64_t g = g0; g - lane < gEnd; g += stride)
         {
             const uint64_t warpG = g - lane;
-            const uint32_t live =
-                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint32_t live = liveOf(warpG);
             const uint64_t e0 = p.begin + warpG * 32;
-            g2s<VS>(p, sm, e0, lane, live);
+            if(pre)
+                r2s<VS>(sm, xn, lane);
+            else
+                g2s<VS>(p, sm, e0, lane, live);
+            const uint64_t nextG = warpG + stride;
+            pre = PF && nextG < gEnd && liveOf(nextG) == 32;
+            if(pre)
+                g2r<VS>(p, xn, p.begin + nextG * 32, lane);
             __syncwarp();
             uint32_t wd[8 * VS];
             const bool mine = g < p.groups;
@@ -269,25 +308,48 @@ namespace lamk
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
         const uint64_t mask = lamd::low_mask(w);
-        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        auto liveOf = [&](uint64_t warpG) -> uint32_t
+        {
+            return static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+        };
+        // compile-time widths: the next full span's W word loads are issued before the current
+        // span is decoded and stored (software pipeline, as k_packv)
+        uint32_t tn[W ? W : 1];
+        const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        auto words_of = [&](uint64_t warpG) { return reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w; };
+        bool pre = W != 0 && g0 - lane < gEnd && liveOf(g0 - lane) == 32;
+        if(pre)
+        {
+#pragma unroll
+            for(int k = 0; k < (W ? W : 1); ++k)
+                tn[k] = __ldcs(words_of(g0 - lane) + lane + 32 * k);
+        }
+        for(uint64_t g = g0; g - lane < gEnd; g += stride)
         {
             const uint64_t warpG = g - lane;
-            const uint32_t live =
-                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint32_t live = liveOf(warpG);
             const uint64_t e0 = p.begin + warpG * 32;
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bits) + e0 / 32 * w;
-            if(W != 0 && live == 32)
+            const uint32_t* src = words_of(warpG);
+            const bool had = pre;
+            if(had)
             {
-                uint32_t t[W ? W : 1];
-#pragma unroll
-                for(int k = 0; k < (W ? W : 1); ++k)
-                    t[k] = __ldcs(src + lane + 32 * k);
 #pragma unroll
                 for(int k = 0; k < (W ? W : 1); ++k)
                 {
                     const uint32_t q = lane + 32 * k;
-                    sm[(q / w) * ws + (q % w)] = t[k];
+                    sm[(q / w) * ws + (q % w)] = tn[k];
                 }
+            }
+            const uint64_t nextG = warpG + stride;
+            pre = W != 0 && nextG < gEnd && liveOf(nextG) == 32;
+            if(pre)
+            {
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                    tn[k] = __ldcs(words_of(nextG) + lane + 32 * k);
+            }
+            if(had)
+            {
             }
             else
             {

@@ -8,7 +8,9 @@ from bench import peaks
 PEAK = peaks()[0]  # MEASURED_PEAKS.json hbm_gbs
 n = 1 << 26
 for a, b, sw, dw, g in [("aos-packed", "soa-mb", 0, 2, 64), ("soa-mb", "aos-packed", 2, 0, 64),
-                        ("aos-packed", "soa-mb", 0, 2, 4096), ("aos-packed", "soa-mb", 0, 2, 5)]:
+                        ("aos-packed", "soa-mb", 0, 2, 4096), ("aos-packed", "soa-mb", 0, 2, 5),
+                        ("soa-mb", "aos-packed", 0, 2, 5), ("soa-mb", "aos-packed", 0, 2, 64),
+                        ("aos-packed", "bytesplit:soa-mb", 0, 2, 64)]:
     la = L.Layout(R32, f"i32:[{n}]", a, wrap=sw, granularity=g)
     lb = L.Layout(R32, f"i32:[{n}]", b, wrap=dw, granularity=g)
     s, d = L.View(la), L.View(lb)

@@ -26,5 +26,26 @@ for n in (1, 37, 4099, 70001):
     copy(MIXED, n, "aos-packed", "soa-mb")
     copy("Record{v:u32}", n, "soa-mb", "bitpack-int:7")
     copy("Record{v:u32}", n, "bitpack-int:7", "soa-mb", wb=2)
+    # round 2 kernels: packv (1/2/8-byte leaves, > 32-bit fields), compile-time float widths
+    copy("Record{v:u16,w:u16}", n, "soa-mb", "bitpack-int:5")
+    copy("Record{v:u16,w:u16}", n, "bitpack-int:5", "soa-mb")
+    copy("Record{a:i8,b:u8}", n, "soa-mb", "bitpack-int:3")
+    copy("Record{v:u64,w:i64}", n, "soa-mb", "bitpack-int:47")
+    copy("Record{v:u64,w:i64}", n, "bitpack-int:47", "soa-mb")
+    copy(R64, n, "soa-mb", "bitpack-float:11,52")
+    copy(R64, n, "bitpack-float:11,52", "soa-mb")
+    copy(R32, n, "soa-mb", "bitpack-float:4,3")
+    copy(R32, n, "bitpack-float:4,3", "soa-mb")
+    copy(R32, n, "soa-mb", "bitpack-float:11,30")
+    copy(R32, n, "bitpack-float:11,30", "soa-mb")
 v = L.View(L.Layout(R32, "i64:[700]", "aosoa:8", wrap=3, granularity=16)); v.nbody_init(1); v.nbody_update(0); v.nbody_update(1); v.nbody_move()
+# exact split kernel (small shards), fast kernel, multi-source update, position packing, manual baselines
+w = L.View(L.Layout(R32, "i64:[3000]", "soa-mb")); w.nbody_init(2)
+w.nbody_update(0, 0, 1000); w.nbody_update(0); w.nbody_update(1); w.nbody_move()
+w.nbody_update_from([(w, 0, 1500), (w, 1500, 3000)], 0, 0, 3000)
+import torch
+buf = torch.empty(4 * 3000, dtype=torch.float32, device="cuda")
+w.nbody_pack_positions(0, 3000, buf.data_ptr(), with_mass=True); torch.cuda.synchronize()
+for kind in ("manual-aos", "manual-soa"):
+    m = L.ManualNbody(kind, 3000); m.update(0); m.update(1); m.move(); m.checksum()
 print("ok")
