@@ -379,13 +379,14 @@ def run_c4_strong(L, world, rank, local, steps=5, warmup=2, n=128 * 1024, layout
         nbody_distributed(layout, n, warmup, mode=mode)  # warm-up: allocation, NCCL rings, caches
         barrier(world)
         t = {}
-        nbody_distributed(layout, n, steps, mode=mode, timing=t)
+        with ClockSampler(local) as clk:
+            nbody_distributed(layout, n, steps, mode=mode, timing=t)
         step = max_over_ranks(t["step_ms"], world)
         exch = max_over_ranks(t["exchange_ms"], world)
         upd = max_over_ranks(t["update_ms"], world)
         out[name] = {"ms_per_step": step, "update_ms": upd, "exchange_ms": exch, "move_ms": t["move_ms"],
                      "interactions_per_s": n * n / (step * 1e-3),
-                     "exchange_bytes_per_step": t["exchange_bytes_per_step"]}
+                     "exchange_bytes_per_step": t["exchange_bytes_per_step"], "clocks": clk.summary()}
     return out
 
 

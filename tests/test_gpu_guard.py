@@ -1,6 +1,8 @@
-"""Out-of-bounds write check without a sanitizer: every destination blob is followed (and
-preceded) by a guard band of a known byte pattern in the same allocation; after the copy the
-guards must be intact.  Covers every kernel family at sizes with ragged tails."""
+"""Out-of-bounds write check without a sanitizer (compute-sanitizer is closed on the GPU pool:
+profiles/r02/compute_sanitizer_refused.log): every destination blob is followed (and preceded)
+by a guard band of a known byte pattern in the same allocation; after the copy the guards must
+be intact.  Covers every kernel family at sizes with ragged tails (stray writes inside a blob
+show up as parity failures in test_gpu_copy / test_gpu_scale instead)."""
 import numpy as np
 import pytest
 
@@ -20,6 +22,13 @@ PAIRS = [
     # record-side one-pass packing (k_rec_pack / k_rec_unpack)
     (R32, "bitpack-float:8,10", "aos-packed"), (R32, "bitpack-float:5,10", "aosoa:8"), (R32, "aosoa:16", "bitpack-float:8,10"),
     ("Record{v:u32,w:i32}", "bitpack-int:7", "aos-packed"), ("Record{v:u32,w:i32}", "aosoa:4", "bitpack-int:29"),
+    # round 2: packv (1/2/8-byte leaves, fields wider than 32 bits), compile-time f32 formats
+    ("Record{v:u16,w:i16}", "soa-mb", "bitpack-int:5"), ("Record{v:u16,w:i16}", "bitpack-int:11", "soa-mb"),
+    ("Record{a:i8,b:u8}", "soa-mb", "bitpack-int:3"), ("Record{a:i8,b:u8}", "bitpack-int:7", "aosoa:32"),
+    ("Record{v:u64,w:i64}", "soa-mb", "bitpack-int:47"), ("Record{v:u64,w:i64}", "bitpack-int:33", "soa-mb"),
+    (R64, "soa-mb", "bitpack-float:11,52"), (R64, "bitpack-float:5,10", "soa-mb"),
+    (R32, "soa-mb", "bitpack-float:4,3"), (R32, "bitpack-float:4,3", "soa-mb"),
+    (R32, "soa-mb", "bitpack-float:11,30"), (R32, "bitpack-float:11,30", "soa-mb"),
 ]
 
 
