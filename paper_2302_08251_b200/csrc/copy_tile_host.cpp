@@ -601,6 +601,118 @@ namespace lamhost
         return true;
     }
 
+    // Uniform physical pairs over multi-stream sides (Split mappings, vec_multi.cu k_vec_multi):
+    // every leaf a same-size (4 or 8 byte) physical move without conversion; on each side a
+    // leaf is either leaf-contiguous (SoA, AoSoA with V | L) or sits in a record stream
+    // (L = 1) whose leaves cover the whole record.
+    static bool tryVecMulti(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si,
+                            DeviceImage& di, const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        const uint32_t nl = p.nleaves;
+        if(nl < 1 || nl > 8 || envNum("LAMB_VEC_MULTI", 1) == 0)
+            return false;
+        const uint32_t sz = p.leaf[0].s[0].size;
+        if(sz != 4 && sz != 8)
+            return false;
+        const uint32_t V = 16 / sz, WPE = sz / 4;
+        if(begin % V)
+            return false;
+        for(uint32_t f = 0; f < nl; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != sz || L.d[0].size != sz
+               || L.stype != L.dtype || L.stype != L.ltype || L.ltype == Bool)
+                return false;
+        }
+        lamk::VMParams vp{};
+        uint32_t row = 0;
+        auto side = [&](bool src, lamk::VMSide& sd) -> bool
+        {
+            uint32_t streams[8], nst = 0;
+            for(uint32_t f = 0; f < nl; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                const lamt_stream& st = p.st[t.stream];
+                const bool soa = st.lanes == 1 && st.bs == sz;
+                const bool aosoa = st.lanes > 1 && st.lanes % V == 0 && st.lshift != 0xFFFFFFFFu && t.ls == sz;
+                if(soa || aosoa)
+                {
+                    sd.mode[f] = 0;
+                    sd.base[f] = st.gptr + t.inblock;
+                    sd.bs[f] = soa ? sz * V : st.bs; // per group of V elements: (e0 >> lsh) * bs
+                    sd.lsh[f] = soa ? 0 : st.lshift;
+                    sd.lmask[f] = soa ? 0 : st.lanes - 1;
+                    if(soa)
+                    {
+                        // e0 is a multiple of V: e0 * sz = (e0 >> 0) * bs with bs = sz, lmask 0
+                        sd.bs[f] = sz;
+                    }
+                    if(sd.base[f] % 16 || (aosoa && st.bs % 16))
+                        return false;
+                    continue;
+                }
+                if(st.lanes != 1 || st.bs % sz || t.inblock % sz || st.bs > 8 * sz || st.gptr % 16)
+                    return false;
+                uint32_t r = 0;
+                while(r < nst && streams[r] != t.stream)
+                    ++r;
+                if(r == nst)
+                    streams[nst++] = t.stream;
+                sd.mode[f] = 1;
+            }
+            // record streams: covered by their leaves (each record position once), V records =
+            // bs * V / 16 vectors, laid out in the lane row
+            for(uint32_t r = 0; r < nst; ++r)
+            {
+                const lamt_stream& st = p.st[streams[r]];
+                const uint32_t rl = st.bs / sz;
+                uint32_t seen = 0, cnt = 0;
+                for(uint32_t f = 0; f < nl; ++f)
+                {
+                    const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                    if(sd.mode[f] != 1 || t.stream != streams[r])
+                        continue;
+                    const uint32_t q = t.inblock / sz;
+                    if(q >= rl || (seen >> q) & 1u)
+                        return false;
+                    seen |= 1u << q;
+                    ++cnt;
+                    sd.wpos[f] = row + q * WPE;
+                    sd.wstep[f] = rl * WPE;
+                }
+                if(cnt != rl)
+                    return false;
+                const uint32_t nv = st.bs * V / 16;
+                for(uint32_t k = 0; k < nv; ++k)
+                {
+                    if(sd.nvec >= 8)
+                        return false;
+                    sd.vb[sd.nvec] = st.gptr + 16ull * k;
+                    sd.vs[sd.nvec] = st.bs;
+                    sd.vrow[sd.nvec] = row + 4 * k;
+                    ++sd.nvec;
+                }
+                row += nv * 4;
+            }
+            return true;
+        };
+        if(!side(true, vp.s) || !side(false, vp.d))
+            return false;
+        vp.rowWords = row | 1u;
+        vp.begin = begin;
+        vp.groups = (end - begin) / V;
+        vp.nl = nl;
+        if(vp.groups == 0 || !lamk::vec_multi(vp, sz, s))
+            return false;
+        addAccessCounts(p, S, vp.groups * V, s);
+        const uint64_t doneEnd = begin + vp.groups * V;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s, false),
+                           "generic_copy(tail)");
+        return true;
+    }
+
     // ChangeType f32 <-> f64 over uniform geometries (vec_transpose.cu k_vec_convert): every leaf
     // PHYS -> PHYS with source size SS and destination size DS (4 <-> 8), one conversion
     // f32 -> f64 or f64 -> f32 between them; each side record-contiguous or leaf-contiguous.
@@ -1067,6 +1179,8 @@ namespace lamhost
         if(!p.uni && trySplit(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
+            return true;
+        if(!p.uni && tryVecMulti(p, begin, end, si, di, S, D, s))
             return true;
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /

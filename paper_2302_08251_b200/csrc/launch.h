@@ -32,6 +32,26 @@ namespace lamk
 
     bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s);
 
+    // register transpose over multi-stream sides (Split mappings), vec_multi.cu
+    struct VMSide
+    {
+        // leaf-contiguous leaves (mode 0): V values at base + (e0 >> lsh) * bs + (e0 & lmask) * S
+        unsigned long long base[8];
+        uint32_t bs[8], lsh[8], lmask[8], mode[8];
+        // record leaves (mode 1): element j's value at row word wpos + j * wstep
+        uint32_t wpos[8], wstep[8];
+        // record streams as 16-byte vectors k < nvec: address vb + e0 * vs, row words [vrow, vrow + 4)
+        unsigned long long vb[8];
+        uint32_t vs[8], vrow[8], nvec;
+    };
+    struct VMParams
+    {
+        VMSide s, d;
+        unsigned long long begin, groups; // groups of V elements
+        uint32_t nl, rowWords;            // rowWords: odd (conflict-free lane rows)
+    };
+    bool vec_multi(const VMParams& p, uint32_t leafSize, cudaStream_t s);
+
     int sm_count(int device);
 
     // Opt `func` in to `smem` bytes of dynamic shared memory on the CURRENT device.  The
