@@ -694,6 +694,22 @@ namespace lamhost
                 }
                 row += nv * 4;
             }
+            // AoS: a single record stream with every leaf at inblock f * sz -> registers only
+            sd.full = 0;
+            if(nst == 1)
+            {
+                bool full = true;
+                for(uint32_t f = 0; f < nl && full; ++f)
+                {
+                    const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                    full = sd.mode[f] == 1 && t.stream == streams[0] && t.inblock == f * sz;
+                }
+                if(full)
+                {
+                    sd.full = 1;
+                    row -= sd.nvec * 4; // no row needed
+                }
+            }
             return true;
         };
         if(!side(true, vp.s) || !side(false, vp.d))

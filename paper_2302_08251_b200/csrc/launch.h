@@ -43,6 +43,7 @@ namespace lamk
         // record streams as 16-byte vectors k < nvec: address vb + e0 * vs, row words [vrow, vrow + 4)
         unsigned long long vb[8];
         uint32_t vs[8], vrow[8], nvec;
+        uint32_t full; // one record stream with every leaf in order (AoS): register renaming, no row
     };
     struct VMParams
     {

@@ -48,21 +48,42 @@ namespace lamk
             for(int f = 0; f < NL; ++f)
                 if(p.s.mode[f] == 0)
                     lx[f] = __ldcs(reinterpret_cast<const uint4*>(vm_leaf_addr<S>(p.s, f, e0)));
-            // record vectors -> the row, word by word
+            if(p.s.full)
+            {
+                // one record stream holding every leaf in order (AoS): the V records are NL
+                // vectors and the AoS -> leaf permutation is compile-time register renaming
 #pragma unroll
-            for(int k = 0; k < NL; ++k)
-                if(k < static_cast<int>(p.s.nvec))
+                for(int k = 0; k < NL; ++k)
                 {
-                    uint32_t* at = row + p.s.vrow[k];
-                    at[0] = rx[k].x;
-                    at[1] = rx[k].y;
-                    at[2] = rx[k].z;
-                    at[3] = rx[k].w;
+                    const W* w = reinterpret_cast<const W*>(&rx[k]);
+#pragma unroll
+                    for(int j = 0; j < V; ++j)
+                    {
+                        const int word = k * V + j;
+                        v[word % NL][word / NL] = w[j];
+                    }
                 }
+            }
+            else
+            {
+                // record vectors -> the row, word by word
+#pragma unroll
+                for(int k = 0; k < NL; ++k)
+                    if(k < static_cast<int>(p.s.nvec))
+                    {
+                        uint32_t* at = row + p.s.vrow[k];
+                        at[0] = rx[k].x;
+                        at[1] = rx[k].y;
+                        at[2] = rx[k].z;
+                        at[3] = rx[k].w;
+                    }
+            }
             // ---- gather every leaf ----
 #pragma unroll
             for(int f = 0; f < NL; ++f)
             {
+                if(p.s.full)
+                    break;
                 if(p.s.mode[f] == 0)
                 {
                     const W* w = reinterpret_cast<const W*>(&lx[f]);
@@ -84,6 +105,23 @@ namespace lamk
                                 | (static_cast<unsigned long long>(at[j * step + 1]) << 32);
                     }
                 }
+            }
+            if(p.d.full)
+            {
+#pragma unroll
+                for(int k = 0; k < NL; ++k)
+                {
+                    uint4 x;
+                    W* w = reinterpret_cast<W*>(&x);
+#pragma unroll
+                    for(int j = 0; j < V; ++j)
+                    {
+                        const int word = k * V + j;
+                        w[j] = v[word % NL][word / NL];
+                    }
+                    __stcs(reinterpret_cast<uint4*>(p.d.vb[k] + e0 * p.d.vs[k]), x);
+                }
+                continue;
             }
             // ---- scatter every leaf: leaf runs straight out, record leaves into the row ----
 #pragma unroll

@@ -11,6 +11,10 @@ PAIRS = [
     (R32, "aos-packed", "aos-aligned", 0), (R32, "soa-mb", "aos-packed", 1), (R32, "aos-packed", "soa-mb", 2),
     (R32, "aos-packed", "bitpack-float:5,10", 0), (R32, "aos-packed", "null", 0),
     ("Record{a:f64,b:u16,c:i8,d:f32}", "aos-packed", "soa-mb", 0),
+    # Split compositions (k_vec_multi)
+    (R32, "split:Pos:soa-mb:aos-packed", "aos-packed", 0), (R32, "soa-mb", "split:Pos:soa-mb:aos-packed", 0),
+    (R32, "aosoa:8", "split:Vel:aosoa:8:soa-mb", 0), (R32, "split:Pos,Mass:aosoa:4:soa-sb", "aos-packed", 0),
+    (R32, "aos-packed", "split:Vel:aos-packed:aos-packed", 0), (R64, "aos-packed", "split:Pos:soa-mb:aos-packed", 0),
 ]
 for schema, a, b, wrap in PAIRS:
     la, lb = L.Layout(schema, f"i32:[{n}]", a), L.Layout(schema, f"i32:[{n}]", b, wrap=wrap, granularity=64)
