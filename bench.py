@@ -448,6 +448,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C4 strong / C5 sharded keys")
+    ap.add_argument("--c4-particles", type=int, default=128 * 1024)
+    ap.add_argument("--c5-records", type=int, default=1_000_000_000)
     args = ap.parse_args()
     if args.impl == "reference":
         # the reference arm is CPU-only: no process group, rank 0 alone works and prints
@@ -541,8 +543,8 @@ def main():
             line["e2e"] = e2e
     if not args.no_extra:
         # configs that shard / communicate at N GPUs (informative keys beside the C2 headline)
-        line["c4_strong"] = run_c4_strong(L, world, rank, local)
-        line["c5_sharded"] = run_c5_sharded(L, world, rank, local)
+        line["c4_strong"] = run_c4_strong(L, world, rank, local, n=args.c4_particles)
+        line["c5_sharded"] = run_c5_sharded(L, world, rank, local, total=args.c5_records)
     if args.suite and rank == 0:
         from bench_suite import run_suite
         line["suite"] = run_suite(L, local)

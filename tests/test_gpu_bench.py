@@ -23,7 +23,7 @@ def _line(out):
 
 def test_bench_single_gpu_small():
     r = subprocess.run([sys.executable, "bench.py", "--records", str(1 << 20), "--steps", "2", "--warmup", "3",
-                        "--no-e2e", "--no-cpu"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+                        "--no-e2e", "--no-cpu", "--no-extra"], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _line(r.stdout)
     assert KEYS <= set(d) and d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
@@ -34,8 +34,12 @@ def test_bench_two_ranks_gloo():
     env = dict(os.environ, LAMB_DIST_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
-                        "--records", str(1 << 20), "--steps", "2", "--warmup", "3", "--no-cpu"],
+                        "--records", str(1 << 20), "--steps", "2", "--warmup", "3", "--no-cpu",
+                        "--c4-particles", "8192", "--c5-records", str(1 << 22)],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _line(r.stdout)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["e2e"]["h2d_bytes_per_step"] > 0
+    # the paths that shard / communicate: n-body with the positions-only exchange, C5 sharded
+    assert d["c4_strong"]["exact"]["interactions_per_s"] > 0 and d["c4_strong"]["fast"]["exchange_bytes_per_step"] > 0
+    assert d["c5_sharded"]["counters_ok"] and d["c5_sharded"]["records_total"] == 1 << 22
