@@ -30,7 +30,11 @@ namespace lamk
         uint32_t vbs, vl, vsh, vinb; // value stream geometry: SoA (vl == 1) or AoSoA (vl % 32 == 0)
     };
 
-    bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s);
+    struct PackVMulti
+    {
+        PackVParams q[8];
+    };
+    bool packv(const PackVParams* jobs, uint32_t n, uint32_t vsize, bool pack, cudaStream_t s);
 
     // register transpose over multi-stream sides (Split mappings), vec_multi.cu
     struct VMSide

@@ -31,6 +31,13 @@ namespace lamk
         uint32_t vbs, vl, vsh, vinb; // value-stream geometry: AoSoA lanes (vl % 32 == 0) or SoA (vl == 1)
     };
 
+    // the leaves of one copy with the same field width and format, one launch: leaf = blockIdx.y
+    // (separate launches per leaf left a ramp and a tail per leaf on multi-leaf records)
+    struct PackMulti
+    {
+        PackParams q[8];
+    };
+
     __device__ __forceinline__ uint64_t val_addr(const PackParams& p, uint64_t e0)
     {
         if(p.vl == 1)
@@ -222,8 +229,9 @@ namespace lamk
     }
 
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackMulti M)
     {
+        const PackParams& p = M.q[blockIdx.y];
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -327,8 +335,9 @@ namespace lamk
 
     // unpack: W words -> 32 values per thread
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, 3) k_unpack32(const __grid_constant__ PackParams p)
+    __global__ void __launch_bounds__(256, 3) k_unpack32(const __grid_constant__ PackMulti M)
     {
+        const PackParams& p = M.q[blockIdx.y];
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -781,58 +790,69 @@ namespace lamk
     }
 
     template<int W, int FMT>
-    static void launch_pack(const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s)
+    static void launch_pack(const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s)
     {
         // opt in to > 48 KB of dynamic shared memory once per instantiation, size and device
+        const dim3 g(resident_grid(k_pack32<W, FMT>, grid, smem, false), n);
         if(pack)
         {
             lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_pack32<W, FMT>), smem), "opt_in_smem");
-            k_pack32<W, FMT><<<resident_grid(k_pack32<W, FMT>, grid, smem, p.facS || p.facD), 256, smem, s>>>(p);
+            k_pack32<W, FMT><<<g, 256, smem, s>>>(m);
         }
         else
         {
             lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_unpack32<W, FMT>), smem), "opt_in_smem");
-            k_unpack32<W, FMT><<<resident_grid(k_unpack32<W, FMT>, grid, smem, p.facS || p.facD), 256, smem, s>>>(p);
+            k_unpack32<W, FMT><<<g, 256, smem, s>>>(m);
         }
     }
 
     template<int... Ws>
-    static bool dispatch_int(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+    static bool dispatch_int(int w, const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s,
                              std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((w == Ws + 1 ? (launch_pack<Ws + 1, 0>(p, pack, grid, smem, s), hit = true) : false), ...);
+        ((w == Ws + 1 ? (launch_pack<Ws + 1, 0>(m, n, pack, grid, smem, s), hit = true) : false), ...);
         return hit;
     }
 
     // any other (E, M) with 1 + E + M <= 32: compile-time width, runtime format
     template<int... Ws>
-    static bool dispatch_flt(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+    static bool dispatch_flt(int w, const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s,
                              std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((w == Ws + 2 ? (launch_pack<Ws + 2, 3>(p, pack, grid, smem, s), hit = true) : false), ...);
+        ((w == Ws + 2 ? (launch_pack<Ws + 2, 3>(m, n, pack, grid, smem, s), hit = true) : false), ...);
         return hit;
     }
 
-    bool pack32(const PackParams& p, bool pack, cudaStream_t s)
+    // jobs[0..n): leaves of one copy with the same width, format and element range (n <= 8)
+    bool pack32(const PackParams* jobs, uint32_t n, bool pack, cudaStream_t s)
     {
+        if(n == 0 || n > 8)
+            return false;
+        const PackParams& p = jobs[0];
         if(p.groups == 0 || p.w < 1 || p.w > 32)
             return false;
-        int dev = 0;
-        cudaGetDevice(&dev);
+        PackMulti m{};
+        for(uint32_t k = 0; k < n; ++k)
+        {
+            if(jobs[k].w != p.w || jobs[k].kind != p.kind || jobs[k].E != p.E || jobs[k].M != p.M
+               || jobs[k].groups != p.groups || jobs[k].begin != p.begin)
+                return false;
+            m.q[k] = jobs[k];
+        }
         const uint64_t want = (p.groups + 255) / 256;
         const unsigned grid = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);
         const size_t smem = 8 * slice_words(p.w) * sizeof(uint32_t);
         if(p.kind == 0)
-            dispatch_int(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
+            dispatch_int(static_cast<int>(p.w), m, n, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
         else if(p.E == 8 && p.M == 10)
-            launch_pack<19, 1>(p, pack, grid, smem, s);
+            launch_pack<19, 1>(m, n, pack, grid, smem, s);
         else if(p.E == 5 && p.M == 10)
-            launch_pack<16, 2>(p, pack, grid, smem, s);
+            launch_pack<16, 2>(m, n, pack, grid, smem, s);
         else if(p.E > 8 || p.M > 23
-                || !dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
-            launch_pack<0, 4>(p, pack, grid, smem, s);
+                || !dispatch_flt(static_cast<int>(p.w), m, n, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
+            launch_pack<0, 4>(m, n, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");
         return true;

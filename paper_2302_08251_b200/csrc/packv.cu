@@ -171,8 +171,9 @@ namespace lamk
     // W != 0: compile-time field width of an integer leaf of 1 or 2 bytes (word boundaries at
     // compile-time positions: pure shift/or chains, as k_pack32); W == 0: runtime width / float
     template<int VS, int W = 0>
-    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_packv(const __grid_constant__ PackVParams p)
+    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_packv(const __grid_constant__ PackVMulti M)
     {
+        const PackVParams& p = M.q[blockIdx.y];
         extern __shared__ __align__(16) uint32_t vsm[];
         const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
@@ -300,8 +301,9 @@ namespace lamk
     }
 
     template<int VS, int W = 0>
-    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_unpackv(const __grid_constant__ PackVParams p)
+    __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_unpackv(const __grid_constant__ PackVMulti M)
     {
+        const PackVParams& p = M.q[blockIdx.y];
         extern __shared__ __align__(16) uint32_t vsm[];
         const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
@@ -476,8 +478,9 @@ namespace lamk
     }
 
     template<int VS, int W = 0>
-    static void launch_v(const PackVParams& p, bool pack, cudaStream_t s)
+    static void launch_v(const PackVMulti& m, uint32_t n, bool pack, cudaStream_t s)
     {
+        const PackVParams& p = m.q[0];
         int dev = 0;
         cudaGetDevice(&dev);
         const size_t smem = 8 * warp_words<VS>() * sizeof(uint32_t);
@@ -489,37 +492,50 @@ namespace lamk
         const uint64_t want = (p.groups + 255) / 256;
         const uint64_t cap = static_cast<uint64_t>(sm_count(dev)) * occ * 4;
         const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-        kern<<<grid, 256, smem, s>>>(p);
+        kern<<<dim3(grid, n), 256, smem, s>>>(m);
     }
 
     // integer leaves of 1 / 2 bytes: a compile-time width per kernel
     template<int VS, int... Ws>
-    static bool dispatch_narrow(const PackVParams& p, bool pack, cudaStream_t s, std::integer_sequence<int, Ws...>)
+    static bool dispatch_narrow(const PackVMulti& m, uint32_t n, bool pack, cudaStream_t s,
+                                std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((static_cast<int>(p.w) == Ws + 1 ? (launch_v<VS, Ws + 1>(p, pack, s), hit = true) : false), ...);
+        ((static_cast<int>(m.q[0].w) == Ws + 1 ? (launch_v<VS, Ws + 1>(m, n, pack, s), hit = true) : false), ...);
         return hit;
     }
 
-    bool packv(const PackVParams& p, uint32_t vsize, bool pack, cudaStream_t s)
+    // jobs[0..n): leaves with the same value size, width, format and range, one launch (leaf = blockIdx.y)
+    bool packv(const PackVParams* jobs, uint32_t n, uint32_t vsize, bool pack, cudaStream_t s)
     {
+        if(n == 0 || n > 8)
+            return false;
+        const PackVParams& p = jobs[0];
         if(p.groups == 0 || p.w < 1 || p.w > 64 || (p.kind == 0 && p.w > 8 * vsize))
             return false;
+        PackVMulti m{};
+        for(uint32_t k = 0; k < n; ++k)
+        {
+            if(jobs[k].w != p.w || jobs[k].kind != p.kind || jobs[k].E != p.E || jobs[k].M != p.M
+               || jobs[k].groups != p.groups || jobs[k].begin != p.begin)
+                return false;
+            m.q[k] = jobs[k];
+        }
         switch(vsize)
         {
         case 1:
-            if(p.kind != 0 || !dispatch_narrow<1>(p, pack, s, std::make_integer_sequence<int, 8>{}))
-                launch_v<1>(p, pack, s);
+            if(p.kind != 0 || !dispatch_narrow<1>(m, n, pack, s, std::make_integer_sequence<int, 8>{}))
+                launch_v<1>(m, n, pack, s);
             break;
         case 2:
-            if(p.kind != 0 || !dispatch_narrow<2>(p, pack, s, std::make_integer_sequence<int, 16>{}))
-                launch_v<2>(p, pack, s);
+            if(p.kind != 0 || !dispatch_narrow<2>(m, n, pack, s, std::make_integer_sequence<int, 16>{}))
+                launch_v<2>(m, n, pack, s);
             break;
         case 4:
-            launch_v<4>(p, pack, s);
+            launch_v<4>(m, n, pack, s);
             break;
         case 8:
-            launch_v<8>(p, pack, s);
+            launch_v<8>(m, n, pack, s);
             break;
         default:
             return false;
