@@ -431,7 +431,10 @@ namespace lamk
                 }
                 used += static_cast<uint32_t>(P);
             }
-            const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 0);
+            // a per-thread setup of a few hundred instructions (stream parameters, edge blocks, the
+            // pattern phase) was amortised over only 4 counters in a one-pass grid (84 instructions
+            // per counter, ncu): grid-stride with 4 CTAs per SM per stream instead
+            const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 4);
             k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();
             return cudaGetLastError();
