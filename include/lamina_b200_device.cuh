@@ -22,7 +22,11 @@
  *
  * SmemRecordTile<T, NL, N> is a shared-memory view with compile-time extents: N records x NL
  * leaves of type T in SoA order, filled / drained cooperatively by a CTA through the mapping.
- * It is the structure the n-body kernels use for their j-tiles.
+ * The library's own n-body kernels (csrc/nbody.cu) stage their j-tiles in the same shape
+ * (compile-time extents, filled through resolved leaf accessors) but as hand-packed float4 /
+ * negated FP32x2-pair arrays that the packed-FMA inner loop consumes directly, not through this
+ * type; SmemRecordTile is exercised by user kernels (examples/device_view_demo.cu,
+ * tests/test_gpu_device_api.py).
  */
 #pragma once
 
