@@ -431,10 +431,9 @@ namespace lamk
                 }
                 used += static_cast<uint32_t>(P);
             }
-            // a per-thread setup of a few hundred instructions (stream parameters, edge blocks, the
-            // pattern phase) was amortised over only 4 counters in a one-pass grid (84 instructions
-            // per counter, ncu): grid-stride with 4 CTAs per SM per stream instead
-            const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 4);
+            // one pass (each thread 4 counters): a grid-stride grid of 4 CTAs/SM/stream cut the
+            // instructions per counter but measured slower (fewer counter loads in flight)
+            const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 0);
             k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();
             return cudaGetLastError();
