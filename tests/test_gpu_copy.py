@@ -370,19 +370,20 @@ def test_bitpack_int16_equals_soa_u16():
                                          ("Record{a:i16,b:u16}", 11), ("Record{v:u64}", 33),
                                          ("Record{v:u64,w:i64}", 47), ("Record{v:i64}", 64),
                                          ("Record{a:i8,b:u64,c:i16}", 5)])
-def test_bitpack_int_other_widths(schema, bits):
+@pytest.mark.parametrize("n", [1189, 4099])  # 1189: one full warp of 32-value groups plus 5 lanes
+def test_bitpack_int_other_widths(schema, bits, n):
     """BitpackIntSoA on 8/16/64-bit leaves (computed.cpp:59-67,101-122): pack truncates to the
-    low b bits, unpack zero/sign-extends; 1 <= b <= 8 * leaf size."""
-    n = 4099
+    low b bits, unpack zero/sign-extends; 1 <= b <= 8 * leaf size.  soa-mb and aosoa:32 take the
+    packv kernels (partial warps included), the others the general engines."""
     rng = np.random.default_rng(bits)
     vals = random_values(rng, leaf_types(schema), n)
-    for phys in ("soa-mb", "aos-packed", "aosoa:8"):
+    for phys in ("soa-mb", "aosoa:32", "aos-packed", "aosoa:8"):
         run_pair(schema, n, phys, f"bitpack-int:{bits}", vals)
     packed = O.make(schema, f"i32:[{n}]", f"bitpack-int:{bits}")
     pb = O.zero_blobs(packed)
     O.write_all(packed, pb, vals)
     back = O.read_all(packed, pb)
-    for phys in ("soa-mb", "aos-packed"):
+    for phys in ("soa-mb", "aosoa:32", "aos-packed"):
         run_pair(schema, n, f"bitpack-int:{bits}", phys, back)
 
 
@@ -393,7 +394,7 @@ def test_bitpack_float_f64_leaves(fmt):
     n = 4099
     rng = np.random.default_rng(52)
     vals = random_values(rng, [9] * 7, n)
-    for phys in ("aos-packed", "soa-mb"):
+    for phys in ("aos-packed", "soa-mb", "aosoa:32"):
         run_pair(R64, n, phys, f"bitpack-float:{fmt}", vals)
     packed = O.make(R64, f"i32:[{n}]", f"bitpack-float:{fmt}")
     pb = O.zero_blobs(packed)
@@ -429,3 +430,18 @@ def test_bool_bytes_canonicalise_on_read(a, b, generic, monkeypatch):
         assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
     vals = O.read_all(md, db)
     assert set(np.unique(vals[:, [0, 2, 4]])) <= {0, 1}
+
+
+@pytest.mark.parametrize("fmt", ["4,3", "5,2", "8,7", "6,9", "3,0", "11,30", "11,52", "8,23"])
+@pytest.mark.parametrize("phys", ["soa-mb", "aosoa:32"])
+def test_bitpack_float_f32_formats(fmt, phys):
+    """f32 leaves through the compile-time-width k_pack32 (E <= 8, M <= 23: FMT 3) and, for fields
+    wider than 32 bits, k_packv<4> -- both directions, ragged size, specials included."""
+    n = 1189
+    rng = np.random.default_rng(int(fmt.replace(",", "")))
+    vals = random_values(rng, [8] * 7, n)
+    run_pair(R32, n, phys, f"bitpack-float:{fmt}", vals)
+    packed = O.make(R32, f"i32:[{n}]", f"bitpack-float:{fmt}")
+    pb = O.zero_blobs(packed)
+    O.write_all(packed, pb, vals)
+    run_pair(R32, n, f"bitpack-float:{fmt}", phys, O.read_all(packed, pb))
