@@ -334,8 +334,14 @@ namespace lamk
     }
 
     // unpack: W words -> 32 values per thread
+    // unpack: 3 CTAs/SM (80 registers) except the widths that spill there
+    __host__ __device__ constexpr int unpack_minb(int W)
+    {
+        return (W >= 14 && W != 16 && W != 32) || W == 6 ? 2 : 3;
+    }
+
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, 3) k_unpack32(const __grid_constant__ PackMulti M)
+    __global__ void __launch_bounds__(256, unpack_minb(W)) k_unpack32(const __grid_constant__ PackMulti M)
     {
         const PackParams& p = M.q[blockIdx.y];
         extern __shared__ __align__(16) uint32_t psm[];
@@ -348,14 +354,34 @@ namespace lamk
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
-        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        auto liveOf = [&](uint64_t warpG) -> uint32_t
+        {
+            return static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+        };
+        auto words_at = [&](uint64_t warpG)
+        { return reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w; };
+        // full warps with a compile-time width: the next span's W coalesced word loads are issued
+        // before the current span is decoded and stored (software pipeline; for narrow widths a
+        // span is only W * 128 bytes of loads per warp, too little to cover the latency alone)
+        // (widths <= 8 only: wider spans already carry enough bytes, and the extra registers
+        // would spill under the 80-register bound)
+        constexpr bool PF = W != 0 && W <= 8;
+        uint32_t tn[W ? W : 1];
+        const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        bool pre = PF && g0 - lane < gEnd && liveOf(g0 - lane) == 32;
+        if(pre)
+        {
+#pragma unroll
+            for(int k = 0; k < (W ? W : 1); ++k)
+                tn[k] = __ldcs(words_at(g0 - lane) + lane + 32 * k);
+        }
+        for(uint64_t g = g0; g - lane < gEnd; g += stride)
         {
             const uint64_t warpG = g - lane;
-            const uint32_t liveLanes =
-                static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
-            const uint32_t* srcw = reinterpret_cast<const uint32_t*>(p.bits) + (p.begin + warpG * 32) / 32 * w;
+            const uint32_t liveLanes = liveOf(warpG);
+            const uint32_t* srcw = words_at(warpG);
             const uint32_t words = liveLanes * w;
-            if(W != 0 && liveLanes == 32)
+            if(!PF && W != 0 && liveLanes == 32)
             {
                 // full warp: the W coalesced word loads are all in flight before any smem store
                 uint32_t t[W ? W : 1];
@@ -367,6 +393,23 @@ namespace lamk
                 {
                     const uint32_t q = lane + 32 * k;
                     slice[(q / w) * ws + (q % w)] = t[k];
+                }
+            }
+            else if(pre)
+            {
+#pragma unroll
+                for(int k = 0; k < (W ? W : 1); ++k)
+                {
+                    const uint32_t q = lane + 32 * k;
+                    slice[(q / w) * ws + (q % w)] = tn[k];
+                }
+                const uint64_t nextG = warpG + stride;
+                pre = PF && nextG < gEnd && liveOf(nextG) == 32;
+                if(pre)
+                {
+#pragma unroll
+                    for(int k = 0; k < (W ? W : 1); ++k)
+                        tn[k] = __ldcs(words_at(nextG) + lane + 32 * k);
                 }
             }
             else
