@@ -299,6 +299,7 @@ namespace lamk
         return a >= 0 ? a / b : -((-a + b - 1) / b);
     }
 
+#define HEAT_CLOSED_K 16
     __global__ void __launch_bounds__(256) k_heat_closed(const __grid_constant__ HeatParams p)
     {
         const HeatStream& st = p.st[blockIdx.y];
@@ -313,7 +314,7 @@ namespace lamk
         // HEAT_K consecutive counters per thread: their read-modify-writes are independent, so all
         // HEAT_K loads are in flight together (one 8-byte RMW per thread left the pass latency-bound
         // at ~2 TB/s of counter traffic)
-        constexpr int HEAT_K = 4;
+        constexpr int HEAT_K = HEAT_CLOSED_K;
         for(int64_t bq = first + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * HEAT_K; bq <= last;
             bq += static_cast<int64_t>(gridDim.x) * blockDim.x * HEAT_K)
         {
@@ -431,9 +432,10 @@ namespace lamk
                 }
                 used += static_cast<uint32_t>(P);
             }
-            // one pass (each thread 4 counters): a grid-stride grid of 4 CTAs/SM/stream cut the
-            // instructions per counter but measured slower (fewer counter loads in flight)
-            const unsigned gx = stream_grid((maxBlocks + 4 * 256 - 1) / (4 * 256), "LAMB_HEAT_CTAS", 0);
+            // one pass, HEAT_CLOSED_K counters per thread: the per-thread setup (stream parameters,
+            // edge blocks, pattern phase: a few hundred instructions) made the 4-counter version
+            // issue-bound (84 instructions per counter, ncu); a grid-stride grid measured slower
+            const unsigned gx = stream_grid((maxBlocks + HEAT_CLOSED_K * 256 - 1) / (HEAT_CLOSED_K * 256), "LAMB_HEAT_CTAS", 0);
             k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();
             return cudaGetLastError();
