@@ -32,7 +32,9 @@ namespace lamk
 
     struct PackVMulti
     {
-        PackVParams q[8];
+        PackVParams base; // shared fields; per-leaf fields below (leaf = blockIdx.y)
+        unsigned long long vals[8], bits[8];
+        uint32_t vinb[8], sgn[8];
     };
     bool packv(const PackVParams* jobs, uint32_t n, uint32_t vsize, bool pack, cudaStream_t s);
 

@@ -33,10 +33,26 @@ namespace lamk
 
     // the leaves of one copy with the same field width and format, one launch: leaf = blockIdx.y
     // (separate launches per leaf left a ramp and a tail per leaf on multi-leaf records)
+    // (shared fields once, per-leaf fields as arrays: the kernel rebuilds its PackParams with
+    // constant-offset parameter reads -- an indexed PackParams[8] cost up to 10% in the hot loop)
     struct PackMulti
     {
-        PackParams q[8];
+        PackParams base;
+        unsigned long long vals[8], bits[8];
+        uint32_t vinb[8], leaf[8], sgn[8], valType[8];
     };
+    __device__ __forceinline__ PackParams leaf_params(const PackMulti& M)
+    {
+        PackParams p = M.base;
+        const uint32_t y = blockIdx.y;
+        p.vals = M.vals[y];
+        p.bits = M.bits[y];
+        p.vinb = M.vinb[y];
+        p.leaf = M.leaf[y];
+        p.sgn = M.sgn[y];
+        p.valType = M.valType[y];
+        return p;
+    }
 
     __device__ __forceinline__ uint64_t val_addr(const PackParams& p, uint64_t e0)
     {
@@ -231,7 +247,7 @@ namespace lamk
     template<int W, int FMT>
     __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackMulti M)
     {
-        const PackParams& p = M.q[blockIdx.y];
+        const PackParams p = leaf_params(M);
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -343,7 +359,7 @@ namespace lamk
     template<int W, int FMT>
     __global__ void __launch_bounds__(256, unpack_minb(W)) k_unpack32(const __grid_constant__ PackMulti M)
     {
-        const PackParams& p = M.q[blockIdx.y];
+        const PackParams p = leaf_params(M);
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -877,12 +893,20 @@ namespace lamk
         if(p.groups == 0 || p.w < 1 || p.w > 32)
             return false;
         PackMulti m{};
+        m.base = p;
         for(uint32_t k = 0; k < n; ++k)
         {
-            if(jobs[k].w != p.w || jobs[k].kind != p.kind || jobs[k].E != p.E || jobs[k].M != p.M
-               || jobs[k].groups != p.groups || jobs[k].begin != p.begin)
+            const PackParams& j = jobs[k];
+            if(j.w != p.w || j.kind != p.kind || j.E != p.E || j.M != p.M || j.groups != p.groups || j.begin != p.begin
+               || j.vbs != p.vbs || j.vl != p.vl || j.vsh != p.vsh || j.facS != p.facS || j.facD != p.facD
+               || j.facSrc != p.facSrc || j.facDst != p.facDst || j.nleaves != p.nleaves)
                 return false;
-            m.q[k] = jobs[k];
+            m.vals[k] = j.vals;
+            m.bits[k] = j.bits;
+            m.vinb[k] = j.vinb;
+            m.leaf[k] = j.leaf;
+            m.sgn[k] = j.sgn;
+            m.valType[k] = j.valType;
         }
         const uint64_t want = (p.groups + 255) / 256;
         const unsigned grid = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);

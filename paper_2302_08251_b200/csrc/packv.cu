@@ -18,6 +18,17 @@
 
 namespace lamk
 {
+    __device__ __forceinline__ PackVParams leafv_params(const PackVMulti& M)
+    {
+        PackVParams p = M.base;
+        const uint32_t y = blockIdx.y;
+        p.vals = M.vals[y];
+        p.bits = M.bits[y];
+        p.vinb = M.vinb[y];
+        p.sgn = M.sgn[y];
+        return p;
+    }
+
     namespace
     {
         template<int VS>
@@ -173,7 +184,7 @@ namespace lamk
     template<int VS, int W = 0>
     __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_packv(const __grid_constant__ PackVMulti M)
     {
-        const PackVParams& p = M.q[blockIdx.y];
+        const PackVParams p = leafv_params(M);
         extern __shared__ __align__(16) uint32_t vsm[];
         const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
@@ -303,7 +314,7 @@ namespace lamk
     template<int VS, int W = 0>
     __global__ void __launch_bounds__(256, VS == 8 ? 2 : 3) k_unpackv(const __grid_constant__ PackVMulti M)
     {
-        const PackVParams& p = M.q[blockIdx.y];
+        const PackVParams p = leafv_params(M);
         extern __shared__ __align__(16) uint32_t vsm[];
         const uint32_t lane = threadIdx.x & 31, w = W ? W : p.w, ws = w | 1u;
         uint32_t* sm = vsm + (threadIdx.x >> 5) * warp_words<VS>();
@@ -480,7 +491,7 @@ namespace lamk
     template<int VS, int W = 0>
     static void launch_v(const PackVMulti& m, uint32_t n, bool pack, cudaStream_t s)
     {
-        const PackVParams& p = m.q[0];
+        const PackVParams& p = m.base;
         int dev = 0;
         cudaGetDevice(&dev);
         const size_t smem = 8 * warp_words<VS>() * sizeof(uint32_t);
@@ -501,7 +512,7 @@ namespace lamk
                                 std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((static_cast<int>(m.q[0].w) == Ws + 1 ? (launch_v<VS, Ws + 1>(m, n, pack, s), hit = true) : false), ...);
+        ((static_cast<int>(m.base.w) == Ws + 1 ? (launch_v<VS, Ws + 1>(m, n, pack, s), hit = true) : false), ...);
         return hit;
     }
 
@@ -514,12 +525,17 @@ namespace lamk
         if(p.groups == 0 || p.w < 1 || p.w > 64 || (p.kind == 0 && p.w > 8 * vsize))
             return false;
         PackVMulti m{};
+        m.base = p;
         for(uint32_t k = 0; k < n; ++k)
         {
-            if(jobs[k].w != p.w || jobs[k].kind != p.kind || jobs[k].E != p.E || jobs[k].M != p.M
-               || jobs[k].groups != p.groups || jobs[k].begin != p.begin)
+            const PackVParams& j = jobs[k];
+            if(j.w != p.w || j.kind != p.kind || j.E != p.E || j.M != p.M || j.groups != p.groups || j.begin != p.begin
+               || j.vbs != p.vbs || j.vl != p.vl || j.vsh != p.vsh)
                 return false;
-            m.q[k] = jobs[k];
+            m.vals[k] = j.vals;
+            m.bits[k] = j.bits;
+            m.vinb[k] = j.vinb;
+            m.sgn[k] = j.sgn;
         }
         switch(vsize)
         {
