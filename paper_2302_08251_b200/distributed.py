@@ -65,7 +65,9 @@ def all_gather_slot(buf, rank: int, world: int, group=None):
     per = buf.numel() // world
     slot = buf[rank * per:(rank + 1) * per]
     if buf.device.type == "cuda" and dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(buf, slot, group=group)
+        # a separate send buffer (per * elem bytes, 1.5 MiB / world at 128K) rather than relying
+        # on NCCL's in-place convention through a view of the output
+        dist.all_gather_into_tensor(buf, slot.clone(), group=group)
         return
     host = buf.cpu()
     dist.all_gather_into_tensor(host, host[rank * per:(rank + 1) * per].clone(), group=group)
