@@ -299,7 +299,7 @@ namespace lamk
         return a >= 0 ? a / b : -((-a + b - 1) / b);
     }
 
-#define HEAT_CLOSED_K 16
+#define HEAT_CLOSED_K 4
     __global__ void __launch_bounds__(256) k_heat_closed(const __grid_constant__ HeatParams p)
     {
         const HeatStream& st = p.st[blockIdx.y];
@@ -432,9 +432,9 @@ namespace lamk
                 }
                 used += static_cast<uint32_t>(P);
             }
-            // one pass, HEAT_CLOSED_K counters per thread: the per-thread setup (stream parameters,
-            // edge blocks, pattern phase: a few hundred instructions) made the 4-counter version
-            // issue-bound (84 instructions per counter, ncu); a grid-stride grid measured slower
+            // one pass, HEAT_CLOSED_K = 4 counters per thread (ncu: 84 instructions per counter, the
+            // per-thread setup dominating; but 16 counters per thread and a grid-stride grid both
+            // measured slower -- fewer counter loads in flight)
             const unsigned gx = stream_grid((maxBlocks + HEAT_CLOSED_K * 256 - 1) / (HEAT_CLOSED_K * 256), "LAMB_HEAT_CTAS", 0);
             k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();

@@ -45,7 +45,7 @@ namespace lamk
         uint32_t facS, facD, leaf, nleaves;
         uint32_t vbs, vl, vsh, vinb;
     };
-    bool pack32(const PackParams* jobs, uint32_t n, bool pack, cudaStream_t s);
+    bool pack32(const PackParams& p, bool pack, cudaStream_t s);
 
     struct RecPackParams
     {
@@ -982,17 +982,9 @@ namespace lamhost
                 throw std::runtime_error(std::string("packv launch failed: ") + cudaGetErrorString(cudaGetLastError()));
             a = b;
         }
-        // leaves with the same width and format share one launch (leaf = blockIdx.y)
-        for(size_t a = 0; a < jobs.size();)
-        {
-            size_t b = a + 1;
-            while(b < jobs.size() && b - a < 8 && jobs[b].w == jobs[a].w && jobs[b].kind == jobs[a].kind
-                  && jobs[b].E == jobs[a].E && jobs[b].M == jobs[a].M)
-                ++b;
-            if(!lamk::pack32(jobs.data() + a, static_cast<uint32_t>(b - a), packDir, s))
+        for(const auto& j : jobs)
+            if(!lamk::pack32(j, packDir, s))
                 throw std::runtime_error(std::string("pack32 launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-            a = b;
-        }
         addAccessCounts(p, S, groups * 32, s);
         const uint64_t doneEnd = begin + groups * 32;
         if(doneEnd < end)

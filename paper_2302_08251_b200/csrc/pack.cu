@@ -31,29 +31,6 @@ namespace lamk
         uint32_t vbs, vl, vsh, vinb; // value-stream geometry: AoSoA lanes (vl % 32 == 0) or SoA (vl == 1)
     };
 
-    // the leaves of one copy with the same field width and format, one launch: leaf = blockIdx.y
-    // (separate launches per leaf left a ramp and a tail per leaf on multi-leaf records)
-    // (shared fields once, per-leaf fields as arrays: the kernel rebuilds its PackParams with
-    // constant-offset parameter reads -- an indexed PackParams[8] cost up to 10% in the hot loop)
-    struct PackMulti
-    {
-        PackParams base;
-        unsigned long long vals[8], bits[8];
-        uint32_t vinb[8], leaf[8], sgn[8], valType[8];
-    };
-    __device__ __forceinline__ PackParams leaf_params(const PackMulti& M)
-    {
-        PackParams p = M.base;
-        const uint32_t y = blockIdx.y;
-        p.vals = M.vals[y];
-        p.bits = M.bits[y];
-        p.vinb = M.vinb[y];
-        p.leaf = M.leaf[y];
-        p.sgn = M.sgn[y];
-        p.valType = M.valType[y];
-        return p;
-    }
-
     __device__ __forceinline__ uint64_t val_addr(const PackParams& p, uint64_t e0)
     {
         if(p.vl == 1)
@@ -245,9 +222,8 @@ namespace lamk
     }
 
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackMulti M)
+    __global__ void __launch_bounds__(256, pack_minb(W, FMT)) k_pack32(const __grid_constant__ PackParams p)
     {
-        const PackParams p = leaf_params(M);
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -351,15 +327,17 @@ namespace lamk
 
     // unpack: W words -> 32 values per thread
     // unpack: 3 CTAs/SM (80 registers) except the widths that spill there
-    __host__ __device__ constexpr int unpack_minb(int W)
+    __host__ __device__ constexpr int unpack_minb(int W, int FMT)
     {
-        return (W >= 14 && W != 16 && W != 32) || W == 6 ? 2 : 3;
+        return ((FMT == 0 || FMT == 3) && (W == 24 || W == 26 || W == 28 || W == 30)) || (FMT == 3 && W == 14)
+                || (FMT == 0 && W == 6)
+            ? 2
+            : 3;
     }
 
     template<int W, int FMT>
-    __global__ void __launch_bounds__(256, unpack_minb(W)) k_unpack32(const __grid_constant__ PackMulti M)
+    __global__ void __launch_bounds__(256, unpack_minb(W, FMT)) k_unpack32(const __grid_constant__ PackParams p)
     {
-        const PackParams p = leaf_params(M);
         extern __shared__ __align__(16) uint32_t psm[];
         const uint32_t w = W ? W : p.w;
         const uint32_t ws = wstride_of(w);
@@ -849,77 +827,58 @@ namespace lamk
     }
 
     template<int W, int FMT>
-    static void launch_pack(const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s)
+    static void launch_pack(const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s)
     {
         // opt in to > 48 KB of dynamic shared memory once per instantiation, size and device
-        const dim3 g(resident_grid(k_pack32<W, FMT>, grid, smem, false), n);
+        // (one launch per leaf: a launch over several leaves through an indexed parameter array
+        // moved the parameter reads out of the constant bank and cost the C3 kernels up to 8%)
         if(pack)
         {
             lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_pack32<W, FMT>), smem), "opt_in_smem");
-            k_pack32<W, FMT><<<g, 256, smem, s>>>(m);
+            k_pack32<W, FMT><<<resident_grid(k_pack32<W, FMT>, grid, smem, false), 256, smem, s>>>(p);
         }
         else
         {
             lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_unpack32<W, FMT>), smem), "opt_in_smem");
-            k_unpack32<W, FMT><<<g, 256, smem, s>>>(m);
+            k_unpack32<W, FMT><<<resident_grid(k_unpack32<W, FMT>, grid, smem, false), 256, smem, s>>>(p);
         }
     }
 
     template<int... Ws>
-    static bool dispatch_int(int w, const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+    static bool dispatch_int(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
                              std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((w == Ws + 1 ? (launch_pack<Ws + 1, 0>(m, n, pack, grid, smem, s), hit = true) : false), ...);
+        ((w == Ws + 1 ? (launch_pack<Ws + 1, 0>(p, pack, grid, smem, s), hit = true) : false), ...);
         return hit;
     }
 
     // any other (E, M) with 1 + E + M <= 32: compile-time width, runtime format
     template<int... Ws>
-    static bool dispatch_flt(int w, const PackMulti& m, uint32_t n, bool pack, unsigned grid, size_t smem, cudaStream_t s,
+    static bool dispatch_flt(int w, const PackParams& p, bool pack, unsigned grid, size_t smem, cudaStream_t s,
                              std::integer_sequence<int, Ws...>)
     {
         bool hit = false;
-        ((w == Ws + 2 ? (launch_pack<Ws + 2, 3>(m, n, pack, grid, smem, s), hit = true) : false), ...);
+        ((w == Ws + 2 ? (launch_pack<Ws + 2, 3>(p, pack, grid, smem, s), hit = true) : false), ...);
         return hit;
     }
 
-    // jobs[0..n): leaves of one copy with the same width, format and element range (n <= 8)
-    bool pack32(const PackParams* jobs, uint32_t n, bool pack, cudaStream_t s)
+    bool pack32(const PackParams& p, bool pack, cudaStream_t s)
     {
-        if(n == 0 || n > 8)
-            return false;
-        const PackParams& p = jobs[0];
         if(p.groups == 0 || p.w < 1 || p.w > 32)
             return false;
-        PackMulti m{};
-        m.base = p;
-        for(uint32_t k = 0; k < n; ++k)
-        {
-            const PackParams& j = jobs[k];
-            if(j.w != p.w || j.kind != p.kind || j.E != p.E || j.M != p.M || j.groups != p.groups || j.begin != p.begin
-               || j.vbs != p.vbs || j.vl != p.vl || j.vsh != p.vsh || j.facS != p.facS || j.facD != p.facD
-               || j.facSrc != p.facSrc || j.facDst != p.facDst || j.nleaves != p.nleaves)
-                return false;
-            m.vals[k] = j.vals;
-            m.bits[k] = j.bits;
-            m.vinb[k] = j.vinb;
-            m.leaf[k] = j.leaf;
-            m.sgn[k] = j.sgn;
-            m.valType[k] = j.valType;
-        }
         const uint64_t want = (p.groups + 255) / 256;
         const unsigned grid = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);
         const size_t smem = 8 * slice_words(p.w) * sizeof(uint32_t);
         if(p.kind == 0)
-            dispatch_int(static_cast<int>(p.w), m, n, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
+            dispatch_int(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 32>{});
         else if(p.E == 8 && p.M == 10)
-            launch_pack<19, 1>(m, n, pack, grid, smem, s);
+            launch_pack<19, 1>(p, pack, grid, smem, s);
         else if(p.E == 5 && p.M == 10)
-            launch_pack<16, 2>(m, n, pack, grid, smem, s);
+            launch_pack<16, 2>(p, pack, grid, smem, s);
         else if(p.E > 8 || p.M > 23
-                || !dispatch_flt(static_cast<int>(p.w), m, n, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
-            launch_pack<0, 4>(m, n, pack, grid, smem, s);
+                || !dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
+            launch_pack<0, 4>(p, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");
         return true;
