@@ -29,5 +29,5 @@ if len(sys.argv) > 1:
     print(f"ALT={os.environ.get('LAMB_NB_ALT', '0')}: {ms:.3f} ms  {ips / 1e12:.3f}e12 inter/s  "
           f"{ips * 20 / 1e12 / 72.19:.4f} of 72.19 TF  pos rel err {perr:.2e}  vel rel err {verr:.2e}", flush=True)
 else:
-    for alt in ("0", "1", "9", "0", "1", "9"):
+    for alt in sys.argv[2:] if len(sys.argv) > 2 else ("0", "1", "8", "1", "8"):
         subprocess.run([sys.executable, __file__, "run"], env=dict(os.environ, LAMB_NB_ALT=alt), check=True)
