@@ -824,7 +824,25 @@ namespace lamhost
         if(!side(true, rp.s, rp.ns) || !side(false, rp.d, rp.nd))
             return false;
         rp.preload = p.dst_holes ? 1 : 0;
-        rp.rowWords = (row / 4) | 1u;
+        // flatten the spans into 16-byte vectors (all in flight at once in the kernel)
+        auto vecs = [&](const lamk::RPSpan* sp, uint32_t n, lamk::RPSpan* out, uint32_t& nv) -> bool
+        {
+            for(uint32_t k = 0; k < n; ++k)
+                for(uint32_t off = 0; off < sp[k].len; off += 16)
+                {
+                    if(nv >= RP_MAXV)
+                        return false;
+                    out[nv] = sp[k];
+                    out[nv].base += off;
+                    out[nv].row += off;
+                    ++nv;
+                }
+            return true;
+        };
+        if(!vecs(rp.s, rp.ns, rp.vin, rp.nvin) || (rp.preload && !vecs(rp.d, rp.nd, rp.vin, rp.nvin))
+           || !vecs(rp.d, rp.nd, rp.vout, rp.nvout))
+            return false;
+        rp.rowWords = (row / 4 + 1) | 1u; // +1: the funnel shift may read one word past a value
         rp.nl = nl;
         rp.begin = begin;
         rp.groups = (end - begin) / RP_G;

@@ -76,12 +76,16 @@ namespace lamk
         uint32_t srow, slsh, slmask, sbs, sls;
         uint32_t drow, dlsh, dlmask, dbs, dls;
     };
+#define RP_MAXV 32
     struct RPParams
     {
         RPSpan s[16], d[16];
         RPLeaf leaf[16];
         uint32_t ns, nd, nl, rowWords, preload;
         unsigned long long begin, groups; // groups of RP_G elements
+        // the spans as 16-byte vectors: loaded (source, + destination when it has holes), stored
+        RPSpan vin[RP_MAXV], vout[RP_MAXV];
+        uint32_t nvin, nvout;
     };
     bool row_permute(const RPParams& p, cudaStream_t s);
 

@@ -8,8 +8,9 @@
 // A thread owns G = 16 consecutive elements.  For every stream of each side the bytes of those
 // elements form one contiguous, 16-byte aligned span (a record stream or AoSoA<L> with L | 16:
 // 16/L blocks; an AoSoA<L> with 16 | L or SoA: one run of 16 values per leaf), loaded with 16-byte
-// vectors into the thread's private shared-memory row (odd word stride: conflict-free), the leaf
-// values moved inside the row (4-byte moves where both offsets allow, else bytes), and the
+// vectors into the thread's private shared-memory row (odd word stride: conflict-free; every
+// vector of the group in flight at once), the leaf values moved inside the row (word-aligned
+// destinations: one funnel shift per word from any source offset; else bytes), and the
 // destination spans written back with 16-byte vectors.  A destination with bytes copyView never
 // writes (padding) is read into the row first, so whole-span stores keep those bytes.
 #include "device_common.cuh"
@@ -17,11 +18,6 @@
 
 namespace lamk
 {
-    __device__ __forceinline__ uint64_t rp_span_addr(const RPSpan& s, uint64_t e0)
-    {
-        return s.base + (e0 >> s.lsh) * s.bs + (e0 & s.lmask) * s.ls;
-    }
-
     __global__ void __launch_bounds__(64) k_row_permute(const __grid_constant__ RPParams p)
     {
         extern __shared__ __align__(16) uint32_t rsm[];
@@ -31,38 +27,25 @@ namespace lamk
         for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < p.groups; g += stride)
         {
             const uint64_t e0 = p.begin + g * RP_G;
-            // ---- spans -> row (source; destination too when it has holes) ----
-            const uint32_t nin = p.ns + (p.preload ? p.nd : 0);
-            for(uint32_t sp = 0; sp < nin; ++sp)
+            // ---- spans -> row (source; destination too when it has holes): every 16-byte vector
+            // of the group in flight at once (RP_MAXV at most), then into the row ----
             {
-                const RPSpan& s = sp < p.ns ? p.s[sp] : p.d[sp - p.ns];
-                const uint4* src = reinterpret_cast<const uint4*>(rp_span_addr(s, e0));
-                uint32_t* at = row + s.row / 4;
-                const uint32_t nv = s.len / 16;
-                uint32_t k = 0;
-                for(; k + 4 <= nv; k += 4)
-                {
-                    uint4 x[4];
+                uint4 x[RP_MAXV];
 #pragma unroll
-                    for(int u = 0; u < 4; ++u)
-                        x[u] = __ldcs(src + k + u);
+                for(int k = 0; k < RP_MAXV; ++k)
+                    if(k < static_cast<int>(p.nvin))
+                        x[k] = __ldcs(reinterpret_cast<const uint4*>(p.vin[k].base + (e0 >> p.vin[k].lsh) * p.vin[k].bs
+                                                                     + (e0 & p.vin[k].lmask) * p.vin[k].ls));
 #pragma unroll
-                    for(int u = 0; u < 4; ++u)
+                for(int k = 0; k < RP_MAXV; ++k)
+                    if(k < static_cast<int>(p.nvin))
                     {
-                        at[4 * (k + u)] = x[u].x;
-                        at[4 * (k + u) + 1] = x[u].y;
-                        at[4 * (k + u) + 2] = x[u].z;
-                        at[4 * (k + u) + 3] = x[u].w;
+                        uint32_t* at = row + p.vin[k].row / 4;
+                        at[0] = x[k].x;
+                        at[1] = x[k].y;
+                        at[2] = x[k].z;
+                        at[3] = x[k].w;
                     }
-                }
-                for(; k < nv; ++k)
-                {
-                    const uint4 x = __ldcs(src + k);
-                    at[4 * k] = x.x;
-                    at[4 * k + 1] = x.y;
-                    at[4 * k + 2] = x.z;
-                    at[4 * k + 3] = x.w;
-                }
             }
             // ---- leaf values: source row bytes -> destination row bytes ----
             for(uint32_t f = 0; f < p.nl; ++f)
@@ -75,24 +58,30 @@ namespace lamk
                     const uint32_t d = L.drow + (j >> L.dlsh) * L.dbs + (j & L.dlmask) * L.dls;
                     if(L.isBool)
                         rb[d] = rb[so] != 0;
-                    else if(L.size >= 4 && ((so | d) & 3) == 0)
-                        for(uint32_t b = 0; b < L.size; b += 4)
-                            row[(d + b) / 4] = row[(so + b) / 4];
+                    else if(L.size >= 4 && (d & 3) == 0)
+                    {
+                        // word-aligned destination: each word from the (possibly unaligned) source
+                        // by one funnel shift of the two words covering it
+                        const uint32_t sh = (so & 3) * 8;
+                        const uint32_t* sw = row + so / 4;
+                        for(uint32_t b = 0; b < L.size / 4; ++b)
+                            row[d / 4 + b] = sh ? __funnelshift_r(sw[b], sw[b + 1], sh) : sw[b];
+                    }
                     else
                         for(uint32_t b = 0; b < L.size; ++b)
                             rb[d + b] = rb[so + b];
                 }
             }
             // ---- destination row -> spans ----
-            for(uint32_t sp = 0; sp < p.nd; ++sp)
-            {
-                const RPSpan& s = p.d[sp];
-                uint4* dst = reinterpret_cast<uint4*>(rp_span_addr(s, e0));
-                const uint32_t* at = row + s.row / 4;
-                const uint32_t nv = s.len / 16;
-                for(uint32_t k = 0; k < nv; ++k)
-                    __stcs(dst + k, make_uint4(at[4 * k], at[4 * k + 1], at[4 * k + 2], at[4 * k + 3]));
-            }
+#pragma unroll
+            for(int k = 0; k < RP_MAXV; ++k)
+                if(k < static_cast<int>(p.nvout))
+                {
+                    const uint32_t* at = row + p.vout[k].row / 4;
+                    __stcs(reinterpret_cast<uint4*>(p.vout[k].base + (e0 >> p.vout[k].lsh) * p.vout[k].bs
+                                                    + (e0 & p.vout[k].lmask) * p.vout[k].ls),
+                           make_uint4(at[0], at[1], at[2], at[3]));
+                }
         }
     }
 
