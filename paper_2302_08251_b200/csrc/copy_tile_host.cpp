@@ -729,134 +729,6 @@ namespace lamhost
         return true;
     }
 
-    // Physical pairs with mixed leaf sizes / padding / unaligned packed leaves (row_permute.cu):
-    // every leaf a same-size physical move without conversion, every stream either a record stream
-    // or AoSoA<L> with L | 16 (16 elements = whole blocks) or with 16 | L (lane runs per leaf).
-    static bool tryRowPermute(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si,
-                              DeviceImage& di, const Lowered& S, const Lowered& D, cudaStream_t s)
-    {
-        const uint32_t nl = p.nleaves;
-        if(nl < 1 || nl > 16 || begin % RP_G || envNum("LAMB_ROW_PERMUTE", 1) == 0)
-            return false;
-        for(uint32_t f = 0; f < nl; ++f)
-        {
-            const lamt_leaf& L = p.leaf[f];
-            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != L.d[0].size || L.stype != L.dtype
-               || L.stype != L.ltype)
-                return false;
-        }
-        lamk::RPParams rp{};
-        uint32_t row = 0;
-        auto side = [&](bool src, lamk::RPSpan* spans, uint32_t& nsp) -> bool
-        {
-            int spanOfStream[LAMT_MAX_STREAMS];
-            for(int& x : spanOfStream)
-                x = -1;
-            for(uint32_t f = 0; f < nl; ++f)
-            {
-                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
-                const lamt_stream& st = p.st[t.stream];
-                const uint32_t L = st.lanes, sz = t.size;
-                lamk::RPLeaf& lf = rp.leaf[f];
-                lf.size = sz;
-                lf.isBool = p.leaf[f].ltype == Bool;
-                uint32_t& lrow = src ? lf.srow : lf.drow;
-                uint32_t& llsh = src ? lf.slsh : lf.dlsh;
-                uint32_t& llmask = src ? lf.slmask : lf.dlmask;
-                uint32_t& lbs = src ? lf.sbs : lf.dbs;
-                uint32_t& lls = src ? lf.sls : lf.dls;
-                if(L > 1 && st.lshift == 0xFFFFFFFFu)
-                    return false; // non-power-of-two lanes
-                if(RP_G % L == 0)
-                {
-                    // the 16 elements are 16 / L whole blocks of this stream: one span per stream
-                    if(spanOfStream[t.stream] < 0)
-                    {
-                        if(nsp >= 16)
-                            return false;
-                        lamk::RPSpan& sp = spans[nsp];
-                        sp.base = st.gptr;
-                        sp.bs = st.bs;
-                        sp.lsh = L == 1 ? 0 : st.lshift;
-                        sp.lmask = 0;
-                        sp.ls = 0;
-                        sp.len = RP_G / L * st.bs;
-                        sp.row = row;
-                        if(sp.base % 16 || sp.len % 16)
-                            return false;
-                        row += sp.len;
-                        spanOfStream[t.stream] = static_cast<int>(nsp++);
-                    }
-                    const lamk::RPSpan& sp = spans[spanOfStream[t.stream]];
-                    lrow = sp.row + t.inblock;
-                    llsh = L == 1 ? 0 : st.lshift;
-                    llmask = L - 1;
-                    lbs = st.bs;
-                    lls = L == 1 ? 0 : t.ls;
-                }
-                else if(L % RP_G == 0)
-                {
-                    // a run of 16 values of this leaf inside one block: one span per leaf
-                    if(nsp >= 16)
-                        return false;
-                    lamk::RPSpan& sp = spans[nsp++];
-                    sp.base = st.gptr + t.inblock;
-                    sp.bs = st.bs;
-                    sp.lsh = st.lshift;
-                    sp.lmask = L - 1;
-                    sp.ls = t.ls;
-                    sp.len = RP_G * sz;
-                    sp.row = row;
-                    if(sp.base % 16 || sp.len % 16 || t.ls != sz)
-                        return false;
-                    row += sp.len;
-                    lrow = sp.row;
-                    llsh = 0;
-                    llmask = 0;
-                    lbs = sz;
-                    lls = 0;
-                }
-                else
-                    return false;
-            }
-            return true;
-        };
-        if(!side(true, rp.s, rp.ns) || !side(false, rp.d, rp.nd))
-            return false;
-        rp.preload = p.dst_holes ? 1 : 0;
-        // flatten the spans into 16-byte vectors (all in flight at once in the kernel)
-        auto vecs = [&](const lamk::RPSpan* sp, uint32_t n, lamk::RPSpan* out, uint32_t& nv) -> bool
-        {
-            for(uint32_t k = 0; k < n; ++k)
-                for(uint32_t off = 0; off < sp[k].len; off += 16)
-                {
-                    if(nv >= RP_MAXV)
-                        return false;
-                    out[nv] = sp[k];
-                    out[nv].base += off;
-                    out[nv].row += off;
-                    ++nv;
-                }
-            return true;
-        };
-        if(!vecs(rp.s, rp.ns, rp.vin, rp.nvin) || (rp.preload && !vecs(rp.d, rp.nd, rp.vin, rp.nvin))
-           || !vecs(rp.d, rp.nd, rp.vout, rp.nvout))
-            return false;
-        rp.rowWords = (row / 4 + 1) | 1u; // +1: the funnel shift may read one word past a value
-        rp.nl = nl;
-        rp.begin = begin;
-        rp.groups = (end - begin) / RP_G;
-        if(rp.groups == 0 || static_cast<size_t>(64) * rp.rowWords * 4 > 200 * 1024 || !lamk::row_permute(rp, s))
-            return false;
-        addAccessCounts(p, S, rp.groups * RP_G, s);
-        const uint64_t doneEnd = begin + rp.groups * RP_G;
-        if(doneEnd < end)
-            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s, false),
-                           "generic_copy(tail)");
-        return true;
-    }
-
     // ChangeType f32 <-> f64 over uniform geometries (vec_transpose.cu k_vec_convert): every leaf
     // PHYS -> PHYS with source size SS and destination size DS (4 <-> 8), one conversion
     // f32 -> f64 or f64 -> f32 between them; each side record-contiguous or leaf-contiguous.
@@ -1326,8 +1198,7 @@ namespace lamhost
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
         if(p.dst_holes)
-            return tryRowPermute(p, begin, end, si, di, S, D, s)
-                || (envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s));
+            return envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s);
         if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
@@ -1337,8 +1208,6 @@ namespace lamhost
         if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryVecMulti(p, begin, end, si, di, S, D, s))
-            return true;
-        if(!p.uni && tryRowPermute(p, begin, end, si, di, S, D, s))
             return true;
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /

@@ -59,35 +59,6 @@ namespace lamk
     };
     bool vec_multi(const VMParams& p, uint32_t leafSize, cudaStream_t s);
 
-    // byte-permutation copy through per-thread rows (row_permute.cu): G = 16 elements per thread
-#define RP_G 16
-    struct RPSpan
-    {
-        // bytes of elements [e0, e0 + 16) of a stream (or of one leaf's lane run) at
-        // base + (e0 >> lsh) * bs + (e0 & lmask) * ls, len bytes, at byte `row` of the thread row
-        unsigned long long base;
-        uint32_t bs, lsh, lmask, ls, len, row;
-    };
-    struct RPLeaf
-    {
-        // value of element j: row byte srow + (j >> slsh) * sbs + (j & slmask) * sls (source),
-        // likewise d* (destination); size bytes; bool leaves are canonicalised
-        uint32_t size, isBool;
-        uint32_t srow, slsh, slmask, sbs, sls;
-        uint32_t drow, dlsh, dlmask, dbs, dls;
-    };
-#define RP_MAXV 32
-    struct RPParams
-    {
-        RPSpan s[16], d[16];
-        RPLeaf leaf[16];
-        uint32_t ns, nd, nl, rowWords, preload;
-        unsigned long long begin, groups; // groups of RP_G elements
-        // the spans as 16-byte vectors: loaded (source, + destination when it has holes), stored
-        RPSpan vin[RP_MAXV], vout[RP_MAXV];
-        uint32_t nvin, nvout;
-    };
-    bool row_permute(const RPParams& p, cudaStream_t s);
 
     int sm_count(int device);
 
