@@ -368,7 +368,7 @@ def _c2_slices(layout, n, a, c):
     return [(0, 4 * n * f + 4 * a, 4 * n * f + 4 * (a + c), 0, 4 * c * f, 4 * c * (f + 1)) for f in range(7)]
 
 
-def run_c4_strong(L, world, rank, local, steps=5, warmup=2, n=128 * 1024, layout="soa-mb"):
+def run_c4_strong(L, world, rank, local, steps=10, warmup=5, n=128 * 1024, layout="soa-mb"):
     """C4 strong scaling: 128K particles TOTAL split over the ranks (i-range shards), per step
     update + move + the positions-only all-gather (distributed.py; one collective of 12 B per
     particle, Mass once).  Step time = max over ranks of the per-step CUDA-event time."""
