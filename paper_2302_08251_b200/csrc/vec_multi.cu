@@ -24,8 +24,11 @@ namespace lamk
         return sd.base[f] + (e0 >> sd.lsh[f]) * sd.bs[f] + (e0 & sd.lmask[f]) * S;
     }
 
+    // 5 CTAs/SM (<= 102 registers): ncu showed the kernel latency-bound at 4 (128 registers);
+    // 6 spilled the 7- and 8-leaf instantiations
+#define VMB 5
     template<int NL, int V>
-    __global__ void __launch_bounds__(128) k_vec_multi(const __grid_constant__ VMParams p)
+    __global__ void __launch_bounds__(128, VMB) k_vec_multi(const __grid_constant__ VMParams p)
     {
         constexpr int S = 16 / V;  // leaf bytes
         constexpr int WPE = S / 4; // 32-bit words per value
