@@ -15,6 +15,9 @@ PAIRS = [
     (R32, "split:Pos:soa-mb:aos-packed", "aos-packed", 0), (R32, "soa-mb", "split:Pos:soa-mb:aos-packed", 0),
     (R32, "aosoa:8", "split:Vel:aosoa:8:soa-mb", 0), (R32, "split:Pos,Mass:aosoa:4:soa-sb", "aos-packed", 0),
     (R32, "aos-packed", "split:Vel:aos-packed:aos-packed", 0), (R64, "aos-packed", "split:Pos:soa-mb:aos-packed", 0),
+    # AoSoA with lane counts no vector group fits (k_vec_rows)
+    (R32, "aosoa:3", "aos-packed", 0), (R32, "soa-mb", "aosoa:3", 0), (R32, "aosoa:6", "soa-sb", 0),
+    (R32, "aosoa:32", "aosoa:3", 0), (R64, "aos-packed", "aosoa:3", 0),
 ]
 for schema, a, b, wrap in PAIRS:
     la, lb = L.Layout(schema, f"i32:[{n}]", a), L.Layout(schema, f"i32:[{n}]", b, wrap=wrap, granularity=64)
