@@ -729,116 +729,6 @@ namespace lamhost
         return true;
     }
 
-    // Uniform physical pairs with AoSoA lane counts no vector group fits (aosoa:3, :6): groups of
-    // G = 3V elements through per-thread rows (vec_multi.cu k_vec_rows).  Every stream must hold
-    // the G elements as whole blocks (G % L == 0; destinations fully covered by their leaves) or
-    // as one lane run per leaf (L % G == 0, power of two).
-    static bool tryVecRows(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
-                           const Lowered& S, const Lowered& D, cudaStream_t s)
-    {
-        const uint32_t nl = p.nleaves;
-        if(nl < 1 || nl > 8 || envNum("LAMB_VEC_ROWS", 1) == 0)
-            return false;
-        const uint32_t sz = p.leaf[0].s[0].size;
-        if(sz != 4 && sz != 8)
-            return false;
-        const uint32_t V = 16 / sz, G = 3 * V;
-        if(begin % G)
-            return false;
-        for(uint32_t f = 0; f < nl; ++f)
-        {
-            const lamt_leaf& L = p.leaf[f];
-            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != sz || L.d[0].size != sz
-               || L.stype != L.dtype || L.stype != L.ltype || L.ltype == Bool)
-                return false;
-        }
-        lamk::VRParams vr{};
-        uint32_t row = 0; // words
-        auto side = [&](bool src, lamk::VRVec* vecs, uint32_t& nv, uint16_t (*off)[12]) -> bool
-        {
-            int rowOfStream[LAMT_MAX_STREAMS];
-            uint32_t covered[LAMT_MAX_STREAMS] = {};
-            for(int& x : rowOfStream)
-                x = -1;
-            for(uint32_t f = 0; f < nl; ++f)
-            {
-                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
-                const lamt_stream& st = p.st[t.stream];
-                const uint32_t L = st.lanes;
-                if(G % L == 0)
-                {
-                    if(rowOfStream[t.stream] < 0)
-                    {
-                        const uint64_t span = uint64_t(G / L) * st.bs;
-                        if(span % 16 || st.gptr % 16 || nv + span / 16 > 24)
-                            return false;
-                        for(uint32_t k = 0; k < span / 16; ++k)
-                        {
-                            lamk::VRVec& v = vecs[nv++];
-                            v.base = st.gptr + (begin / L) * st.bs + 16ull * k;
-                            v.gstride = span;
-                            v.lsh = 64;
-                            v.row = row + 4 * k;
-                        }
-                        rowOfStream[t.stream] = static_cast<int>(row);
-                        row += static_cast<uint32_t>(span / 4);
-                    }
-                    if(t.inblock % 4 || (L > 1 && t.ls != sz))
-                        return false;
-                    covered[t.stream] += L * sz;
-                    for(uint32_t j = 0; j < G; ++j)
-                        off[f][j] = static_cast<uint16_t>(rowOfStream[t.stream]
-                                                          + ((j / L) * st.bs + t.inblock + (j % L) * sz) / 4);
-                }
-                else if(L % G == 0 && st.lshift != 0xFFFFFFFFu && t.ls == sz)
-                {
-                    // one run of G values of this leaf inside a block: 3 vectors
-                    const uint64_t b0 = st.gptr + t.inblock;
-                    if(b0 % 16 || nv + 3 > 24)
-                        return false;
-                    for(uint32_t k = 0; k < 3; ++k)
-                    {
-                        lamk::VRVec& v = vecs[nv++];
-                        v.base = b0 + 16ull * k;
-                        v.lsh = st.lshift;
-                        v.lmask = L - 1;
-                        v.bs = st.bs;
-                        v.ls = sz;
-                        v.row = row + 4 * k;
-                    }
-                    for(uint32_t j = 0; j < G; ++j)
-                        off[f][j] = static_cast<uint16_t>(row + j * sz / 4);
-                    row += 12;
-                }
-                else
-                    return false;
-            }
-            // whole-block stores: a destination block stream must be covered by its leaves
-            if(!src)
-                for(uint32_t k = 0; k < LAMT_MAX_STREAMS; ++k)
-                    if(rowOfStream[k] >= 0 && covered[k] != p.st[k].bs)
-                        return false;
-            return true;
-        };
-        if(!side(true, vr.vin, vr.nvin, vr.soff) || !side(false, vr.vout, vr.nvout, vr.doff))
-            return false;
-        if(row > 65000)
-            return false;
-        vr.rowWords = row | 1u;
-        vr.nl = nl;
-        vr.begin = begin;
-        vr.groups = (end - begin) / G;
-        if(vr.groups == 0 || !lamk::vec_rows(vr, sz, s))
-            return false;
-        addAccessCounts(p, S, vr.groups * G, s);
-        const uint64_t doneEnd = begin + vr.groups * G;
-        if(doneEnd < end)
-            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
-                                              D.fac, s, false),
-                           "generic_copy(tail)");
-        return true;
-    }
-
     // ChangeType f32 <-> f64 over uniform geometries (vec_transpose.cu k_vec_convert): every leaf
     // PHYS -> PHYS with source size SS and destination size DS (4 <-> 8), one conversion
     // f32 -> f64 or f64 -> f32 between them; each side record-contiguous or leaf-contiguous.
@@ -1322,8 +1212,6 @@ namespace lamhost
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /
         // lane by a magic multiply -- measured 1.7x over the warp-tile transpose (aosoa:2, aosoa:3)
-        if(tryVecRows(p, begin, end, si, di, S, D, s))
-            return true;
         const uint64_t maxL = std::max<uint64_t>(std::max<uint64_t>(p.ul_s, p.ul_d), 1);
         if(p.uni && envNum("LAMB_DIRECT", 1) != 0 && end < (uint64_t{1} << 32) / maxL)
         {

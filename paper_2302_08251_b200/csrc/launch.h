@@ -59,21 +59,6 @@ namespace lamk
     };
     bool vec_multi(const VMParams& p, uint32_t leafSize, cudaStream_t s);
 
-    // uniform pairs in groups of 3V elements through per-thread rows (vec_multi.cu k_vec_rows)
-    struct VRVec
-    {
-        // block stream (lsh == 64): base + g * gstride ; lane run: base + (e0 >> lsh) * bs + (e0 & lmask) * ls
-        unsigned long long base, gstride;
-        uint32_t lsh, lmask, bs, ls, row; // row: word offset of the vector in the thread row
-    };
-    struct VRParams
-    {
-        VRVec vin[24], vout[24];
-        uint32_t nvin, nvout, nl, rowWords;
-        uint16_t soff[8][12], doff[8][12]; // word offset of leaf f, element j in the row
-        unsigned long long begin, groups;  // groups of 3V elements
-    };
-    bool vec_rows(const VRParams& p, uint32_t leafSize, cudaStream_t s);
 
 
     int sm_count(int device);

@@ -204,105 +204,3 @@ namespace lamk
         return true;
     }
 } // namespace lamk
-
-namespace lamk
-{
-    // ---- uniform pairs with AoSoA<L> lane counts that are not a multiple of V (aosoa:3, :6):
-    // a thread owns G = 3V consecutive elements, so every stream's bytes for them are whole
-    // blocks (G % L == 0) or whole lane runs (L % G == 0); every 16-byte vector of the group is
-    // loaded at once into the thread's row, each value moves row -> row at offsets the host
-    // tabulated per leaf and element (no division by L in the kernel), and the destination
-    // vectors leave from the row.  k_uniform_direct (4-byte gathers through L1) reached 70%.
-    __device__ __forceinline__ uint64_t vr_addr(const VRVec& v, uint64_t g, uint64_t e0)
-    {
-        return v.lsh == 64 ? v.base + g * v.gstride : v.base + (e0 >> v.lsh) * v.bs + (e0 & v.lmask) * v.ls;
-    }
-
-    template<int NL, int V>
-    __global__ void __launch_bounds__(128, 2) k_vec_rows(const __grid_constant__ VRParams p)
-    {
-        constexpr int G = 3 * V, S = 16 / V, WPE = S / 4, NVMAX = 3 * NL;
-        extern __shared__ __align__(16) uint32_t vrsm[];
-        uint32_t* row = vrsm + threadIdx.x * p.rowWords;
-        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < p.groups; g += stride)
-        {
-            const uint64_t e0 = p.begin + g * G;
-            {
-                uint4 x[NVMAX];
-#pragma unroll
-                for(int k = 0; k < NVMAX; ++k)
-                    if(k < static_cast<int>(p.nvin))
-                        x[k] = __ldcs(reinterpret_cast<const uint4*>(vr_addr(p.vin[k], g, e0)));
-#pragma unroll
-                for(int k = 0; k < NVMAX; ++k)
-                    if(k < static_cast<int>(p.nvin))
-                    {
-                        uint32_t* at = row + p.vin[k].row;
-                        at[0] = x[k].x;
-                        at[1] = x[k].y;
-                        at[2] = x[k].z;
-                        at[3] = x[k].w;
-                    }
-            }
-#pragma unroll
-            for(int f = 0; f < NL; ++f)
-            {
-#pragma unroll
-                for(int j = 0; j < G; ++j)
-                {
-                    const uint32_t so = p.soff[f][j], d = p.doff[f][j];
-                    row[d] = row[so];
-                    if constexpr(WPE == 2)
-                        row[d + 1] = row[so + 1];
-                }
-            }
-#pragma unroll
-            for(int k = 0; k < NVMAX; ++k)
-                if(k < static_cast<int>(p.nvout))
-                {
-                    const uint32_t* at = row + p.vout[k].row;
-                    __stcs(reinterpret_cast<uint4*>(vr_addr(p.vout[k], g, e0)), make_uint4(at[0], at[1], at[2], at[3]));
-                }
-        }
-    }
-
-    template<int V>
-    static bool launch_rows_v(const VRParams& p, cudaStream_t s)
-    {
-        const size_t smem = static_cast<size_t>(128) * p.rowWords * sizeof(uint32_t);
-        if(smem > 200 * 1024)
-            return false;
-        const unsigned grid = stream_grid((p.groups + 127) / 128, "LAMB_VEC_CTAS", 0);
-        auto go = [&](auto kern)
-        {
-            lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(kern), smem), "opt_in_smem");
-            kern<<<grid, 128, smem, s>>>(p);
-        };
-        switch(p.nl)
-        {
-        case 1: go(k_vec_rows<1, V>); break;
-        case 2: go(k_vec_rows<2, V>); break;
-        case 3: go(k_vec_rows<3, V>); break;
-        case 4: go(k_vec_rows<4, V>); break;
-        case 5: go(k_vec_rows<5, V>); break;
-        case 6: go(k_vec_rows<6, V>); break;
-        case 7: go(k_vec_rows<7, V>); break;
-        case 8: go(k_vec_rows<8, V>); break;
-        default: return false;
-        }
-        return true;
-    }
-
-    bool vec_rows(const VRParams& p, uint32_t leafSize, cudaStream_t s)
-    {
-        if(p.groups == 0)
-            return false;
-        const bool ok = leafSize == 4 ? launch_rows_v<4>(p, s) : leafSize == 8 ? launch_rows_v<2>(p, s) : false;
-        if(!ok)
-            return false;
-        count_launch();
-        lam_cuda_check(cudaGetLastError(), "kernel launch");
-        return true;
-    }
-} // namespace lamk
