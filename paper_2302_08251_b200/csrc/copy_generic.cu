@@ -10,6 +10,7 @@
 
 #include <cstdlib>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -315,31 +316,25 @@ namespace lamk
         // HEAT_K loads are in flight together (one 8-byte RMW per thread left the pass latency-bound
         // at ~2 TB/s of counter traffic)
         constexpr int HEAT_K = HEAT_CLOSED_K;
-        for(int64_t bq = first + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * HEAT_K; bq <= last;
-            bq += static_cast<int64_t>(gridDim.x) * blockDim.x * HEAT_K)
+        // streams with a count pattern: k_heat_pattern streams their interior [pLo, pHi]; this
+        // kernel walks only the edge blocks (virtual index v -> block: below pLo, then above pHi)
+        (void)invP;
+        const int64_t nLow = P ? st.pLo - first : 0;
+        const int64_t nv = P ? nLow + (last - st.pHi) : last - first + 1;
+        auto blockOf = [&](int64_t v) { return P == 0 ? first + v : (v < nLow ? first + v : st.pHi + 1 + (v - nLow)); };
+        for(int64_t vq = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * HEAT_K; vq < nv;
+            vq += static_cast<int64_t>(gridDim.x) * blockDim.x * HEAT_K)
         {
             unsigned long long c[HEAT_K], h[HEAT_K];
-            // interior blocks: the periodic pattern (one modulo per thread, then increments)
-            int64_t m = 0;
-            const bool inner = P != 0 && bq >= st.pLo && bq + HEAT_K - 1 <= st.pHi;
-            if(inner)
-            {
-                m = bq - st.pb0;
-                m -= floor_div_r(m, P, invP) * P;
-            }
+            int64_t bk[HEAT_K];
 #pragma unroll
             for(int k = 0; k < HEAT_K; ++k)
             {
-                const int64_t b = bq + k;
+                const int64_t b = blockOf(vq + k);
+                bk[k] = b;
                 c[k] = 0;
-                if(b > last)
+                if(vq + k >= nv || b > last)
                     continue;
-                if(inner)
-                {
-                    c[k] = p.pattern[st.patOff + m];
-                    m = m + 1 == P ? 0 : m + 1;
-                    continue;
-                }
                 for(uint32_t t = st.t0; t < st.t1; ++t)
                 {
                     const HeatTerm& ht = p.term[t];
@@ -356,19 +351,49 @@ namespace lamk
 #pragma unroll
             for(int k = 0; k < HEAT_K; ++k)
             {
-                const int64_t b = bq + k;
+                const int64_t b = bk[k];
                 h[k] = (c[k] && b != first && b != last) ? heat[b] : 0;
             }
 #pragma unroll
             for(int k = 0; k < HEAT_K; ++k)
             {
-                const int64_t b = bq + k;
+                const int64_t b = bk[k];
                 if(!c[k])
                     continue;
                 if(b == first || b == last)
                     atomicAdd(heat + b, c[k]); // edge blocks may be shared with another stream
                 else
                     heat[b] = h[k] + c[k];
+            }
+        }
+    }
+
+    // interior heat blocks of the streams with a count pattern: a streaming read-modify-write,
+    // 8 independent counters per thread, counts from the period table (no per-block formula)
+    __global__ void __launch_bounds__(256) k_heat_pattern(const __grid_constant__ HeatParams p)
+    {
+        const HeatStream& st = p.st[blockIdx.y];
+        const int64_t P = st.period;
+        if(P == 0)
+            return;
+        unsigned long long* heat = p.heat + p.heatOff[st.nr];
+        const double invP = 1.0 / static_cast<double>(P);
+        constexpr int K = 8;
+        for(int64_t bq = st.pLo + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * K; bq <= st.pHi;
+            bq += static_cast<int64_t>(gridDim.x) * blockDim.x * K)
+        {
+            int64_t m = bq - st.pb0;
+            m -= floor_div_r(m, P, invP) * P;
+            unsigned long long h[K];
+#pragma unroll
+            for(int k = 0; k < K; ++k)
+                h[k] = bq + k <= st.pHi ? heat[bq + k] : 0;
+#pragma unroll
+            for(int k = 0; k < K; ++k)
+            {
+                if(bq + k <= st.pHi)
+                    heat[bq + k] = h[k] + p.pattern[st.patOff + m];
+                m = m + 1 == P ? 0 : m + 1;
             }
         }
     }
@@ -435,7 +460,22 @@ namespace lamk
             // one pass, HEAT_CLOSED_K = 4 counters per thread (ncu: 84 instructions per counter, the
             // per-thread setup dominating; but 16 counters per thread and a grid-stride grid both
             // measured slower -- fewer counter loads in flight)
-            const unsigned gx = stream_grid((maxBlocks + HEAT_CLOSED_K * 256 - 1) / (HEAT_CLOSED_K * 256), "LAMB_HEAT_CTAS", 0);
+            uint64_t maxInterior = 0, maxRest = 0;
+            for(uint32_t k = 0; k < q.nstreams; ++k)
+            {
+                const HeatStream& st = q.st[k];
+                const uint64_t span = ((st.base0 + p.end * st.bs - 1) / p.gran) - ((st.base0 + p.begin * st.bs) / p.gran) + 1;
+                const uint64_t inner = st.period ? static_cast<uint64_t>(st.pHi - st.pLo + 1) : 0;
+                maxInterior = std::max(maxInterior, inner);
+                maxRest = std::max(maxRest, span - inner);
+            }
+            if(maxInterior)
+            {
+                const unsigned gp = stream_grid((maxInterior + 8 * 256 - 1) / (8 * 256), "LAMB_HEAT_CTAS", 0);
+                k_heat_pattern<<<dim3(gp, q.nstreams), 256, 0, s>>>(q);
+                count_launch();
+            }
+            const unsigned gx = stream_grid((maxRest + HEAT_CLOSED_K * 256 - 1) / (HEAT_CLOSED_K * 256), "LAMB_HEAT_CTAS", 0);
             k_heat_closed<<<dim3(gx, q.nstreams), 256, 0, s>>>(q);
             count_launch();
             return cudaGetLastError();
