@@ -368,32 +368,42 @@ namespace lamk
         }
     }
 
-    // interior heat blocks of the streams with a count pattern: a streaming read-modify-write,
-    // 8 independent counters per thread, counts from the period table (no per-block formula)
+    // interior heat blocks of the streams with a count pattern: a streaming read-modify-write.
+    // A warp owns 32 * K consecutive counters, lane l the counters l, l + 32, ... (every load and
+    // store instruction is 256 contiguous bytes); the period table is copied to shared memory
+    // (per-lane indices into the constant bank would serialise).
     __global__ void __launch_bounds__(256) k_heat_pattern(const __grid_constant__ HeatParams p)
     {
+        __shared__ uint32_t pat[2048];
         const HeatStream& st = p.st[blockIdx.y];
         const int64_t P = st.period;
         if(P == 0)
             return;
+        for(uint32_t k = threadIdx.x; k < P; k += blockDim.x)
+            pat[k] = p.pattern[st.patOff + k];
+        __syncthreads();
         unsigned long long* heat = p.heat + p.heatOff[st.nr];
         const double invP = 1.0 / static_cast<double>(P);
         constexpr int K = 8;
-        for(int64_t bq = st.pLo + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * K; bq <= st.pHi;
-            bq += static_cast<int64_t>(gridDim.x) * blockDim.x * K)
+        const int64_t lane = threadIdx.x & 31, warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+        const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+        const int64_t step32 = 32 - floor_div_r(32, P, invP) * P; // 32 mod P
+        for(int64_t chunk = st.pLo + warp * 32 * K; chunk <= st.pHi; chunk += warps * 32 * K)
         {
-            int64_t m = bq - st.pb0;
+            const int64_t b0 = chunk + lane;
+            int64_t m = b0 - st.pb0;
             m -= floor_div_r(m, P, invP) * P;
             unsigned long long h[K];
 #pragma unroll
             for(int k = 0; k < K; ++k)
-                h[k] = bq + k <= st.pHi ? heat[bq + k] : 0;
+                h[k] = b0 + 32 * k <= st.pHi ? heat[b0 + 32 * k] : 0;
 #pragma unroll
             for(int k = 0; k < K; ++k)
             {
-                if(bq + k <= st.pHi)
-                    heat[bq + k] = h[k] + p.pattern[st.patOff + m];
-                m = m + 1 == P ? 0 : m + 1;
+                if(b0 + 32 * k <= st.pHi)
+                    heat[b0 + 32 * k] = h[k] + pat[m];
+                m += step32;
+                m = m >= P ? m - P : m;
             }
         }
     }
