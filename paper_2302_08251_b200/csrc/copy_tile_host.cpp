@@ -70,6 +70,11 @@ namespace lamk
 
 using namespace lamb;
 
+namespace lamjit
+{
+    bool tryCopy(const lamt_params& p, uint64_t begin, uint64_t end, uint64_t* doneEnd, cudaStream_t s);
+}
+
 namespace lamhost
 {
     namespace
@@ -1149,6 +1154,23 @@ namespace lamhost
     }
 
 
+    // physical pairs no fixed kernel covers (mixed leaf sizes, unaligned packed records, lane
+    // counts no vector group fits, padded destinations): a kernel generated for the exact pair
+    // (jit.cpp); false when NVRTC is unavailable or the pair does not fit its 16-byte groups
+    static bool tryJit(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
+                       const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        uint64_t doneEnd = begin;
+        if(!lamjit::tryCopy(p, begin, end, &doneEnd, s))
+            return false;
+        addAccessCounts(p, S, doneEnd - begin, s);
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s, false),
+                           "generic_copy(tail)");
+        return true;
+    }
+
     // the data moves through the tile kernels (none of which counts heat); a Heatmap on either
     // side is then accounted over the whole range in one pass that touches ranges, not data
     static bool launchTile(const Lowered& S, const DeviceImage& si, const std::vector<uint8_t*>& sptr, const Lowered& D,
@@ -1198,7 +1220,8 @@ namespace lamhost
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
         if(p.dst_holes)
-            return envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s);
+            return tryJit(p, begin, end, si, di, S, D, s)
+                || (envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s));
         if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
@@ -1208,6 +1231,9 @@ namespace lamhost
         if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
             return true;
         if(!p.uni && tryVecMulti(p, begin, end, si, di, S, D, s))
+            return true;
+        // (uniform pairs stay on the direct / warp-transpose paths below: measured faster there)
+        if(!p.uni && tryJit(p, begin, end, si, di, S, D, s))
             return true;
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /

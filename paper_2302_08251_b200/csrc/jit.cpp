@@ -1,0 +1,569 @@
+// Run-time specialised copy kernels for physical layout pairs (NVRTC).
+//
+// The reference's mappings are run-time objects (mapping.hpp:44-155); LLAMA, the library the
+// paper describes, resolves them at compile time.  For the physical pairs the fixed kernels do
+// not cover -- records with mixed leaf sizes and unaligned packed leaves, AoSoA lane counts no
+// vector group fits, padded destinations -- this path does what LLAMA's compile-time mappings
+// do: it generates a kernel for the exact pair of lowered layouts, with every block stride,
+// lane count and leaf offset a literal, compiles it with NVRTC for sm_100a (once per pair,
+// cached) and launches it.
+//
+// The generated kernel: a thread owns G consecutive elements, chosen so that for every stream
+// of both sides the bytes of those elements are whole 16-byte vectors (G/L whole blocks of a
+// record / AoSoA<L> stream, or one run of G values of a leaf inside an AoSoA<L> block).  It
+// loads every source vector (ld.global.cs.v4), assembles every destination word with PRMT byte
+// permutes whose selectors are compile-time constants, and stores every destination vector
+// (st.global.cs.v4).  Destination bytes copyView never writes (padding) come from the
+// destination's own old words, loaded first.  The semantics are copyView's fieldwise loop
+// (view.cpp:184-188) on physical leaves: a byte permutation of the leaf bytes.  Bool leaves
+// (canonicalised on read) and conversions stay with the general engines.
+//
+// NVRTC is loaded with dlopen; when it is absent or a compile fails the pair falls back to the
+// warp-tile engine (never to the CPU).
+#include "capi_internal.hpp"
+#include "launch.h"
+#include "tile.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+namespace lamjit
+{
+    namespace
+    {
+        typedef struct _nvrtcProgram* nvrtcProgram;
+        struct Nvrtc
+        {
+            bool ok = false;
+            int (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+            int (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+            int (*cubinSize)(nvrtcProgram, size_t*) = nullptr;
+            int (*cubin)(nvrtcProgram, char*) = nullptr;
+            int (*logSize)(nvrtcProgram, size_t*) = nullptr;
+            int (*log)(nvrtcProgram, char*) = nullptr;
+            int (*destroy)(nvrtcProgram*) = nullptr;
+        };
+
+        Nvrtc& nvrtc()
+        {
+            static Nvrtc n;
+            static std::once_flag once;
+            std::call_once(
+                once,
+                [&]
+                {
+                    void* h = nullptr;
+                    for(const char* name : {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"})
+                        if((h = dlopen(name, RTLD_NOW | RTLD_LOCAL)))
+                            break;
+                    if(!h)
+                        return;
+                    n.create = reinterpret_cast<decltype(n.create)>(dlsym(h, "nvrtcCreateProgram"));
+                    n.compile = reinterpret_cast<decltype(n.compile)>(dlsym(h, "nvrtcCompileProgram"));
+                    n.cubinSize = reinterpret_cast<decltype(n.cubinSize)>(dlsym(h, "nvrtcGetCUBINSize"));
+                    n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+                    n.logSize = reinterpret_cast<decltype(n.logSize)>(dlsym(h, "nvrtcGetProgramLogSize"));
+                    n.log = reinterpret_cast<decltype(n.log)>(dlsym(h, "nvrtcGetProgramLog"));
+                    n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+                    n.ok = n.create && n.compile && n.cubinSize && n.cubin && n.logSize && n.log && n.destroy;
+                });
+            return n;
+        }
+
+        // compiled kernels by generated source (a failed compile is remembered as nullptr)
+        std::mutex g_mu;
+        std::map<std::string, cudaKernel_t> g_cache;
+
+        cudaKernel_t compile(const std::string& src)
+        {
+            {
+                std::lock_guard<std::mutex> lk(g_mu);
+                auto it = g_cache.find(src);
+                if(it != g_cache.end())
+                    return it->second;
+            }
+            Nvrtc& n = nvrtc();
+            cudaKernel_t kern = nullptr;
+            if(n.ok)
+            {
+                nvrtcProgram prog = nullptr;
+                if(n.create(&prog, src.c_str(), "lamjit.cu", 0, nullptr, nullptr) == 0)
+                {
+                    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
+                    const int rc = n.compile(prog, 3, opts);
+                    if(rc != 0 && std::getenv("LAMB_JIT_LOG"))
+                    {
+                        size_t ls = 0;
+                        n.logSize(prog, &ls);
+                        std::string lg(ls, '\0');
+                        n.log(prog, lg.data());
+                        std::fprintf(stderr, "lamjit: compile failed (%d):\n%s\n%s\n", rc, lg.c_str(), src.c_str());
+                    }
+                    if(rc == 0)
+                    {
+                        size_t sz = 0;
+                        n.cubinSize(prog, &sz);
+                        std::vector<char> bin(sz);
+                        n.cubin(prog, bin.data());
+                        cudaLibrary_t lib = nullptr;
+                        if(cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess)
+                        {
+                            if(cudaLibraryGetKernel(&kern, lib, "lamjit_copy") != cudaSuccess)
+                                kern = nullptr;
+                        }
+                        cudaGetLastError(); // a failed load must not poison later launches
+                    }
+                    n.destroy(&prog);
+                }
+            }
+            std::lock_guard<std::mutex> lk(g_mu);
+            g_cache[src] = kern;
+            return kern;
+        }
+    } // namespace
+
+    // one side of a pair, as 16-byte vectors of the G-element group
+    struct Span
+    {
+        bool run = false;            // false: G/L whole blocks (address base + g * gstride)
+        unsigned long long base = 0; // run: leaf-run base (stream + inblock); block: stream + (begin/L)*bs
+        uint64_t gstride = 0;        // block: bytes per group
+        uint32_t lsh = 0, bs = 0, lmask = 0, ls = 0; // run: base + (e0 >> lsh)*bs + (e0 & lmask)*ls
+        uint32_t bytes = 0;          // multiple of 16
+        uint32_t word0 = 0;          // first word of the span in the side's word space
+    };
+
+    bool tryCopy(const lamt_params& p, uint64_t begin, uint64_t end, uint64_t* doneEnd, cudaStream_t s)
+    {
+        const char* env = std::getenv("LAMB_JIT");
+        if(env && env[0] == '0')
+            return false;
+        const uint32_t nl = p.nleaves;
+        if(nl < 1 || nl > LAMT_MAX_LEAVES)
+            return false;
+        for(uint32_t f = 0; f < nl; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != L.d[0].size || L.stype != L.dtype
+               || L.stype != L.ltype || L.ltype == lamb::Bool)
+                return false;
+        }
+        // the smallest group size G for which every stream of both sides is whole vectors
+        std::vector<uint32_t> candidates = {4, 8, 16, 32, 12, 24, 48};
+        std::vector<Span> sv[2];
+        std::vector<int> spanOfStream[2];
+        // leaf f, element j, byte b -> (span word index, byte) on each side
+        auto build = [&](uint32_t G, bool src, std::vector<Span>& spans, std::vector<int>& sos,
+                         std::vector<uint32_t>& wordOf) -> bool
+        {
+            spans.clear();
+            sos.assign(LAMT_MAX_STREAMS, -1);
+            std::vector<int> runOfLeaf(nl, -1);
+            uint32_t words = 0;
+            for(uint32_t f = 0; f < nl; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                const lamt_stream& st = p.st[t.stream];
+                const uint32_t L = st.lanes;
+                if(G % L == 0)
+                {
+                    if(sos[t.stream] < 0)
+                    {
+                        Span sp;
+                        sp.run = false;
+                        sp.base = st.gptr + (begin / L) * st.bs;
+                        sp.gstride = uint64_t(G / L) * st.bs;
+                        sp.bytes = static_cast<uint32_t>(sp.gstride);
+                        if(sp.bytes % 16 || sp.base % 16 || sp.gstride % 16)
+                            return false;
+                        sp.word0 = words;
+                        words += sp.bytes / 4;
+                        sos[t.stream] = static_cast<int>(spans.size());
+                        spans.push_back(sp);
+                    }
+                }
+                else if(L % G == 0 && st.lshift != 0xFFFFFFFFu)
+                {
+                    Span sp;
+                    sp.run = true;
+                    sp.base = st.gptr + t.inblock;
+                    sp.lsh = st.lshift;
+                    sp.bs = st.bs;
+                    sp.lmask = L - 1;
+                    sp.ls = t.ls;
+                    sp.bytes = G * t.size;
+                    if(t.ls != t.size || sp.bytes % 16 || sp.base % 16 || st.bs % 16)
+                        return false;
+                    sp.word0 = words;
+                    words += sp.bytes / 4;
+                    runOfLeaf[f] = static_cast<int>(spans.size());
+                    spans.push_back(sp);
+                }
+                else
+                    return false;
+            }
+            if(words > 1024)
+                return false;
+            wordOf.assign(size_t(nl) * G * 16, 0xFFFFFFFFu);
+            for(uint32_t f = 0; f < nl; ++f)
+            {
+                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
+                const lamt_stream& st = p.st[t.stream];
+                const uint32_t L = st.lanes;
+                for(uint32_t j = 0; j < G; ++j)
+                    for(uint32_t b = 0; b < t.size; ++b)
+                    {
+                        uint32_t byteInSpan, w0;
+                        if(runOfLeaf[f] >= 0)
+                        {
+                            byteInSpan = j * t.size + b;
+                            w0 = spans[runOfLeaf[f]].word0;
+                        }
+                        else
+                        {
+                            byteInSpan = (j / L) * st.bs + t.inblock + (L > 1 ? (j % L) * t.ls : 0) + b;
+                            w0 = spans[sos[t.stream]].word0;
+                        }
+                        // (word << 2) | byte
+                        wordOf[(size_t(f) * G + j) * 16 + b] = ((w0 + byteInSpan / 4) << 2) | (byteInSpan & 3);
+                    }
+            }
+            return true;
+        };
+        uint32_t G = 0;
+        std::vector<uint32_t> wS, wD;
+        for(uint32_t c : candidates)
+        {
+            if(begin % c)
+                continue;
+            if(build(c, true, sv[0], spanOfStream[0], wS) && build(c, false, sv[1], spanOfStream[1], wD))
+            {
+                G = c;
+                break;
+            }
+        }
+        if(G == 0)
+            return false;
+        const uint64_t groups = (end - begin) / G;
+        if(groups == 0)
+            return false;
+        // destination word -> its 4 source bytes (0xFFFFFFFF: a hole, keep the old byte)
+        uint32_t dWords = 0;
+        for(const Span& sp : sv[1])
+            dWords += sp.bytes / 4;
+        std::vector<uint32_t> srcOfDst(size_t(dWords) * 4, 0xFFFFFFFFu);
+        for(uint32_t f = 0; f < nl; ++f)
+            for(uint32_t j = 0; j < G; ++j)
+                for(uint32_t b = 0; b < p.leaf[f].s[0].size; ++b)
+                {
+                    const size_t k = (size_t(f) * G + j) * 16 + b;
+                    const uint32_t d = wD[k];
+                    srcOfDst[size_t(d >> 2) * 4 + (d & 3)] = wS[k];
+                }
+        // destination vectors with holes are preloaded
+        std::vector<bool> holeVec(dWords / 4, false);
+        for(uint32_t w = 0; w < dWords; ++w)
+            for(uint32_t b = 0; b < 4; ++b)
+                if(srcOfDst[size_t(w) * 4 + b] == 0xFFFFFFFFu)
+                    holeVec[w / 4] = true;
+
+        // ---- generate ----
+        // A warp owns 32 consecutive groups.  A block span (G/L whole blocks) of K > 1 vectors per
+        // group is one contiguous 32*K-vector region per warp: it moves between HBM and a
+        // warp-private shared-memory slab with coalesced 16-byte accesses, slot t at t*KP with
+        // KP = K | 1 so the per-thread 16-byte slab accesses are bank-conflict-free.  Leaf runs of
+        // AoSoA blocks and one-vector spans are accessed by their own thread directly.
+        struct Lay
+        {
+            bool staged;
+            uint32_t K, KP, rb;
+        };
+        const char* envStage = std::getenv("LAMB_JIT_STAGE");
+        const bool stageOn = !(envStage && envStage[0] == '0');
+        std::vector<Lay> lay[2];
+        uint32_t slab[2] = {0, 0}; // slab vectors per warp on each side
+        uint32_t directWords = 0;
+        for(int side = 0; side < 2; ++side)
+            for(const Span& sp : sv[side])
+            {
+                Lay l;
+                l.K = sp.bytes / 16;
+                l.staged = stageOn && !sp.run && l.K > 1;
+                l.KP = l.K | 1u;
+                l.rb = slab[side];
+                if(l.staged)
+                    slab[side] += 32 * l.KP;
+                else if(side == 0)
+                    directWords += 4 * l.K;
+                lay[side].push_back(l);
+            }
+        const uint32_t warpBytes = (slab[0] + slab[1]) * 16;
+        if(warpBytes > 100 * 1024 || directWords > 96)
+            return false;
+        // padded destinations of wide records (slabs past 40 KB per warp, <= 5 warps per SM plus the
+        // preload pass) measured slower here than on the warp-tile engine
+        bool anyHole = false;
+        for(bool h : holeVec)
+            anyHole |= h;
+        if(anyHole && warpBytes > 40 * 1024)
+            return false;
+        const size_t nspan = sv[0].size() + sv[1].size();
+        if(nspan > 48)
+            return false;
+        std::ostringstream o;
+        o << "struct LJP { unsigned long long base[" << nspan << "]; unsigned long long begin, groups; };\n"
+          << "__device__ __forceinline__ unsigned prm(unsigned a, unsigned b, unsigned s) { unsigned r; "
+             "asm(\"prmt.b32 %0, %1, %2, %3;\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(s)); return r; }\n"
+          << "__device__ __forceinline__ uint4 ldg(unsigned long long a) { uint4 v; asm volatile(\"ld.global.cs.v4.u32 "
+             "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
+          << "__device__ __forceinline__ uint4 ldo(unsigned long long a) { uint4 v; asm volatile(\"ld.global.v4.u32 "
+             "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
+          << "__device__ __forceinline__ void stg(unsigned long long a, uint4 v) { asm volatile(\"st.global.cs.v4.u32 [%0], "
+             "{%1,%2,%3,%4};\" :: \"l\"(a), \"r\"(v.x), \"r\"(v.y), \"r\"(v.z), \"r\"(v.w) : \"memory\"); }\n"
+          << "extern \"C\" __global__ void __launch_bounds__(128) lamjit_copy(const LJP P) {\n"
+          << " extern __shared__ uint4 lj_sm[];\n"
+          << " const unsigned lane = threadIdx.x & 31u;\n"
+          << " uint4* ss = lj_sm + (threadIdx.x >> 5) * " << (slab[0] + slab[1]) << "u;\n"
+          << " uint4* sd = ss + " << slab[0] << "u;\n (void)ss; (void)sd;\n"
+          << " const unsigned long long wstride = (unsigned long long)gridDim.x * (blockDim.x >> 5) * 32ull;\n"
+          << " for(unsigned long long gw = ((unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32ull; "
+             "gw < P.groups; gw += wstride) {\n"
+          << "  const unsigned cnt = (unsigned)min(32ull, P.groups - gw);\n"
+          << "  const unsigned long long g = gw + lane;\n"
+          << "  const bool act = lane < cnt;\n"
+          << "  const unsigned long long e0 = P.begin + g * " << G << "ull;\n  (void)e0;\n";
+        auto addr = [&](const Span& sp, size_t idx) -> std::string
+        {
+            std::ostringstream a;
+            if(sp.run)
+                a << "(P.base[" << idx << "] + (e0 >> " << sp.lsh << ") * " << sp.bs << "ull + (e0 & " << sp.lmask
+                  << "ull) * " << sp.ls << "ull)";
+            else
+                a << "(P.base[" << idx << "] + g * " << sp.gstride << "ull)";
+            return a.str();
+        };
+        auto slot = [&](const Lay& l, uint32_t v) -> std::string
+        {
+            std::ostringstream a;
+            a << "[" << l.rb << "u + lane * " << l.KP << "u + " << v << "u]";
+            return a.str();
+        };
+        auto coop = [&](const Span& sp, const Lay& l, size_t idx, bool load, const char* slabName, const char* fn)
+        {
+            o << "  { const unsigned long long a = P.base[" << idx << "] + gw * " << sp.gstride << "ull;\n"
+              << "#pragma unroll\n   for(unsigned j = 0; j < " << l.K << "u; ++j) { const unsigned i = lane + 32u * j; "
+              << "if(i < cnt * " << l.K << "u) ";
+            if(load)
+                o << slabName << "[" << l.rb << "u + (i / " << l.K << "u) * " << l.KP << "u + i % " << l.K << "u] = " << fn
+                  << "(a + 16ull * i); } }\n";
+            else
+                o << "stg(a + 16ull * i, " << slabName << "[" << l.rb << "u + (i / " << l.K << "u) * " << l.KP << "u + i % "
+                  << l.K << "u]); } }\n";
+        };
+        // direct source vectors first (most loads in flight), then the coalesced slab loads
+        for(size_t k = 0; k < sv[0].size(); ++k)
+            if(!lay[0][k].staged)
+            {
+                for(uint32_t v = 0; v < lay[0][k].K; ++v)
+                    o << "  uint4 S" << k << "_" << v << " = make_uint4(0u, 0u, 0u, 0u);\n";
+                o << "  if(act) { const unsigned long long a = " << addr(sv[0][k], k) << ";";
+                for(uint32_t v = 0; v < lay[0][k].K; ++v)
+                    o << " S" << k << "_" << v << " = ldg(a + " << 16 * v << "ull);";
+                o << " }\n";
+            }
+        for(size_t k = 0; k < sv[0].size(); ++k)
+            if(lay[0][k].staged)
+                coop(sv[0][k], lay[0][k], k, true, "ss", "ldg");
+        for(size_t k = 0; k < sv[1].size(); ++k)
+        {
+            bool holes = false;
+            for(uint32_t v = 0; v < lay[1][k].K; ++v)
+                holes |= holeVec[sv[1][k].word0 / 4 + v];
+            if(lay[1][k].staged && holes)
+                coop(sv[1][k], lay[1][k], sv[0].size() + k, true, "sd", "ldo");
+        }
+        o << "  __syncwarp();\n  if(act) {\n";
+        // source word w -> "S<k>_<v>.<c>"; staged vectors are read from the slab at first use
+        std::vector<int> spanOfWord;
+        for(size_t k = 0; k < sv[0].size(); ++k)
+            for(uint32_t w = 0; w < sv[0][k].bytes / 4; ++w)
+                spanOfWord.push_back(static_cast<int>(k));
+        std::vector<bool> emitted(spanOfWord.size() / 4, false);
+        auto srcWord = [&](uint32_t w) -> std::string
+        {
+            const int k = spanOfWord[w];
+            const uint32_t v = (w - sv[0][k].word0) / 4;
+            if(lay[0][k].staged && !emitted[w / 4])
+            {
+                o << "   const uint4 S" << k << "_" << v << " = ss" << slot(lay[0][k], v) << ";\n";
+                emitted[w / 4] = true;
+            }
+            static const char* comp = "xyzw";
+            return "S" + std::to_string(k) + "_" + std::to_string(v) + "." + comp[w & 3];
+        };
+        for(size_t k = 0; k < sv[1].size(); ++k)
+        {
+            const Span& sp = sv[1][k];
+            const Lay& l = lay[1][k];
+            const size_t idx = sv[0].size() + k;
+            const std::string ad = "ad" + std::to_string(k);
+            if(!l.staged)
+                o << "   const unsigned long long " << ad << " = " << addr(sp, idx) << ";\n";
+            for(uint32_t v = 0; v < l.K; ++v)
+            {
+                const uint32_t w0 = sp.word0 + 4 * v;
+                std::string oldName = "O" + std::to_string(k) + "_" + std::to_string(v);
+                if(holeVec[w0 / 4])
+                {
+                    if(l.staged)
+                        o << "   const uint4 " << oldName << " = sd" << slot(l, v) << ";\n";
+                    else
+                        o << "   const uint4 " << oldName << " = ldo(" << ad << " + " << 16 * v << "ull);\n";
+                }
+                std::string dn[4];
+                for(uint32_t c = 0; c < 4; ++c)
+                {
+                    const uint32_t w = w0 + c;
+                    std::string var[4];
+                    uint32_t byt[4];
+                    for(uint32_t b = 0; b < 4; ++b)
+                    {
+                        const uint32_t sw = srcOfDst[size_t(w) * 4 + b];
+                        if(sw == 0xFFFFFFFFu)
+                        {
+                            var[b] = oldName + "." + "xyzw"[c];
+                            byt[b] = b;
+                        }
+                        else
+                        {
+                            var[b] = srcWord(sw >> 2);
+                            byt[b] = sw & 3;
+                        }
+                    }
+                    if(var[0] == var[1] && var[1] == var[2] && var[2] == var[3] && byt[0] == 0 && byt[1] == 1 && byt[2] == 2
+                       && byt[3] == 3)
+                    {
+                        dn[c] = var[0];
+                        continue;
+                    }
+                    // PRMT chain: the first step takes bytes of two words, each further step adds one
+                    std::string acc;
+                    bool placed[4] = {false, false, false, false};
+                    for(uint32_t b = 0; b < 4; ++b)
+                    {
+                        if(placed[b])
+                            continue;
+                        const std::string x = var[b];
+                        uint32_t sel = 0;
+                        std::ostringstream e;
+                        if(acc.empty())
+                        {
+                            std::string y;
+                            for(uint32_t c2 = 0; c2 < 4; ++c2)
+                                if(var[c2] != x && y.empty())
+                                    y = var[c2];
+                            for(uint32_t c2 = 0; c2 < 4; ++c2)
+                            {
+                                uint32_t nib = 0;
+                                if(var[c2] == x)
+                                {
+                                    nib = byt[c2];
+                                    placed[c2] = true;
+                                }
+                                else if(!y.empty() && var[c2] == y)
+                                {
+                                    nib = 4 + byt[c2];
+                                    placed[c2] = true;
+                                }
+                                sel |= nib << (4 * c2);
+                            }
+                            e << "prm(" << x << ", " << (y.empty() ? x : y) << ", 0x" << std::hex << sel << std::dec << "u)";
+                        }
+                        else
+                        {
+                            for(uint32_t c2 = 0; c2 < 4; ++c2)
+                            {
+                                uint32_t nib = c2;
+                                if(!placed[c2] && var[c2] == x)
+                                {
+                                    nib = 4 + byt[c2];
+                                    placed[c2] = true;
+                                }
+                                sel |= nib << (4 * c2);
+                            }
+                            e << "prm(" << acc << ", " << x << ", 0x" << std::hex << sel << std::dec << "u)";
+                        }
+                        acc = e.str();
+                    }
+                    dn[c] = acc;
+                }
+                const std::string val = "make_uint4(" + dn[0] + ", " + dn[1] + ", " + dn[2] + ", " + dn[3] + ")";
+                if(l.staged)
+                    o << "   sd" << slot(l, v) << " = " << val << ";\n";
+                else
+                    o << "   stg(" << ad << " + " << 16 * v << "ull, " << val << ");\n";
+            }
+        }
+        o << "  }\n  __syncwarp();\n";
+        for(size_t k = 0; k < sv[1].size(); ++k)
+            if(lay[1][k].staged)
+                coop(sv[1][k], lay[1][k], sv[0].size() + k, false, "sd", "");
+        o << "  __syncwarp();\n }\n}\n";
+        const std::string src = o.str();
+        if(const char* dump = std::getenv("LAMB_JIT_DUMP"))
+            if(FILE* fp = std::fopen(dump, "a"))
+            {
+                std::fprintf(fp, "// G=%u groups=%llu\n%s\n", G, static_cast<unsigned long long>(groups), src.c_str());
+                std::fclose(fp);
+            }
+        const cudaKernel_t kern = compile(src);
+        if(!kern)
+            return false;
+        // warps per CTA: 4 while the slabs fit 100 KB per CTA
+        const uint32_t wpc = warpBytes == 0 ? 4 : std::max<uint32_t>(1, std::min<uint32_t>(4, (100 * 1024) / warpBytes));
+        const size_t smem = size_t(wpc) * warpBytes;
+        if(smem > 48 * 1024
+           && cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem))
+               != cudaSuccess)
+        {
+            cudaGetLastError();
+            return false;
+        }
+        // parameters: the span bases (runtime pointers), begin, groups
+        std::vector<unsigned long long> prm(nspan + 2);
+        for(size_t k = 0; k < sv[0].size(); ++k)
+            prm[k] = sv[0][k].base;
+        for(size_t k = 0; k < sv[1].size(); ++k)
+            prm[sv[0].size() + k] = sv[1][k].base;
+        prm[nspan] = begin;
+        prm[nspan + 1] = groups;
+        void* args[] = {prm.data()};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t warps = (groups + 31) / 32;
+        const uint64_t want = (warps + wpc - 1) / wpc;
+        const uint64_t cap = static_cast<uint64_t>(lamk::sm_count(dev)) * (64 / wpc);
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        const cudaError_t e =
+            cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(32 * wpc), args, smem, s);
+        if(e != cudaSuccess)
+        {
+            cudaGetLastError();
+            return false;
+        }
+        lamk::count_launch();
+        *doneEnd = begin + groups * G;
+        return true;
+    }
+} // namespace lamjit
