@@ -155,7 +155,7 @@ namespace lamjit
         {
             const lamt_leaf& L = p.leaf[f];
             if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != L.d[0].size || L.stype != L.dtype
-               || L.stype != L.ltype || L.ltype == lamb::Bool)
+               || L.stype != L.ltype)
                 return false;
         }
         // the smallest group size G for which every stream of both sides is whole vectors
@@ -262,6 +262,8 @@ namespace lamjit
         for(const Span& sp : sv[1])
             dWords += sp.bytes / 4;
         std::vector<uint32_t> srcOfDst(size_t(dWords) * 4, 0xFFFFFFFFu);
+        // bytes of bool leaves: canonicalised to 0 / 1 (any non-zero byte reads as true, scalar.hpp)
+        std::vector<uint32_t> boolMask(dWords, 0);
         for(uint32_t f = 0; f < nl; ++f)
             for(uint32_t j = 0; j < G; ++j)
                 for(uint32_t b = 0; b < p.leaf[f].s[0].size; ++b)
@@ -269,6 +271,8 @@ namespace lamjit
                     const size_t k = (size_t(f) * G + j) * 16 + b;
                     const uint32_t d = wD[k];
                     srcOfDst[size_t(d >> 2) * 4 + (d & 3)] = wS[k];
+                    if(p.leaf[f].ltype == lamb::Bool)
+                        boolMask[d >> 2] |= 0xFFu << (8 * (d & 3));
                 }
         // destination vectors with holes are preloaded
         std::vector<bool> holeVec(dWords / 4, false);
@@ -289,7 +293,20 @@ namespace lamjit
             uint32_t K, KP, rb;
         };
         const char* envStage = std::getenv("LAMB_JIT_STAGE");
-        const bool stageOn = !(envStage && envStage[0] == '0');
+        // Which sides go through slabs (profiles/r02/jit/jit_variants.log, 21 pairs): by default the
+        // destination only -- uncoalesced stores cost more than uncoalesced loads, and one staged side
+        // keeps twice the warps resident (0.79-0.93 of HBM where staging both gave 0.44-0.83) --
+        // unless the source's direct loads would not fit in registers; then the source only.
+        // LAMB_JIT_STAGE = 1 (both), s, d, 0 (neither) overrides.
+        uint32_t srcWords = 0;
+        for(const Span& sp : sv[0])
+            srcWords += sp.bytes / 4;
+        char mode = envStage && envStage[0] ? envStage[0] : 'a';
+        const bool autoMode = mode == 'a';
+        if(autoMode)
+            mode = srcWords <= 96 ? 'd' : 's';
+        const bool stageOn = mode != '0';
+        const bool stageSide[2] = {mode != 'd', mode != 's'};
         std::vector<Lay> lay[2];
         uint32_t slab[2] = {0, 0}; // slab vectors per warp on each side
         uint32_t directWords = 0;
@@ -298,7 +315,7 @@ namespace lamjit
             {
                 Lay l;
                 l.K = sp.bytes / 16;
-                l.staged = stageOn && !sp.run && l.K > 1;
+                l.staged = stageOn && stageSide[side] && !sp.run && l.K > 1;
                 l.KP = l.K | 1u;
                 l.rb = slab[side];
                 if(l.staged)
@@ -310,13 +327,11 @@ namespace lamjit
         const uint32_t warpBytes = (slab[0] + slab[1]) * 16;
         if(warpBytes > 100 * 1024 || directWords > 96)
             return false;
-        // padded destinations of wide records (slabs past 40 KB per warp, <= 5 warps per SM plus the
-        // preload pass) measured slower here than on the warp-tile engine
         bool anyHole = false;
         for(bool h : holeVec)
             anyHole |= h;
-        if(anyHole && warpBytes > 40 * 1024)
-            return false;
+        if(autoMode && anyHole && mode == 's')
+            return false; // padded destinations read back thread by thread: the warp-tile engine is faster
         const size_t nspan = sv[0].size() + sv[1].size();
         if(nspan > 48)
             return false;
@@ -324,6 +339,8 @@ namespace lamjit
         o << "struct LJP { unsigned long long base[" << nspan << "]; unsigned long long begin, groups; };\n"
           << "__device__ __forceinline__ unsigned prm(unsigned a, unsigned b, unsigned s) { unsigned r; "
              "asm(\"prmt.b32 %0, %1, %2, %3;\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(s)); return r; }\n"
+          << "__device__ __forceinline__ unsigned bcn(unsigned w, unsigned m) { return (w & ~m) | (__vcmpne4(w & m, 0u) & m & "
+             "0x01010101u); }\n"
           << "__device__ __forceinline__ uint4 ldg(unsigned long long a) { uint4 v; asm volatile(\"ld.global.cs.v4.u32 "
              "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
           << "__device__ __forceinline__ uint4 ldo(unsigned long long a) { uint4 v; asm volatile(\"ld.global.v4.u32 "
@@ -454,6 +471,8 @@ namespace lamjit
                        && byt[3] == 3)
                     {
                         dn[c] = var[0];
+                        if(boolMask[w])
+                            dn[c] = "bcn(" + dn[c] + ", " + std::to_string(boolMask[w]) + "u)";
                         continue;
                     }
                     // PRMT chain: the first step takes bytes of two words, each further step adds one
@@ -506,6 +525,8 @@ namespace lamjit
                         acc = e.str();
                     }
                     dn[c] = acc;
+                    if(boolMask[w])
+                        dn[c] = "bcn(" + dn[c] + ", " + std::to_string(boolMask[w]) + "u)";
                 }
                 const std::string val = "make_uint4(" + dn[0] + ", " + dn[1] + ", " + dn[2] + ", " + dn[3] + ")";
                 if(l.staged)
@@ -530,7 +551,9 @@ namespace lamjit
         if(!kern)
             return false;
         // warps per CTA: 4 while the slabs fit 100 KB per CTA
-        const uint32_t wpc = warpBytes == 0 ? 4 : std::max<uint32_t>(1, std::min<uint32_t>(4, (100 * 1024) / warpBytes));
+        const char* envCta = std::getenv("LAMB_JIT_CTA_KB");
+        const uint32_t ctaBytes = (envCta ? static_cast<uint32_t>(std::atoi(envCta)) : 100) * 1024;
+        const uint32_t wpc = warpBytes == 0 ? 4 : std::max<uint32_t>(1, std::min<uint32_t>(4, ctaBytes / warpBytes));
         const size_t smem = size_t(wpc) * warpBytes;
         if(smem > 48 * 1024
            && cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import random_values
+from conftest import MIXED, random_values
 from oracle import lamina_oracle as O
 from test_gpu_copy import run_pair
 
@@ -101,3 +101,32 @@ def test_jit_disabled_gives_same_bytes(monkeypatch):
         outs.append([x.copy() for x in d.download_all()])
     for x, y in zip(*outs):
         assert np.array_equal(x, y)
+
+
+BOOLREC = "Record{a:bool,b:u8,c:bool,d:f32,e:bool}"
+
+
+@pytest.mark.parametrize("schema,a,b", [
+    (BOOLREC, "aos-packed", "soa-mb"), (BOOLREC, "soa-mb", "aos-aligned"), (BOOLREC, "aosoa:16", "aos-packed"),
+    (MIXED, "aos-packed", "soa-mb"), (MIXED, "soa-mb", "aos-packed"), (MIXED, "aosoa:8", "aos-packed"),
+])
+def test_jit_bool_bytes_canonicalise(schema, a, b, tmp_path, monkeypatch):
+    """Source blobs of random bytes (bool bytes 0x02..0xFF included): the generated kernel writes
+    every bool as 0x01 / 0x00 like ScalarValue::fromStorageBits(Bool) (scalar.hpp:259-261)."""
+    from paper_2302_08251_b200 import lamina as L
+    dump = str(tmp_path / "jit.cu")
+    monkeypatch.setenv("LAMB_JIT_DUMP", dump)
+    n = 4103
+    ext = f"i32:[{n}]"
+    ms, md = O.make(schema, ext, a), O.make(schema, ext, b)
+    rng = np.random.default_rng(3)
+    sb = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(ms)]
+    db = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(md)]
+    gs, gd = L.View(L.Layout(schema, ext, a)), L.View(L.Layout(schema, ext, b))
+    gs.upload_all(sb)
+    gd.upload_all(db)
+    O.copy_view(ms, sb, md, db)
+    L.copy_view(gs, gd)
+    for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
+        assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
+    assert _dump_size(dump) > 0

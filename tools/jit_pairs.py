@@ -13,6 +13,7 @@ from bench import peaks
 PEAK = peaks()[0]
 MIXED = "Record{a:f64,b:u16,c:i8,d:f32}"
 MIX2 = "Record{a:i8,b:u16,c:i32,d:u64,e:f32,f:f64,h:Record{x:i16,y:f32[3]}}"
+MIXB = "Record{a:i8,b:u16,c:i32,d:u64,e:f32,f:f64,g:bool,h:Record{x:i16,y:f32[3]}}"  # tests/conftest.py MIXED
 DUMP = os.path.abspath("gpurun_out/jit_src.cu")
 PAIRS = [
     (MIXED, "aos-packed", "soa-mb"), (MIXED, "soa-mb", "aos-packed"), (MIXED, "aos-packed", "soa-sb"),
@@ -22,12 +23,14 @@ PAIRS = [
     (R32, "aosoa:6", "soa-sb"), (R32, "aosoa:32", "aosoa:3"), (R64, "aos-packed", "aosoa:3"),
     (R64, "aosoa:3", "soa-mb"), ("Record{a:u16,b:u8}", "aos-packed", "soa-mb"),
     ("Record{a:u16,b:u8}", "aos-aligned", "soa-mb"),
+    (MIXB, "aos-packed", "soa-mb"), (MIXB, "soa-mb", "aos-packed"), (MIXB, "aos-packed", "aos-aligned"),
+    (MIXB, "aosoa:8", "soa-mb"),
 ]
 
 
 def run(schema, a, b, n, jit, reps, stage=True):
     os.environ["LAMB_JIT"] = "1" if jit else "0"
-    os.environ["LAMB_JIT_STAGE"] = "1" if stage else "0"
+    os.environ["LAMB_JIT_STAGE"] = "a" if stage else "1"
     la, lb = L.Layout(schema, f"i32:[{n}]", a), L.Layout(schema, f"i32:[{n}]", b)
     s, d = L.View(la), L.View(lb)
     _fill(L, s, 1)
@@ -63,7 +66,7 @@ def main():
             tag = f"{schema[:20]:20} {a:>12} -> {b:<12} n={n:<9}"
             if reps:
                 print(f"{tag} jit={'Y' if took else 'n'} same={same} jit {g1:6.0f} GB/s ({g1 / PEAK:.2f}) "
-                      f"unstaged {g2 / PEAK:.2f} fixed {g0:6.0f} GB/s ({g0 / PEAK:.2f})  first-call {c1:.2f}s", flush=True)
+                      f"both-staged {g2 / PEAK:.2f} fixed {g0:6.0f} GB/s ({g0 / PEAK:.2f})  first-call {c1:.2f}s", flush=True)
             else:
                 print(f"{tag} jit={'Y' if took else 'n'} same={same}", flush=True)
     print("jit_pairs:", "OK" if not bad else f"{bad} MISMATCHES")
