@@ -303,8 +303,16 @@ namespace lamjit
             srcWords += sp.bytes / 4;
         char mode = envStage && envStage[0] ? envStage[0] : 'a';
         const bool autoMode = mode == 'a';
+        // widest block span on each side (16-byte vectors per thread)
+        uint32_t maxK[2] = {0, 0};
+        for(int side = 0; side < 2; ++side)
+            for(const Span& sp : sv[side])
+                if(!sp.run)
+                    maxK[side] = std::max(maxK[side], sp.bytes / 16);
         if(autoMode)
-            mode = srcWords <= 96 ? 'd' : 's';
+            mode = (srcWords <= 96 || maxK[1] > maxK[0]) ? 'd' : 's';
+        // a source too wide for registers, not staged: its vectors are loaded at first use
+        const bool lazySrc = mode == 'd' && srcWords > 96;
         const bool stageOn = mode != '0';
         const bool stageSide[2] = {mode != 'd', mode != 's'};
         std::vector<Lay> lay[2];
@@ -325,7 +333,7 @@ namespace lamjit
                 lay[side].push_back(l);
             }
         const uint32_t warpBytes = (slab[0] + slab[1]) * 16;
-        if(warpBytes > 100 * 1024 || directWords > 96)
+        if(warpBytes > 100 * 1024 || (directWords > 96 && !lazySrc))
             return false;
         bool anyHole = false;
         for(bool h : holeVec)
@@ -389,7 +397,7 @@ namespace lamjit
         };
         // direct source vectors first (most loads in flight), then the coalesced slab loads
         for(size_t k = 0; k < sv[0].size(); ++k)
-            if(!lay[0][k].staged)
+            if(!lay[0][k].staged && !lazySrc)
             {
                 for(uint32_t v = 0; v < lay[0][k].K; ++v)
                     o << "  uint4 S" << k << "_" << v << " = make_uint4(0u, 0u, 0u, 0u);\n";
@@ -410,6 +418,10 @@ namespace lamjit
                 coop(sv[1][k], lay[1][k], sv[0].size() + k, true, "sd", "ldo");
         }
         o << "  __syncwarp();\n  if(act) {\n";
+        if(lazySrc)
+            for(size_t k = 0; k < sv[0].size(); ++k)
+                if(!lay[0][k].staged)
+                    o << "   const unsigned long long as" << k << " = " << addr(sv[0][k], k) << ";\n";
         // source word w -> "S<k>_<v>.<c>"; staged vectors are read from the slab at first use
         std::vector<int> spanOfWord;
         for(size_t k = 0; k < sv[0].size(); ++k)
@@ -423,6 +435,11 @@ namespace lamjit
             if(lay[0][k].staged && !emitted[w / 4])
             {
                 o << "   const uint4 S" << k << "_" << v << " = ss" << slot(lay[0][k], v) << ";\n";
+                emitted[w / 4] = true;
+            }
+            else if(lazySrc && !emitted[w / 4])
+            {
+                o << "   const uint4 S" << k << "_" << v << " = ldg(as" << k << " + " << 16 * v << "ull);\n";
                 emitted[w / 4] = true;
             }
             static const char* comp = "xyzw";
