@@ -1232,8 +1232,10 @@ namespace lamhost
             return true;
         if(!p.uni && tryVecMulti(p, begin, end, si, di, S, D, s))
             return true;
-        // (uniform pairs stay on the direct / warp-transpose paths below: measured faster there)
-        if(!p.uni && tryJit(p, begin, end, si, di, S, D, s))
+        // uniform pairs get here when the register transpose cannot take them (AoSoA lanes that are not
+        // a power of two or not a multiple of 16/size): the generated kernel measured 0.81-0.99 of HBM
+        // on them against 0.59-0.71 for k_uniform_direct (profiles/r02/jit/jit_uni.log)
+        if((!p.uni || envNum("LAMB_JIT_UNI", 1) != 0) && tryJit(p, begin, end, si, di, S, D, s))
             return true;
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /
