@@ -297,6 +297,73 @@ namespace lamd
         return sign | (static_cast<uint32_t>(static_cast<int>(ef) - bias + 127) << 23) | (man << (23 - M));
     }
 
+    // The two functions above without branches, for the bit-packing kernels' hot loops
+    // (float_encode_f32_small took ~43 instructions per value with its BRA/BSSY pairs and
+    // kept k_pack32<8,3> ALU-bound at 36% of HBM).  Per-format constants are built once per
+    // thread by f32_codec; the results are bit-identical to the branchy functions (checked
+    // exhaustively over all 2^32 f32 inputs, tests/test_gpu_codec.py).
+    struct F32Codec
+    {
+        uint32_t sh, half, lsbAnd, odd, C1, minN, ovf, inf, nan, sgnSh, sgnBit; // encode
+        float s1, s2;
+        uint32_t mag, C2, subMax; // decode
+        float ds, dsOff;
+    };
+
+    LAM_DEV F32Codec f32_codec(uint32_t E, uint32_t M)
+    {
+        F32Codec c;
+        const int bias = (1 << (E - 1)) - 1;
+        const uint32_t maxExp = (1u << E) - 1u;
+        c.sh = 23 - M;
+        c.half = c.sh ? (1u << (c.sh - 1)) - 1u : 0u;
+        c.lsbAnd = (c.sh && M) ? 1u : 0u;
+        c.odd = M == 0 ? 1u : 0u;
+        c.C1 = static_cast<uint32_t>(bias - 127) << M;
+        c.minN = static_cast<uint32_t>(127 - bias + 1) << 23;
+        c.ovf = static_cast<uint32_t>(static_cast<int>(maxExp) - bias + 127) << 23;
+        c.inf = maxExp << M;
+        c.nan = M ? (c.inf | (1u << (M - 1))) : c.inf;
+        c.sgnSh = 31 - (E + M);
+        c.sgnBit = 1u << (E + M);
+        c.s1 = __uint_as_float(static_cast<uint32_t>(M + 127) << 23);
+        c.s2 = __uint_as_float(static_cast<uint32_t>(bias - 1 + 127) << 23);
+        c.mag = (1u << (E + M)) - 1u;
+        c.C2 = static_cast<uint32_t>(127 - bias) << 23;
+        c.subMax = 1u << M; // magnitudes below: exponent field 0
+        // subnormal: man * 2^(1 - bias - M) = (float(2^23 + man) - 2^23) * 2^(1 - bias - M), one FFMA
+        const int k = 1 - bias - static_cast<int>(M);
+        c.ds = k >= -126 ? __uint_as_float(static_cast<uint32_t>(k + 127) << 23) : __uint_as_float(1u << (k + 149));
+        const int k2 = k + 23;
+        c.dsOff = -(k2 >= -126 ? __uint_as_float(static_cast<uint32_t>(k2 + 127) << 23) : __uint_as_float(1u << (k2 + 149)));
+        return c;
+    }
+
+    LAM_DEV uint32_t f32_encode_bf(const F32Codec& c, uint32_t b)
+    {
+        const uint32_t a = b & 0x7FFFFFFFu;
+        const uint32_t r = a + c.half + (((a >> c.sh) & c.lsbAnd) | c.odd);
+        const uint32_t nrm = (r >> c.sh) + c.C1;
+        // |x| < 2^(1 - bias): RNE(|x| * 2^(M + bias - 1)) by the 2^23 magic add (the product is < 2^M <= 2^23)
+        const float t = __fmul_rn(__uint_as_float(a), c.s1);
+        const uint32_t q = __float_as_uint(__fmaf_rn(t, c.s2, 8388608.0f)) - 0x4B000000u;
+        uint32_t res = a >= c.minN ? nrm : q;
+        res = r >= c.ovf ? c.inf : res;
+        res = a > 0x7F800000u ? c.nan : res;
+        return res | ((b >> c.sgnSh) & c.sgnBit);
+    }
+
+    LAM_DEV uint32_t f32_decode_bf(const F32Codec& c, uint32_t p)
+    {
+        const uint32_t mag = p & c.mag;
+        const uint32_t sign = (p << c.sgnSh) & 0x80000000u;
+        const uint32_t nrm = (mag << c.sh) + c.C2;
+        const uint32_t sub = __float_as_uint(__fmaf_rn(__uint_as_float(mag | 0x4B000000u), c.ds, c.dsOff));
+        uint32_t res = mag < c.subMax ? sub : nrm;
+        res = mag >= c.inf ? (mag > c.inf ? 0x7FC00000u : 0x7F800000u) : res;
+        return sign | res;
+    }
+
     // Fast f32 encoders, equal to floatEncode((double)f, E, M) on every f32 input
     // (checked exhaustively against the reference on the GPU, tests/test_gpu_codec.py).
     LAM_DEV uint32_t encode_e8m10_f32(uint32_t b)

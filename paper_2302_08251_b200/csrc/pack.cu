@@ -98,7 +98,7 @@ namespace lamk
     // FMT: 0 integer, 1 f32 e8m10 (W=19), 2 f32 e5m10 (W=16), 3 any f32 format with E <= 8,
     // M <= 23 (runtime E, M; the 32-bit codec), 4 any float format (runtime E, M).
     template<int FMT>
-    __device__ __forceinline__ uint32_t enc_t(const PackParams& p, uint32_t v, uint32_t mask)
+    __device__ __forceinline__ uint32_t enc_t(const PackParams& p, const lamd::F32Codec& fc, uint32_t v, uint32_t mask)
     {
         if constexpr(FMT == 0)
             return v & mask;
@@ -107,13 +107,13 @@ namespace lamk
         else if constexpr(FMT == 2)
             return lamd::encode_e5m10_f32(v);
         else if constexpr(FMT == 3)
-            return lamd::float_encode_f32_small(v, p.E, p.M);
+            return lamd::f32_encode_bf(fc, v);
         else
             return static_cast<uint32_t>(lamd::float_encode_f32(v, p.E, p.M));
     }
 
     template<int FMT>
-    __device__ __forceinline__ uint32_t dec_t(const PackParams& p, uint32_t pat, uint32_t w)
+    __device__ __forceinline__ uint32_t dec_t(const PackParams& p, const lamd::F32Codec& fc, uint32_t pat, uint32_t w)
     {
         if constexpr(FMT == 0)
         {
@@ -138,7 +138,7 @@ namespace lamk
             return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
         }
         else if constexpr(FMT == 3)
-            return lamd::float_decode_f32(pat, p.E, p.M);
+            return lamd::f32_decode_bf(fc, pat);
         else if(p.E <= 8 && p.M <= 23)
             return lamd::float_decode_f32(pat, p.E, p.M);
         else
@@ -233,6 +233,7 @@ namespace lamk
         const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
+        const lamd::F32Codec fc = lamd::f32_codec(p.E, p.M); // FMT 3 only (dead code otherwise)
         const uint64_t gEnd = (p.groups + 31) / 32 * 32; // whole warps iterate together
         for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
         {
@@ -266,7 +267,7 @@ namespace lamk
                     // encode once per value (a value can straddle two words)
 #pragma unroll
                     for(int i = 0; i < 32; ++i)
-                        v[i] = enc_t<FMT>(p, v[i], mask);
+                        v[i] = enc_t<FMT>(p, fc, v[i], mask);
                     // word k = bits [32k, 32k+32): values floor(32k/W) .. floor((32k+31)/W)
 #pragma unroll
                     for(int k = 0; k < W; ++k)
@@ -292,7 +293,7 @@ namespace lamk
 #pragma unroll
                     for(int i = 0; i < 32; ++i)
                     {
-                        acc |= static_cast<unsigned long long>(enc_t<FMT>(p, v[i], mask)) << nb;
+                        acc |= static_cast<unsigned long long>(enc_t<FMT>(p, fc, v[i], mask)) << nb;
                         nb += w;
                         if(nb >= 32)
                         {
@@ -329,7 +330,7 @@ namespace lamk
     // unpack: 3 CTAs/SM (80 registers) except the widths that spill there
     __host__ __device__ constexpr int unpack_minb(int W, int FMT)
     {
-        return ((FMT == 0 || FMT == 3) && (W == 24 || W == 26 || W == 28 || W == 30)) || (FMT == 3 && W == 14)
+        return ((FMT == 0 || FMT == 3) && (W == 24 || W == 26 || W == 28 || W == 30)) || (FMT == 3 && (W == 14 || W == 27))
                 || (FMT == 0 && W == 6)
             ? 2
             : 3;
@@ -347,6 +348,7 @@ namespace lamk
         const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         unsigned long long cnt = 0;
+        const lamd::F32Codec fc = lamd::f32_codec(p.E, p.M); // FMT 3 only (dead code otherwise)
         const uint64_t gEnd = (p.groups + 31) / 32 * 32;
         auto liveOf = [&](uint64_t warpG) -> uint32_t
         {
@@ -428,7 +430,7 @@ namespace lamk
                         uint32_t pat = wd[k] >> sh;
                         if(sh + W > 32)
                             pat |= wd[k + 1] << (32 - sh);
-                        v[i] = dec_t<FMT>(p, pat & mask, w);
+                        v[i] = dec_t<FMT>(p, fc, pat & mask, w);
                     }
                 }
                 else
@@ -444,7 +446,7 @@ namespace lamk
                             ++k;
                             nb += 32;
                         }
-                        v[i] = dec_t<FMT>(p, static_cast<uint32_t>(acc) & mask, w);
+                        v[i] = dec_t<FMT>(p, fc, static_cast<uint32_t>(acc) & mask, w);
                         acc >>= w;
                         nb -= w;
                     }
@@ -586,6 +588,7 @@ namespace lamk
             PackParams p{};
             p.E = q.E;
             p.M = q.M;
+            const lamd::F32Codec fc = lamd::f32_codec(q.E, q.M);
             const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
             uint32_t v[32];
             const uint32_t* pv = psm + rec_base(q, lane, wp);
@@ -604,7 +607,7 @@ namespace lamk
             }
 #pragma unroll
             for(int i = 0; i < 32; ++i)
-                v[i] = enc_t<FMT>(p, v[i], mask);
+                v[i] = enc_t<FMT>(p, fc, v[i], mask);
             if constexpr(W != 0)
             {
 #pragma unroll
@@ -696,6 +699,7 @@ namespace lamk
                 PackParams p{};
                 p.E = q.E;
                 p.M = q.M;
+                const lamd::F32Codec fc = lamd::f32_codec(q.E, q.M);
                 p.sgn = (q.sgnMask >> wp) & 1u;
                 const uint32_t mask = w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u);
                 const uint32_t* my = slice + lane * ws;
@@ -712,7 +716,7 @@ namespace lamk
                         uint32_t pat = wd[k] >> sh;
                         if(sh + W > 32)
                             pat |= wd[k + 1] << (32 - sh);
-                        v[i] = dec_t<FMT>(p, pat & mask, w);
+                        v[i] = dec_t<FMT>(p, fc, pat & mask, w);
                     }
                 }
                 else
@@ -728,7 +732,7 @@ namespace lamk
                             ++k;
                             nb += 32;
                         }
-                        v[i] = dec_t<FMT>(p, static_cast<uint32_t>(acc) & mask, w);
+                        v[i] = dec_t<FMT>(p, fc, static_cast<uint32_t>(acc) & mask, w);
                         acc >>= w;
                         nb -= w;
                     }
