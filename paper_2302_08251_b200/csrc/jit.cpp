@@ -151,12 +151,36 @@ namespace lamjit
         const uint32_t nl = p.nleaves;
         if(nl < 1 || nl > LAMT_MAX_LEAVES)
             return false;
+        // every leaf a byte move without conversion; a side is one physical term of the value's
+        // size, or byte planes (Bytesplit, computed.cpp:405-502: term k holds byte k)
+        std::vector<uint32_t> vsz(nl);
         for(uint32_t f = 0; f < nl; ++f)
         {
             const lamt_leaf& L = p.leaf[f];
-            if(L.skind != LAMT_K_PHYS || L.dkind != LAMT_K_PHYS || L.s[0].size != L.d[0].size || L.stype != L.dtype
-               || L.stype != L.ltype)
+            if(L.stype != L.dtype || L.stype != L.ltype)
                 return false;
+            vsz[f] = static_cast<uint32_t>(lamb::scalarSize(L.ltype));
+            for(int side = 0; side < 2; ++side)
+            {
+                const uint8_t kind = side ? L.dkind : L.skind;
+                const uint8_t nt = side ? L.dn : L.sn;
+                const lamt_term* t = side ? L.d : L.s;
+                if(kind == LAMT_K_PHYS)
+                {
+                    if(t[0].size != vsz[f])
+                        return false;
+                }
+                else if(kind == LAMT_K_SPLIT)
+                {
+                    if(nt != vsz[f])
+                        return false;
+                    for(uint32_t k = 0; k < nt; ++k)
+                        if(t[k].size != 1)
+                            return false;
+                }
+                else
+                    return false;
+            }
         }
         // the smallest group size G for which every stream of both sides is whole vectors
         std::vector<uint32_t> candidates = {4, 8, 16, 32, 12, 24, 48};
@@ -168,75 +192,75 @@ namespace lamjit
         {
             spans.clear();
             sos.assign(LAMT_MAX_STREAMS, -1);
-            std::vector<int> runOfLeaf(nl, -1);
             uint32_t words = 0;
-            for(uint32_t f = 0; f < nl; ++f)
-            {
-                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
-                const lamt_stream& st = p.st[t.stream];
-                const uint32_t L = st.lanes;
-                if(G % L == 0)
-                {
-                    if(sos[t.stream] < 0)
-                    {
-                        Span sp;
-                        sp.run = false;
-                        sp.base = st.gptr + (begin / L) * st.bs;
-                        sp.gstride = uint64_t(G / L) * st.bs;
-                        sp.bytes = static_cast<uint32_t>(sp.gstride);
-                        if(sp.bytes % 16 || sp.base % 16 || sp.gstride % 16)
-                            return false;
-                        sp.word0 = words;
-                        words += sp.bytes / 4;
-                        sos[t.stream] = static_cast<int>(spans.size());
-                        spans.push_back(sp);
-                    }
-                }
-                else if(L % G == 0 && st.lshift != 0xFFFFFFFFu)
-                {
-                    Span sp;
-                    sp.run = true;
-                    sp.base = st.gptr + t.inblock;
-                    sp.lsh = st.lshift;
-                    sp.bs = st.bs;
-                    sp.lmask = L - 1;
-                    sp.ls = t.ls;
-                    sp.bytes = G * t.size;
-                    if(t.ls != t.size || sp.bytes % 16 || sp.base % 16 || st.bs % 16)
-                        return false;
-                    sp.word0 = words;
-                    words += sp.bytes / 4;
-                    runOfLeaf[f] = static_cast<int>(spans.size());
-                    spans.push_back(sp);
-                }
-                else
-                    return false;
-            }
-            if(words > 1024)
-                return false;
             wordOf.assign(size_t(nl) * G * 16, 0xFFFFFFFFu);
             for(uint32_t f = 0; f < nl; ++f)
             {
-                const lamt_term& t = src ? p.leaf[f].s[0] : p.leaf[f].d[0];
-                const lamt_stream& st = p.st[t.stream];
-                const uint32_t L = st.lanes;
-                for(uint32_t j = 0; j < G; ++j)
-                    for(uint32_t b = 0; b < t.size; ++b)
+                const lamt_leaf& lf = p.leaf[f];
+                const bool split = (src ? lf.skind : lf.dkind) == LAMT_K_SPLIT;
+                const uint32_t nt = split ? vsz[f] : 1;
+                for(uint32_t k = 0; k < nt; ++k)
+                {
+                    const lamt_term& t = src ? lf.s[k] : lf.d[k];
+                    const lamt_stream& st = p.st[t.stream];
+                    const uint32_t L = st.lanes;
+                    int run = -1;
+                    if(G % L == 0)
                     {
-                        uint32_t byteInSpan, w0;
-                        if(runOfLeaf[f] >= 0)
+                        if(sos[t.stream] < 0)
                         {
-                            byteInSpan = j * t.size + b;
-                            w0 = spans[runOfLeaf[f]].word0;
+                            Span sp;
+                            sp.run = false;
+                            sp.base = st.gptr + (begin / L) * st.bs;
+                            sp.gstride = uint64_t(G / L) * st.bs;
+                            sp.bytes = static_cast<uint32_t>(sp.gstride);
+                            if(sp.bytes % 16 || sp.base % 16 || sp.gstride % 16 || words + sp.bytes / 4 > 4096)
+                                return false;
+                            sp.word0 = words;
+                            words += sp.bytes / 4;
+                            sos[t.stream] = static_cast<int>(spans.size());
+                            spans.push_back(sp);
                         }
-                        else
-                        {
-                            byteInSpan = (j / L) * st.bs + t.inblock + (L > 1 ? (j % L) * t.ls : 0) + b;
-                            w0 = spans[sos[t.stream]].word0;
-                        }
-                        // (word << 2) | byte
-                        wordOf[(size_t(f) * G + j) * 16 + b] = ((w0 + byteInSpan / 4) << 2) | (byteInSpan & 3);
                     }
+                    else if(L % G == 0 && st.lshift != 0xFFFFFFFFu)
+                    {
+                        Span sp;
+                        sp.run = true;
+                        sp.base = st.gptr + t.inblock;
+                        sp.lsh = st.lshift;
+                        sp.bs = st.bs;
+                        sp.lmask = L - 1;
+                        sp.ls = t.ls;
+                        sp.bytes = G * t.size;
+                        if(t.ls != t.size || sp.bytes % 16 || sp.base % 16 || st.bs % 16)
+                            return false;
+                        sp.word0 = words;
+                        words += sp.bytes / 4;
+                        run = static_cast<int>(spans.size());
+                        spans.push_back(sp);
+                    }
+                    else
+                        return false;
+                    // value bytes this term holds: all of them (physical) or byte k (plane)
+                    const uint32_t b0 = split ? k : 0, nb = split ? 1 : vsz[f];
+                    for(uint32_t j = 0; j < G; ++j)
+                        for(uint32_t i = 0; i < nb; ++i)
+                        {
+                            uint32_t byteInSpan, w0;
+                            if(run >= 0)
+                            {
+                                byteInSpan = j * t.size + i;
+                                w0 = spans[run].word0;
+                            }
+                            else
+                            {
+                                byteInSpan = (j / L) * st.bs + t.inblock + (L > 1 ? (j % L) * t.ls : 0) + i;
+                                w0 = spans[sos[t.stream]].word0;
+                            }
+                            // (word << 2) | byte
+                            wordOf[(size_t(f) * G + j) * 16 + b0 + i] = ((w0 + byteInSpan / 4) << 2) | (byteInSpan & 3);
+                        }
+                }
             }
             return true;
         };
@@ -266,7 +290,7 @@ namespace lamjit
         std::vector<uint32_t> boolMask(dWords, 0);
         for(uint32_t f = 0; f < nl; ++f)
             for(uint32_t j = 0; j < G; ++j)
-                for(uint32_t b = 0; b < p.leaf[f].s[0].size; ++b)
+                for(uint32_t b = 0; b < vsz[f]; ++b)
                 {
                     const size_t k = (size_t(f) * G + j) * 16 + b;
                     const uint32_t d = wD[k];
@@ -341,7 +365,7 @@ namespace lamjit
         if(autoMode && anyHole && mode == 's')
             return false; // padded destinations read back thread by thread: the warp-tile engine is faster
         const size_t nspan = sv[0].size() + sv[1].size();
-        if(nspan > 48)
+        if(nspan > 96)
             return false;
         std::ostringstream o;
         o << "struct LJP { unsigned long long base[" << nspan << "]; unsigned long long begin, groups; };\n"

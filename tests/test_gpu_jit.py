@@ -28,6 +28,9 @@ PAIRS = [
     (MIX8, "aos-packed", "soa-mb"), (MIX8, "aosoa:16", "aos-packed"),
     (TINY, "aos-packed", "soa-mb"), (TINY, "aos-aligned", "soa-mb"), (TINY, "soa-sb", "aos-aligned"),
     (BYTES3, "aos-packed", "soa-mb"), (BYTES3, "soa-mb", "aos-packed"),
+    # byte planes (Bytesplit): every value byte is its own term
+    (MIX4, "aos-packed", "bytesplit:soa-mb"), (MIX4, "bytesplit:soa-mb", "aos-aligned"),
+    (MIX4, "aosoa:16", "bytesplit:aosoa:32"), (MIX8, "bytesplit:soa-mb", "aos-packed"),
 ]
 
 
@@ -109,6 +112,7 @@ BOOLREC = "Record{a:bool,b:u8,c:bool,d:f32,e:bool}"
 @pytest.mark.parametrize("schema,a,b", [
     (BOOLREC, "aos-packed", "soa-mb"), (BOOLREC, "soa-mb", "aos-aligned"), (BOOLREC, "aosoa:16", "aos-packed"),
     (MIXED, "aos-packed", "soa-mb"), (MIXED, "soa-mb", "aos-packed"), (MIXED, "aosoa:8", "aos-packed"),
+    (MIXED, "aos-packed", "bytesplit:soa-mb"), (BOOLREC, "bytesplit:soa-mb", "aos-aligned"),
 ])
 def test_jit_bool_bytes_canonicalise(schema, a, b, tmp_path, monkeypatch):
     """Source blobs of random bytes (bool bytes 0x02..0xFF included): the generated kernel writes

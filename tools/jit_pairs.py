@@ -25,6 +25,9 @@ PAIRS = [
     ("Record{a:u16,b:u8}", "aos-aligned", "soa-mb"),
     (MIXB, "aos-packed", "soa-mb"), (MIXB, "soa-mb", "aos-packed"), (MIXB, "aos-packed", "aos-aligned"),
     (MIXB, "aosoa:8", "soa-mb"),
+    (MIXED, "aos-packed", "bytesplit:soa-sb"), (MIXED, "aos-packed", "bytesplit:soa-mb"),
+    (MIXED, "bytesplit:soa-mb", "aos-packed"), (MIXB, "aos-packed", "bytesplit:soa-mb"),
+    (R64, "aosoa:8", "bytesplit:aosoa:32"),
 ]
 
 
