@@ -1,6 +1,8 @@
 // copyView dispatch (view.cpp:168-189) and the host-buffer entry point.
 #include "capi_internal.hpp"
 
+#include <cstdio>
+
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -222,6 +224,8 @@ namespace lamhost
         }
         if(!(fg && fg[0] == '1') && tileCopy(src, dst, begin, end, s))
             return;
+        if(std::getenv("LAMB_TRACE") && std::getenv("LAMB_TRACE")[0] == '1')
+            std::fprintf(stderr, "lamb path: generic\n");
         lam_cuda_check(lamk::generic_copy(src.img.hdr, dst.img.hdr, begin, end,
                                           static_cast<uint32_t>(a.schema().leafCount()), src.L->fac, dst.L->fac, s),
                        "generic_copy");

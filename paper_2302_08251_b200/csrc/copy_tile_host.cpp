@@ -9,6 +9,7 @@
 #include "capi_internal.hpp"
 #include "tile.h"
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -570,6 +571,25 @@ namespace lamhost
             }
             if(!leafContig)
                 return false;
+            if(!src && L == V && bs == nl * 16)
+            {
+                // AoSoA<V> destination: a thread's V elements are one whole block, leaf f's vector at
+                // f * 16, so the warp's 32 blocks are contiguous and are staged like AoS records
+                // (512-byte stores instead of 16-byte stores at the block stride)
+                bool blockMajor = true;
+                const lamt_term& t0 = p.leaf[0].d[0];
+                for(uint32_t f = 0; f < nl && blockMajor; ++f)
+                {
+                    const lamt_term& t = p.leaf[f].d[0];
+                    blockMajor = t.stream == t0.stream && t.inblock == f * 16;
+                }
+                if(blockMajor && p.st[t0.stream].gptr % 16 == 0 && envNum("LAMB_VEC_BLOCKSTAGE", 1) != 0)
+                {
+                    sd.recordContig = 2;
+                    sd.recBase = p.st[t0.stream].gptr;
+                    return true;
+                }
+            }
             sd.recordContig = 0;
             sd.bs = bs;
             sd.lanes = L;
@@ -1154,6 +1174,14 @@ namespace lamhost
     }
 
 
+    // LAMB_TRACE=1: the path each copy takes, on stderr (diagnostics only)
+    static void trace(const char* what)
+    {
+        static const bool on = std::getenv("LAMB_TRACE") && std::getenv("LAMB_TRACE")[0] == '1';
+        if(on)
+            std::fprintf(stderr, "lamb path: %s\n", what);
+    }
+
     // physical pairs no fixed kernel covers (mixed leaf sizes, unaligned packed records, lane
     // counts no vector group fits, padded destinations): a kernel generated for the exact pair
     // (jit.cpp); false when NVRTC is unavailable or the pair does not fit its 16-byte groups
@@ -1193,7 +1221,7 @@ namespace lamhost
     {
         Plan pl = makePlan(S, D);
         if(!pl.ok)
-            return false;
+            return trace("no tile plan"), false;
         lamt_params& p = pl.p;
         const uint64_t n = end - begin;
         const uint64_t ntiles = n / p.T;
@@ -1220,23 +1248,27 @@ namespace lamhost
         p.facSrc = reinterpret_cast<unsigned long long>(si.facDev);
         p.facDst = reinterpret_cast<unsigned long long>(di.facDev);
         if(p.dst_holes)
-            return tryJit(p, begin, end, si, di, S, D, s)
-                || (envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s));
+        {
+            if(tryJit(p, begin, end, si, di, S, D, s))
+                return trace("jit (holes)"), true;
+            trace("warp tile (holes)");
+            return envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s);
+        }
         if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("vec"), true;
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("pack"), true;
         if(!p.uni && trySplit(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("planes"), true;
         if(!p.uni && tryVecConvert(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("vec convert"), true;
         if(!p.uni && tryVecMulti(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("vec multi"), true;
         // uniform pairs get here when the register transpose cannot take them (AoSoA lanes that are not
         // a power of two or not a multiple of 16/size): the generated kernel measured 0.81-0.99 of HBM
         // on them against 0.59-0.71 for k_uniform_direct (profiles/r02/jit/jit_uni.log)
         if((!p.uni || envNum("LAMB_JIT_UNI", 1) != 0) && tryJit(p, begin, end, si, di, S, D, s))
-            return true;
+            return trace("jit"), true;
         // uniform pairs the register transpose cannot take (AoSoA lanes not a multiple of 16/size,
         // non-power-of-two lanes): direct per-element moves through L1 (k_uniform_direct), block /
         // lane by a magic multiply -- measured 1.7x over the warp-tile transpose (aosoa:2, aosoa:3)
@@ -1247,6 +1279,7 @@ namespace lamhost
             q.umag_s = q.ul_s > 1 ? static_cast<uint32_t>(((uint64_t{1} << 32) + q.ul_s - 1) / q.ul_s) : 0;
             q.umag_d = q.ul_d > 1 ? static_cast<uint32_t>(((uint64_t{1} << 32) + q.ul_d - 1) / q.ul_d) : 0;
             q.facS = q.facD = 0;
+            trace("uniform direct");
             lam_cuda_check(lamk::uniform_direct(q, end - begin, s), "uniform_direct");
             addAccessCounts(p, S, end - begin, s);
             return true;
@@ -1284,6 +1317,7 @@ namespace lamhost
                 }
                 if(8ull * (q.src_bytes + q.dst_bytes) <= 200 * 1024)
                 {
+                    trace("uniform warp");
                     lam_cuda_check(lamk::uniform_warp(q, static_cast<uint32_t>(ntw), s), "uniform_warp");
                     const uint64_t doneEnd = begin + ntw * wt;
                     if(doneEnd < end)
@@ -1295,7 +1329,8 @@ namespace lamhost
             }
         }
         if(envNum("LAMB_WARP_TILE", 1) != 0 && tryWarpTile(p, S, D, si, di, begin, end, s))
-            return true;
+            return trace("warp tile"), true;
+        trace("tma tile");
         lam_cuda_check(lamk::tile_copy(p, pl.smem, pl.ctas, s), "tile_copy");
         const uint64_t doneEnd = begin + ntiles * p.T;
         if(doneEnd < end)

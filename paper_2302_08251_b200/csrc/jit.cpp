@@ -83,6 +83,7 @@ namespace lamjit
         // compiled kernels by generated source (a failed compile is remembered as nullptr)
         std::mutex g_mu;
         std::map<std::string, cudaKernel_t> g_cache;
+        std::map<std::string, cudaKernel_t> g_keyCache; // by plan key (jit.cpp tryCopy)
 
         cudaKernel_t compile(const std::string& src)
         {
@@ -304,6 +305,39 @@ namespace lamjit
             for(uint32_t b = 0; b < 4; ++b)
                 if(srcOfDst[size_t(w) * 4 + b] == 0xFFFFFFFFu)
                     holeVec[w / 4] = true;
+        // pass-through spans: a destination block span that is byte for byte a source block span
+        // (an SoA leaf or byte plane on both sides, AoSoA<L> to AoSoA<L>, ...) is copied by the warp
+        // as one coalesced vector stream, without registers or slabs
+        std::vector<int> passSrc(sv[1].size(), -1);
+        std::vector<bool> srcPassed(sv[0].size(), false);
+        for(size_t m = 0; m < sv[1].size(); ++m)
+        {
+            const Span& dm = sv[1][m];
+            if(dm.run)
+                continue;
+            const uint32_t s0 = srcOfDst[size_t(dm.word0) * 4];
+            if(s0 == 0xFFFFFFFFu || (s0 & 3))
+                continue;
+            for(size_t k = 0; k < sv[0].size(); ++k)
+            {
+                const Span& sk = sv[0][k];
+                if(sk.run || srcPassed[k] || sk.word0 != (s0 >> 2) || sk.bytes != dm.bytes || sk.gstride != dm.gstride)
+                    continue;
+                bool same = true;
+                for(uint32_t w = 0; w < dm.bytes / 4 && same; ++w)
+                {
+                    same = boolMask[dm.word0 + w] == 0;
+                    for(uint32_t b = 0; b < 4 && same; ++b)
+                        same = srcOfDst[size_t(dm.word0 + w) * 4 + b] == (((sk.word0 + w) << 2) | b);
+                }
+                if(same)
+                {
+                    passSrc[m] = static_cast<int>(k);
+                    srcPassed[k] = true;
+                }
+                break;
+            }
+        }
 
         // ---- generate ----
         // A warp owns 32 consecutive groups.  A block span (G/L whole blocks) of K > 1 vectors per
@@ -323,41 +357,44 @@ namespace lamjit
         // unless the source's direct loads would not fit in registers; then the source only.
         // LAMB_JIT_STAGE = 1 (both), s, d, 0 (neither) overrides.
         uint32_t srcWords = 0;
-        for(const Span& sp : sv[0])
-            srcWords += sp.bytes / 4;
+        for(size_t k = 0; k < sv[0].size(); ++k)
+            if(!srcPassed[k])
+                srcWords += sv[0][k].bytes / 4;
         char mode = envStage && envStage[0] ? envStage[0] : 'a';
         const bool autoMode = mode == 'a';
         // widest block span on each side (16-byte vectors per thread)
         uint32_t maxK[2] = {0, 0};
         for(int side = 0; side < 2; ++side)
-            for(const Span& sp : sv[side])
-                if(!sp.run)
-                    maxK[side] = std::max(maxK[side], sp.bytes / 16);
+            for(size_t k = 0; k < sv[side].size(); ++k)
+                if(!sv[side][k].run && !(side ? passSrc[k] >= 0 : srcPassed[k]))
+                    maxK[side] = std::max(maxK[side], sv[side][k].bytes / 16);
         if(autoMode)
             mode = (srcWords <= 96 || maxK[1] > maxK[0]) ? 'd' : 's';
-        // a source too wide for registers, not staged: its vectors are loaded at first use
-        const bool lazySrc = mode == 'd' && srcWords > 96;
         const bool stageOn = mode != '0';
         const bool stageSide[2] = {mode != 'd', mode != 's'};
         std::vector<Lay> lay[2];
         uint32_t slab[2] = {0, 0}; // slab vectors per warp on each side
         uint32_t directWords = 0;
         for(int side = 0; side < 2; ++side)
-            for(const Span& sp : sv[side])
+            for(size_t k = 0; k < sv[side].size(); ++k)
             {
+                const Span& sp = sv[side][k];
+                const bool passed = side ? passSrc[k] >= 0 : srcPassed[k];
                 Lay l;
                 l.K = sp.bytes / 16;
-                l.staged = stageOn && stageSide[side] && !sp.run && l.K > 1;
+                l.staged = stageOn && stageSide[side] && !sp.run && l.K > 1 && !passed;
                 l.KP = l.K | 1u;
                 l.rb = slab[side];
                 if(l.staged)
                     slab[side] += 32 * l.KP;
-                else if(side == 0)
+                else if(side == 0 && !passed)
                     directWords += 4 * l.K;
                 lay[side].push_back(l);
             }
+        // a source too wide for registers and not staged: its vectors are loaded at first use
+        const bool lazySrc = directWords > 96;
         const uint32_t warpBytes = (slab[0] + slab[1]) * 16;
-        if(warpBytes > 100 * 1024 || (directWords > 96 && !lazySrc))
+        if(warpBytes > 100 * 1024)
             return false;
         bool anyHole = false;
         for(bool h : holeVec)
@@ -367,6 +404,56 @@ namespace lamjit
         const size_t nspan = sv[0].size() + sv[1].size();
         if(nspan > 96)
             return false;
+        // cache key: everything the generated source depends on (not the base pointers, begin or
+        // groups, which are kernel parameters), so a repeated pair skips generation entirely
+        std::string key;
+        auto put = [&](uint64_t x) { key.append(reinterpret_cast<const char*>(&x), sizeof x); };
+        put(G);
+        put(static_cast<uint64_t>(mode));
+        put(lazySrc);
+        put(slab[0]);
+        put(slab[1]);
+        for(int side = 0; side < 2; ++side)
+        {
+            put(sv[side].size());
+            for(size_t k = 0; k < sv[side].size(); ++k)
+            {
+                const Span& sp = sv[side][k];
+                const Lay& l = lay[side][k];
+                put(sp.run);
+                put(sp.gstride);
+                put((uint64_t(sp.lsh) << 32) | sp.bs);
+                put((uint64_t(sp.lmask) << 32) | sp.ls);
+                put((uint64_t(sp.bytes) << 32) | sp.word0);
+                put((uint64_t(l.staged) << 48) | (uint64_t(l.K) << 32) | (uint64_t(l.KP) << 16) | l.rb);
+            }
+        }
+        for(int x : passSrc)
+            put(static_cast<uint64_t>(static_cast<int64_t>(x)));
+        key.append(reinterpret_cast<const char*>(srcOfDst.data()), srcOfDst.size() * sizeof(uint32_t));
+        key.append(reinterpret_cast<const char*>(boolMask.data()), boolMask.size() * sizeof(uint32_t));
+        for(bool h : holeVec)
+            key.push_back(h ? '1' : '0');
+        cudaKernel_t kern = nullptr;
+        bool known = false;
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            auto it = g_keyCache.find(key);
+            if(it != g_keyCache.end())
+            {
+                known = true;
+                kern = it->second;
+            }
+        }
+        const char* dump = std::getenv("LAMB_JIT_DUMP");
+        if(known && dump)
+            if(FILE* fp = std::fopen(dump, "a"))
+            {
+                std::fprintf(fp, "// G=%u groups=%llu (cached)\n", G, static_cast<unsigned long long>(groups));
+                std::fclose(fp);
+            }
+        if(!known)
+        {
         std::ostringstream o;
         o << "struct LJP { unsigned long long base[" << nspan << "]; unsigned long long begin, groups; };\n"
           << "__device__ __forceinline__ unsigned prm(unsigned a, unsigned b, unsigned s) { unsigned r; "
@@ -419,9 +506,45 @@ namespace lamjit
                 o << "stg(a + 16ull * i, " << slabName << "[" << l.rb << "u + (i / " << l.K << "u) * " << l.KP << "u + i % "
                   << l.K << "u]); } }\n";
         };
+        // pass-through spans: warp-coalesced vector copies; the vectors of all such spans are
+        // batched 16 per lane, every load of a batch issued before its first store
+        {
+            std::vector<std::pair<size_t, uint32_t>> pv; // (destination span, vector j)
+            for(size_t m = 0; m < sv[1].size(); ++m)
+                if(passSrc[m] >= 0)
+                    for(uint32_t j = 0; j < lay[1][m].K; ++j)
+                        pv.emplace_back(m, j);
+            for(size_t m = 0; m < sv[1].size(); ++m)
+                if(passSrc[m] >= 0)
+                {
+                    const size_t k = static_cast<size_t>(passSrc[m]);
+                    o << "  const unsigned long long pa" << m << " = P.base[" << k << "] + gw * " << sv[0][k].gstride
+                      << "ull, pd" << m << " = P.base[" << sv[0].size() + m << "] + gw * " << sv[1][m].gstride << "ull;\n";
+                }
+            for(size_t b0 = 0; b0 < pv.size(); b0 += 16)
+            {
+                const size_t b1 = std::min(pv.size(), b0 + 16);
+                o << "  {\n";
+                for(size_t q = b0; q < b1; ++q)
+                {
+                    const size_t m = pv[q].first;
+                    const uint32_t j = pv[q].second, K = lay[1][m].K;
+                    o << "   uint4 t" << q - b0 << "; const unsigned i" << q - b0 << " = lane + " << 32 * j << "u; if(i" << q - b0
+                      << " < cnt * " << K << "u) t" << q - b0 << " = ldg(pa" << m << " + 16ull * i" << q - b0 << ");\n";
+                }
+                for(size_t q = b0; q < b1; ++q)
+                {
+                    const size_t m = pv[q].first;
+                    const uint32_t K = lay[1][m].K;
+                    o << "   if(i" << q - b0 << " < cnt * " << K << "u) stg(pd" << m << " + 16ull * i" << q - b0 << ", t" << q - b0
+                      << ");\n";
+                }
+                o << "  }\n";
+            }
+        }
         // direct source vectors first (most loads in flight), then the coalesced slab loads
         for(size_t k = 0; k < sv[0].size(); ++k)
-            if(!lay[0][k].staged && !lazySrc)
+            if(!lay[0][k].staged && !lazySrc && !srcPassed[k])
             {
                 for(uint32_t v = 0; v < lay[0][k].K; ++v)
                     o << "  uint4 S" << k << "_" << v << " = make_uint4(0u, 0u, 0u, 0u);\n";
@@ -444,7 +567,7 @@ namespace lamjit
         o << "  __syncwarp();\n  if(act) {\n";
         if(lazySrc)
             for(size_t k = 0; k < sv[0].size(); ++k)
-                if(!lay[0][k].staged)
+                if(!lay[0][k].staged && !srcPassed[k])
                     o << "   const unsigned long long as" << k << " = " << addr(sv[0][k], k) << ";\n";
         // source word w -> "S<k>_<v>.<c>"; staged vectors are read from the slab at first use
         std::vector<int> spanOfWord;
@@ -471,6 +594,8 @@ namespace lamjit
         };
         for(size_t k = 0; k < sv[1].size(); ++k)
         {
+            if(passSrc[k] >= 0)
+                continue; // copied above
             const Span& sp = sv[1][k];
             const Lay& l = lay[1][k];
             const size_t idx = sv[0].size() + k;
@@ -582,13 +707,16 @@ namespace lamjit
                 coop(sv[1][k], lay[1][k], sv[0].size() + k, false, "sd", "");
         o << "  __syncwarp();\n }\n}\n";
         const std::string src = o.str();
-        if(const char* dump = std::getenv("LAMB_JIT_DUMP"))
+        if(dump)
             if(FILE* fp = std::fopen(dump, "a"))
             {
                 std::fprintf(fp, "// G=%u groups=%llu\n%s\n", G, static_cast<unsigned long long>(groups), src.c_str());
                 std::fclose(fp);
             }
-        const cudaKernel_t kern = compile(src);
+        kern = compile(src);
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_keyCache[key] = kern;
+        }
         if(!kern)
             return false;
         // warps per CTA: 4 while the slabs fit 100 KB per CTA

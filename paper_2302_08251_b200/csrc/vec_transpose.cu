@@ -102,6 +102,8 @@ namespace lamk
                 uint4* slice = reinterpret_cast<uint4*>(vsm) + (threadIdx.x >> 5) * (32 * NL);
                 const uint32_t lane = threadIdx.x & 31;
                 const bool fullWarp = __activemask() == 0xFFFFFFFFu && (g - lane) + 32 <= p.groups;
+                // recordContig 2: AoSoA<V> blocks (leaf-major), vector k = leaf k's V values
+                const bool blockMajor = p.d.recordContig == 2;
                 if(fullWarp)
                 {
 #pragma unroll
@@ -113,7 +115,7 @@ namespace lamk
                         for(int j = 0; j < V; ++j)
                         {
                             const int word = k * V + j;
-                            w[j] = v[word % NL][word / NL];
+                            w[j] = blockMajor ? v[k][j] : v[word % NL][word / NL];
                         }
                         slice[lane * NL + k] = x;
                     }
@@ -136,7 +138,7 @@ namespace lamk
                         for(int j = 0; j < V; ++j)
                         {
                             const int word = k * V + j;
-                            w[j] = v[word % NL][word / NL];
+                            w[j] = blockMajor ? v[k][j] : v[word % NL][word / NL];
                         }
                         __stcs(base + k, x);
                     }
