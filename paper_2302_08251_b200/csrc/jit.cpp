@@ -313,15 +313,13 @@ namespace lamjit
         for(size_t m = 0; m < sv[1].size(); ++m)
         {
             const Span& dm = sv[1][m];
-            if(dm.run)
-                continue;
             const uint32_t s0 = srcOfDst[size_t(dm.word0) * 4];
             if(s0 == 0xFFFFFFFFu || (s0 & 3))
                 continue;
             for(size_t k = 0; k < sv[0].size(); ++k)
             {
                 const Span& sk = sv[0][k];
-                if(sk.run || srcPassed[k] || sk.word0 != (s0 >> 2) || sk.bytes != dm.bytes || sk.gstride != dm.gstride)
+                if(srcPassed[k] || sk.word0 != (s0 >> 2) || sk.bytes != dm.bytes)
                     continue;
                 bool same = true;
                 for(uint32_t w = 0; w < dm.bytes / 4 && same; ++w)
@@ -369,7 +367,11 @@ namespace lamjit
                 if(!sv[side][k].run && !(side ? passSrc[k] >= 0 : srcPassed[k]))
                     maxK[side] = std::max(maxK[side], sv[side][k].bytes / 16);
         if(autoMode)
-            mode = (srcWords <= 96 || maxK[1] > maxK[0]) ? 'd' : 's';
+            mode = (srcWords <= 128 || maxK[1] >= maxK[0]) ? 'd' : 's';
+        // uniform pairs whose sides are both wide blocks beyond the register budget (aosoa:8 <->
+        // aosoa:3, R64 aos-packed -> aosoa:3) measured faster on k_uniform_direct
+        if(autoMode && p.uni && srcWords > 128 && maxK[1] > 8)
+            return false;
         const bool stageOn = mode != '0';
         const bool stageSide[2] = {mode != 'd', mode != 's'};
         std::vector<Lay> lay[2];
@@ -392,7 +394,7 @@ namespace lamjit
                 lay[side].push_back(l);
             }
         // a source too wide for registers and not staged: its vectors are loaded at first use
-        const bool lazySrc = directWords > 96;
+        const bool lazySrc = directWords > 128;
         const uint32_t warpBytes = (slab[0] + slab[1]) * 16;
         if(warpBytes > 100 * 1024)
             return false;
@@ -460,6 +462,9 @@ namespace lamjit
              "asm(\"prmt.b32 %0, %1, %2, %3;\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(s)); return r; }\n"
           << "__device__ __forceinline__ unsigned bcn(unsigned w, unsigned m) { return (w & ~m) | (__vcmpne4(w & m, 0u) & m & "
              "0x01010101u); }\n"
+          << "__device__ __forceinline__ unsigned long long lj_run(unsigned long long base, unsigned long long e, unsigned sh, "
+             "unsigned long long bs, unsigned long long mask, unsigned long long ls, unsigned v) { return base + (e >> sh) * bs + "
+             "(e & mask) * ls + 16ull * v; }\n"
           << "__device__ __forceinline__ uint4 ldg(unsigned long long a) { uint4 v; asm volatile(\"ld.global.cs.v4.u32 "
              "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
           << "__device__ __forceinline__ uint4 ldo(unsigned long long a) { uint4 v; asm volatile(\"ld.global.v4.u32 "
@@ -507,8 +512,20 @@ namespace lamjit
                   << l.K << "u]); } }\n";
         };
         // pass-through spans: warp-coalesced vector copies; the vectors of all such spans are
-        // batched 16 per lane, every load of a batch issued before its first store
+        // batched 16 per lane, every load of a batch issued before its first store.  Vector i of
+        // the warp's region of span m is vector i % K of group gw + i / K: contiguous for a block
+        // span, and for a leaf run the runs of consecutive groups are adjacent inside a block.
         {
+            auto passAddr = [&](const Span& sp, size_t idx, const std::string& i, uint32_t K) -> std::string
+            {
+                std::ostringstream a;
+                if(!sp.run)
+                    a << "(pb" << idx << " + 16ull * " << i << ")";
+                else
+                    a << "lj_run(P.base[" << idx << "], P.begin + (gw + " << i << " / " << K << "u) * " << G << "ull, " << sp.lsh
+                      << "u, " << sp.bs << "ull, " << sp.lmask << "ull, " << sp.ls << "ull, " << i << " % " << K << "u)";
+                return a.str();
+            };
             std::vector<std::pair<size_t, uint32_t>> pv; // (destination span, vector j)
             for(size_t m = 0; m < sv[1].size(); ++m)
                 if(passSrc[m] >= 0)
@@ -516,27 +533,32 @@ namespace lamjit
                         pv.emplace_back(m, j);
             for(size_t m = 0; m < sv[1].size(); ++m)
                 if(passSrc[m] >= 0)
-                {
-                    const size_t k = static_cast<size_t>(passSrc[m]);
-                    o << "  const unsigned long long pa" << m << " = P.base[" << k << "] + gw * " << sv[0][k].gstride
-                      << "ull, pd" << m << " = P.base[" << sv[0].size() + m << "] + gw * " << sv[1][m].gstride << "ull;\n";
-                }
+                    for(int side = 0; side < 2; ++side)
+                    {
+                        const size_t k = side ? m : static_cast<size_t>(passSrc[m]);
+                        const Span& sp = sv[side][k];
+                        const size_t idx = side ? sv[0].size() + m : k;
+                        if(!sp.run)
+                            o << "  const unsigned long long pb" << idx << " = P.base[" << idx << "] + gw * " << sp.gstride << "ull;\n";
+                    }
             for(size_t b0 = 0; b0 < pv.size(); b0 += 16)
             {
                 const size_t b1 = std::min(pv.size(), b0 + 16);
                 o << "  {\n";
                 for(size_t q = b0; q < b1; ++q)
                 {
-                    const size_t m = pv[q].first;
+                    const size_t m = pv[q].first, k = static_cast<size_t>(passSrc[m]);
                     const uint32_t j = pv[q].second, K = lay[1][m].K;
-                    o << "   uint4 t" << q - b0 << "; const unsigned i" << q - b0 << " = lane + " << 32 * j << "u; if(i" << q - b0
-                      << " < cnt * " << K << "u) t" << q - b0 << " = ldg(pa" << m << " + 16ull * i" << q - b0 << ");\n";
+                    const std::string i = "i" + std::to_string(q - b0);
+                    o << "   uint4 t" << q - b0 << "; const unsigned " << i << " = lane + " << 32 * j << "u; if(" << i << " < cnt * " << K
+                      << "u) t" << q - b0 << " = ldg(" << passAddr(sv[0][k], k, i, K) << ");\n";
                 }
                 for(size_t q = b0; q < b1; ++q)
                 {
                     const size_t m = pv[q].first;
                     const uint32_t K = lay[1][m].K;
-                    o << "   if(i" << q - b0 << " < cnt * " << K << "u) stg(pd" << m << " + 16ull * i" << q - b0 << ", t" << q - b0
+                    const std::string i = "i" + std::to_string(q - b0);
+                    o << "   if(" << i << " < cnt * " << K << "u) stg(" << passAddr(sv[1][m], sv[0].size() + m, i, K) << ", t" << q - b0
                       << ");\n";
                 }
                 o << "  }\n";
