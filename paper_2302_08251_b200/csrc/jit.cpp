@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -84,6 +85,7 @@ namespace lamjit
         std::mutex g_mu;
         std::map<std::string, cudaKernel_t> g_cache;
         std::map<std::string, cudaKernel_t> g_keyCache; // by plan key (jit.cpp tryCopy)
+        std::map<std::string, char> g_modeCache;         // autotuned staging mode per pair
 
         cudaKernel_t compile(const std::string& src)
         {
@@ -152,28 +154,38 @@ namespace lamjit
         const uint32_t nl = p.nleaves;
         if(nl < 1 || nl > LAMT_MAX_LEAVES)
             return false;
-        // every leaf a byte move without conversion; a side is one physical term of the value's
-        // size, or byte planes (Bytesplit, computed.cpp:405-502: term k holds byte k)
-        std::vector<uint32_t> vsz(nl);
+        // every leaf a byte move, or a ChangeType conversion (computed.cpp:228-404) between f32 and
+        // f64 or between integer types; a side is one physical term of its stored size, or byte
+        // planes (Bytesplit, computed.cpp:405-502: term k holds byte k)
+        auto isInt = [](int t) { return t <= lamb::U64; };
+        auto cvtOk = [&](int a, int b)
+        {
+            return a == b || ((a == lamb::F32 || a == lamb::F64) && (b == lamb::F32 || b == lamb::F64)) || (isInt(a) && isInt(b));
+        };
+        std::vector<uint32_t> ssz(nl), dsz(nl);
+        std::vector<bool> conv(nl, false);
         for(uint32_t f = 0; f < nl; ++f)
         {
             const lamt_leaf& L = p.leaf[f];
-            if(L.stype != L.dtype || L.stype != L.ltype)
+            if(!cvtOk(L.stype, L.ltype) || !cvtOk(L.ltype, L.dtype))
                 return false;
-            vsz[f] = static_cast<uint32_t>(lamb::scalarSize(L.ltype));
+            conv[f] = L.stype != L.ltype || L.ltype != L.dtype;
+            ssz[f] = static_cast<uint32_t>(lamb::scalarSize(L.stype));
+            dsz[f] = static_cast<uint32_t>(lamb::scalarSize(L.dtype));
             for(int side = 0; side < 2; ++side)
             {
                 const uint8_t kind = side ? L.dkind : L.skind;
                 const uint8_t nt = side ? L.dn : L.sn;
                 const lamt_term* t = side ? L.d : L.s;
+                const uint32_t sz = side ? dsz[f] : ssz[f];
                 if(kind == LAMT_K_PHYS)
                 {
-                    if(t[0].size != vsz[f])
+                    if(t[0].size != sz)
                         return false;
                 }
                 else if(kind == LAMT_K_SPLIT)
                 {
-                    if(nt != vsz[f])
+                    if(nt != sz)
                         return false;
                     for(uint32_t k = 0; k < nt; ++k)
                         if(t[k].size != 1)
@@ -199,7 +211,8 @@ namespace lamjit
             {
                 const lamt_leaf& lf = p.leaf[f];
                 const bool split = (src ? lf.skind : lf.dkind) == LAMT_K_SPLIT;
-                const uint32_t nt = split ? vsz[f] : 1;
+                const uint32_t vs = src ? ssz[f] : dsz[f];
+                const uint32_t nt = split ? vs : 1;
                 for(uint32_t k = 0; k < nt; ++k)
                 {
                     const lamt_term& t = src ? lf.s[k] : lf.d[k];
@@ -243,7 +256,7 @@ namespace lamjit
                     else
                         return false;
                     // value bytes this term holds: all of them (physical) or byte k (plane)
-                    const uint32_t b0 = split ? k : 0, nb = split ? 1 : vsz[f];
+                    const uint32_t b0 = split ? k : 0, nb = split ? 1 : vs;
                     for(uint32_t j = 0; j < G; ++j)
                         for(uint32_t i = 0; i < nb; ++i)
                         {
@@ -289,16 +302,35 @@ namespace lamjit
         std::vector<uint32_t> srcOfDst(size_t(dWords) * 4, 0xFFFFFFFFu);
         // bytes of bool leaves: canonicalised to 0 / 1 (any non-zero byte reads as true, scalar.hpp)
         std::vector<uint32_t> boolMask(dWords, 0);
+        // converted values are "virtual" source words after the real ones: value (f, j) converted
+        // to the destination's stored type, ceil(dsz / 4) words
+        uint32_t sWordsAll = 0;
+        for(const Span& sp : sv[0])
+            sWordsAll += sp.bytes / 4;
+        struct Virt
+        {
+            uint32_t f, j, first;
+        };
+        std::vector<Virt> virt; // per virtual word
         for(uint32_t f = 0; f < nl; ++f)
             for(uint32_t j = 0; j < G; ++j)
-                for(uint32_t b = 0; b < vsz[f]; ++b)
+            {
+                uint32_t vid = 0;
+                if(conv[f])
+                {
+                    vid = sWordsAll + static_cast<uint32_t>(virt.size());
+                    for(uint32_t q = 0; q < (dsz[f] + 3) / 4; ++q)
+                        virt.push_back({f, j, vid});
+                }
+                for(uint32_t b = 0; b < dsz[f]; ++b)
                 {
                     const size_t k = (size_t(f) * G + j) * 16 + b;
                     const uint32_t d = wD[k];
-                    srcOfDst[size_t(d >> 2) * 4 + (d & 3)] = wS[k];
-                    if(p.leaf[f].ltype == lamb::Bool)
+                    srcOfDst[size_t(d >> 2) * 4 + (d & 3)] = conv[f] ? (((vid + b / 4) << 2) | (b & 3)) : wS[k];
+                    if(!conv[f] && p.leaf[f].ltype == lamb::Bool)
                         boolMask[d >> 2] |= 0xFFu << (8 * (d & 3));
                 }
+            }
         // destination vectors with holes are preloaded
         std::vector<bool> holeVec(dWords / 4, false);
         for(uint32_t w = 0; w < dWords; ++w)
@@ -358,20 +390,22 @@ namespace lamjit
         for(size_t k = 0; k < sv[0].size(); ++k)
             if(!srcPassed[k])
                 srcWords += sv[0][k].bytes / 4;
-        char mode = envStage && envStage[0] ? envStage[0] : 'a';
-        const bool autoMode = mode == 'a';
+        const char forcedMode = envStage && envStage[0] ? envStage[0] : 'a';
+        const bool autoMode = forcedMode == 'a';
         // widest block span on each side (16-byte vectors per thread)
         uint32_t maxK[2] = {0, 0};
         for(int side = 0; side < 2; ++side)
             for(size_t k = 0; k < sv[side].size(); ++k)
                 if(!sv[side][k].run && !(side ? passSrc[k] >= 0 : srcPassed[k]))
                     maxK[side] = std::max(maxK[side], sv[side][k].bytes / 16);
-        if(autoMode)
-            mode = (srcWords <= 128 || maxK[1] >= maxK[0]) ? 'd' : 's';
+        const char heuristic = (srcWords <= 128 || maxK[1] >= maxK[0]) ? 'd' : 's';
         // uniform pairs whose sides are both wide blocks beyond the register budget (aosoa:8 <->
         // aosoa:3, R64 aos-packed -> aosoa:3) measured faster on k_uniform_direct
         if(autoMode && p.uni && srcWords > 128 && maxK[1] > 8)
             return false;
+        // one generated kernel per staging mode; timedMs != nullptr times the launch (autotuning)
+        auto attempt = [&](char mode, float* timedMs) -> bool
+        {
         const bool stageOn = mode != '0';
         const bool stageSide[2] = {mode != 'd', mode != 's'};
         std::vector<Lay> lay[2];
@@ -411,7 +445,7 @@ namespace lamjit
         std::string key;
         auto put = [&](uint64_t x) { key.append(reinterpret_cast<const char*>(&x), sizeof x); };
         put(G);
-        put(static_cast<uint64_t>(mode));
+        put(static_cast<uint64_t>(static_cast<unsigned char>(mode)));
         put(lazySrc);
         put(slab[0]);
         put(slab[1]);
@@ -432,6 +466,8 @@ namespace lamjit
         }
         for(int x : passSrc)
             put(static_cast<uint64_t>(static_cast<int64_t>(x)));
+        for(uint32_t f = 0; f < nl; ++f)
+            put((uint64_t(p.leaf[f].stype) << 16) | (uint64_t(p.leaf[f].ltype) << 8) | p.leaf[f].dtype);
         key.append(reinterpret_cast<const char*>(srcOfDst.data()), srcOfDst.size() * sizeof(uint32_t));
         key.append(reinterpret_cast<const char*>(boolMask.data()), boolMask.size() * sizeof(uint32_t));
         for(bool h : holeVec)
@@ -462,6 +498,22 @@ namespace lamjit
              "asm(\"prmt.b32 %0, %1, %2, %3;\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(s)); return r; }\n"
           << "__device__ __forceinline__ unsigned bcn(unsigned w, unsigned m) { return (w & ~m) | (__vcmpne4(w & m, 0u) & m & "
              "0x01010101u); }\n"
+          << "__device__ __forceinline__ void lj_cvt(unsigned lo, unsigned hi, int from, int to, unsigned& ol, unsigned& oh) {\n"
+             " if(from == to) { ol = lo; oh = hi; return; }\n"
+             " if(from == 8 && to == 9) { unsigned long long r;\n"
+             "  if((lo & 0x7F800000u) == 0x7F800000u && (lo & 0x7FFFFFu)) r = ((unsigned long long)(lo >> 31) << 63) | "
+             "0x7FF8000000000000ull | ((unsigned long long)(lo & 0x7FFFFFu) << 29);\n"
+             "  else r = (unsigned long long)__double_as_longlong((double)__uint_as_float(lo));\n"
+             "  ol = (unsigned)r; oh = (unsigned)(r >> 32); return; }\n"
+             " if(from == 9 && to == 8) { const unsigned long long b = lo | ((unsigned long long)hi << 32); oh = 0u;\n"
+             "  if((b & 0x7FF0000000000000ull) == 0x7FF0000000000000ull && (b & 0x000FFFFFFFFFFFFFull)) "
+             "ol = ((hi >> 31) << 31) | 0x7FC00000u | (unsigned)((b >> 29) & 0x3FFFFFu);\n"
+             "  else ol = __float_as_uint(__double2float_rn(__longlong_as_double((long long)b))); return; }\n"
+             " const unsigned fw = 8u * ((0x18484218421ull >> (4 * from)) & 0xF), tw = 8u * ((0x18484218421ull >> (4 * to)) & 0xF);\n"
+             " unsigned long long v = lo | ((unsigned long long)hi << 32);\n"
+             " if(from <= 3 && fw < 64) { const unsigned long long sb = 1ull << (fw - 1); v = ((v & ((1ull << fw) - 1ull)) ^ sb) - sb; }\n"
+             " if(tw < 64) v &= (1ull << tw) - 1ull;\n"
+             " ol = (unsigned)v; oh = (unsigned)(v >> 32); }\n"
           << "__device__ __forceinline__ unsigned long long lj_run(unsigned long long base, unsigned long long e, unsigned sh, "
              "unsigned long long bs, unsigned long long mask, unsigned long long ls, unsigned v) { return base + (e >> sh) * bs + "
              "(e & mask) * ls + 16ull * v; }\n"
@@ -597,8 +649,105 @@ namespace lamjit
             for(uint32_t w = 0; w < sv[0][k].bytes / 4; ++w)
                 spanOfWord.push_back(static_cast<int>(k));
         std::vector<bool> emitted(spanOfWord.size() / 4, false);
-        auto srcWord = [&](uint32_t w) -> std::string
+        // a word from 4 (variable, byte) pairs: a PRMT chain whose first step takes the bytes of two
+        // words and each further step adds one ("0u" supplies zero bytes)
+        auto assemble = [&](const std::string* var, const uint32_t* byt) -> std::string
         {
+            if(var[0] == var[1] && var[1] == var[2] && var[2] == var[3] && byt[0] == 0 && byt[1] == 1 && byt[2] == 2
+               && byt[3] == 3)
+                return var[0];
+            std::string acc;
+            bool placed[4] = {false, false, false, false};
+            for(uint32_t b = 0; b < 4; ++b)
+            {
+                if(placed[b])
+                    continue;
+                const std::string x = var[b];
+                uint32_t sel = 0;
+                std::ostringstream e;
+                if(acc.empty())
+                {
+                    std::string y;
+                    for(uint32_t c2 = 0; c2 < 4; ++c2)
+                        if(var[c2] != x && y.empty())
+                            y = var[c2];
+                    for(uint32_t c2 = 0; c2 < 4; ++c2)
+                    {
+                        uint32_t nib = 0;
+                        if(var[c2] == x)
+                        {
+                            nib = byt[c2];
+                            placed[c2] = true;
+                        }
+                        else if(!y.empty() && var[c2] == y)
+                        {
+                            nib = 4 + byt[c2];
+                            placed[c2] = true;
+                        }
+                        sel |= nib << (4 * c2);
+                    }
+                    e << "prm(" << x << ", " << (y.empty() ? x : y) << ", 0x" << std::hex << sel << std::dec << "u)";
+                }
+                else
+                {
+                    for(uint32_t c2 = 0; c2 < 4; ++c2)
+                    {
+                        uint32_t nib = c2;
+                        if(!placed[c2] && var[c2] == x)
+                        {
+                            nib = 4 + byt[c2];
+                            placed[c2] = true;
+                        }
+                        sel |= nib << (4 * c2);
+                    }
+                    e << "prm(" << acc << ", " << x << ", 0x" << std::hex << sel << std::dec << "u)";
+                }
+                acc = e.str();
+            }
+            return acc;
+        };
+        std::vector<bool> vEmitted(virt.size(), false);
+        std::function<std::string(uint32_t)> srcWord;
+        srcWord = [&](uint32_t w) -> std::string
+        {
+            if(w >= sWordsAll)
+            {
+                // a converted value: gather its stored bytes, convert stype -> ltype -> dtype
+                const Virt& vt = virt[w - sWordsAll];
+                const uint32_t first = vt.first - sWordsAll;
+                const std::string nm = "V" + std::to_string(first);
+                if(!vEmitted[first])
+                {
+                    vEmitted[first] = true;
+                    const lamt_leaf& lf = p.leaf[vt.f];
+                    std::string half[2];
+                    for(uint32_t h = 0; h < 2; ++h)
+                    {
+                        std::string var[4];
+                        uint32_t byt[4];
+                        for(uint32_t b = 0; b < 4; ++b)
+                        {
+                            const uint32_t vb = 4 * h + b;
+                            if(vb < ssz[vt.f])
+                            {
+                                const uint32_t sw = wS[(size_t(vt.f) * G + vt.j) * 16 + vb];
+                                var[b] = srcWord(sw >> 2);
+                                byt[b] = sw & 3;
+                            }
+                            else
+                            {
+                                var[b] = "0u";
+                                byt[b] = 0;
+                            }
+                        }
+                        half[h] = (4 * h < ssz[vt.f]) ? assemble(var, byt) : "0u";
+                    }
+                    o << "   unsigned " << nm << "_0, " << nm << "_1;\n   { unsigned t0, t1; lj_cvt(" << half[0] << ", " << half[1]
+                      << ", " << int(lf.stype) << ", " << int(lf.ltype) << ", t0, t1); lj_cvt(t0, t1, " << int(lf.ltype) << ", "
+                      << int(lf.dtype) << ", " << nm << "_0, " << nm << "_1); }\n";
+                }
+                return nm + "_" + std::to_string(w - vt.first);
+            }
             const int k = spanOfWord[w];
             const uint32_t v = (w - sv[0][k].word0) / 4;
             if(lay[0][k].staged && !emitted[w / 4])
@@ -655,64 +804,7 @@ namespace lamjit
                             byt[b] = sw & 3;
                         }
                     }
-                    if(var[0] == var[1] && var[1] == var[2] && var[2] == var[3] && byt[0] == 0 && byt[1] == 1 && byt[2] == 2
-                       && byt[3] == 3)
-                    {
-                        dn[c] = var[0];
-                        if(boolMask[w])
-                            dn[c] = "bcn(" + dn[c] + ", " + std::to_string(boolMask[w]) + "u)";
-                        continue;
-                    }
-                    // PRMT chain: the first step takes bytes of two words, each further step adds one
-                    std::string acc;
-                    bool placed[4] = {false, false, false, false};
-                    for(uint32_t b = 0; b < 4; ++b)
-                    {
-                        if(placed[b])
-                            continue;
-                        const std::string x = var[b];
-                        uint32_t sel = 0;
-                        std::ostringstream e;
-                        if(acc.empty())
-                        {
-                            std::string y;
-                            for(uint32_t c2 = 0; c2 < 4; ++c2)
-                                if(var[c2] != x && y.empty())
-                                    y = var[c2];
-                            for(uint32_t c2 = 0; c2 < 4; ++c2)
-                            {
-                                uint32_t nib = 0;
-                                if(var[c2] == x)
-                                {
-                                    nib = byt[c2];
-                                    placed[c2] = true;
-                                }
-                                else if(!y.empty() && var[c2] == y)
-                                {
-                                    nib = 4 + byt[c2];
-                                    placed[c2] = true;
-                                }
-                                sel |= nib << (4 * c2);
-                            }
-                            e << "prm(" << x << ", " << (y.empty() ? x : y) << ", 0x" << std::hex << sel << std::dec << "u)";
-                        }
-                        else
-                        {
-                            for(uint32_t c2 = 0; c2 < 4; ++c2)
-                            {
-                                uint32_t nib = c2;
-                                if(!placed[c2] && var[c2] == x)
-                                {
-                                    nib = 4 + byt[c2];
-                                    placed[c2] = true;
-                                }
-                                sel |= nib << (4 * c2);
-                            }
-                            e << "prm(" << acc << ", " << x << ", 0x" << std::hex << sel << std::dec << "u)";
-                        }
-                        acc = e.str();
-                    }
-                    dn[c] = acc;
+                    dn[c] = assemble(var, byt);
                     if(boolMask[w])
                         dn[c] = "bcn(" + dn[c] + ", " + std::to_string(boolMask[w]) + "u)";
                 }
@@ -769,8 +861,23 @@ namespace lamjit
         const uint64_t want = (warps + wpc - 1) / wpc;
         const uint64_t cap = static_cast<uint64_t>(lamk::sm_count(dev)) * (64 / wpc);
         const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        if(timedMs)
+        {
+            cudaEventCreate(&ev[0]);
+            cudaEventCreate(&ev[1]);
+            cudaEventRecord(ev[0], s);
+        }
         const cudaError_t e =
             cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(32 * wpc), args, smem, s);
+        if(timedMs)
+        {
+            cudaEventRecord(ev[1], s);
+            cudaEventSynchronize(ev[1]);
+            cudaEventElapsedTime(timedMs, ev[0], ev[1]);
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+        }
         if(e != cudaSuccess)
         {
             cudaGetLastError();
@@ -779,5 +886,67 @@ namespace lamjit
         lamk::count_launch();
         *doneEnd = begin + groups * G;
         return true;
+        };
+
+        if(!autoMode)
+            return attempt(forcedMode, nullptr);
+        // Staging mode: the heuristic above, or -- the first time a pair is copied at >= 2^22
+        // elements outside stream capture -- the fastest of the four modes, each timed on the copy
+        // itself (every mode writes the same bytes, so the last timed launch leaves the finished
+        // copy), remembered per pair.  LAMB_JIT_TUNE=0 keeps the heuristic.
+        std::string pairKey;
+        {
+            auto put = [&](uint64_t x) { pairKey.append(reinterpret_cast<const char*>(&x), sizeof x); };
+            put(G);
+            for(int side = 0; side < 2; ++side)
+                for(const Span& sp : sv[side])
+                {
+                    put(sp.run);
+                    put(sp.gstride);
+                    put((uint64_t(sp.lsh) << 32) | sp.bs);
+                    put((uint64_t(sp.lmask) << 32) | sp.ls);
+                    put((uint64_t(sp.bytes) << 32) | sp.word0);
+                }
+            for(uint32_t f = 0; f < nl; ++f)
+                put((uint64_t(p.leaf[f].stype) << 16) | (uint64_t(p.leaf[f].ltype) << 8) | p.leaf[f].dtype);
+            pairKey.append(reinterpret_cast<const char*>(srcOfDst.data()), srcOfDst.size() * sizeof(uint32_t));
+            pairKey.append(reinterpret_cast<const char*>(boolMask.data()), boolMask.size() * sizeof(uint32_t));
+        }
+        char chosen = heuristic;
+        bool decided = false;
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            auto it = g_modeCache.find(pairKey);
+            if(it != g_modeCache.end())
+            {
+                chosen = it->second;
+                decided = true;
+            }
+        }
+        const char* tune = std::getenv("LAMB_JIT_TUNE");
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if(!decided && !(tune && tune[0] == '0') && groups * G >= (uint64_t{1} << 22) && cap == cudaStreamCaptureStatusNone)
+        {
+            float best = 0;
+            char bestMode = 0;
+            for(char m : {'d', 's', '1', '0'})
+            {
+                float ms = 0;
+                if(!attempt(m, nullptr)) // warm: module load, first-touch
+                    continue;
+                if(attempt(m, &ms) && (bestMode == 0 || ms < best))
+                {
+                    best = ms;
+                    bestMode = m;
+                }
+            }
+            if(bestMode == 0)
+                return false;
+            std::lock_guard<std::mutex> lk(g_mu);
+            g_modeCache[pairKey] = bestMode;
+            return true;
+        }
+        return attempt(chosen, nullptr);
     }
 } // namespace lamjit

@@ -134,3 +134,32 @@ def test_jit_bool_bytes_canonicalise(schema, a, b, tmp_path, monkeypatch):
     for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
         assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
     assert _dump_size(dump) > 0
+
+
+@pytest.mark.parametrize("schema,a,b", [
+    (MIX4, "aos-packed", "changetype:f64=f32:soa-mb"), (MIX4, "changetype:f64=f32:aosoa:8", "aos-aligned"),
+    (MIX4, "soa-mb", "changetype:f32=f64,u16=u32,i8=i64:aos-packed"),
+    (MIXED, "aos-packed", "changetype:f64=f32,i8=i64,u16=u8:aosoa:2"),
+    (MIXED, "changetype:f64=f32,i8=i64,u16=u8:aosoa:2", "soa-mb"),
+    (MIXED, "aosoa:8", "changetype:h.y=f64:bytesplit:soa-mb"),
+    ("Record{Pos:Record{x:f32,y:f32,z:f32},Vel:Record{x:f32,y:f32,z:f32},Mass:f32}", "aosoa:3", "changetype:f32=f64:soa-mb"),
+])
+def test_jit_conversions_raw_bytes(schema, a, b, tmp_path, monkeypatch):
+    """ChangeType conversions in the generated kernel (f32 <-> f64 with NaN payloads, integer
+    sign extension and truncation) on source blobs of random bytes, against the oracle."""
+    from paper_2302_08251_b200 import lamina as L
+    dump = str(tmp_path / "jit.cu")
+    monkeypatch.setenv("LAMB_JIT_DUMP", dump)
+    n = 4111
+    ext = f"i32:[{n}]"
+    ms, md = O.make(schema, ext, a), O.make(schema, ext, b)
+    rng = np.random.default_rng(17)
+    sb = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(ms)]
+    db = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(md)]
+    gs, gd = L.View(L.Layout(schema, ext, a)), L.View(L.Layout(schema, ext, b))
+    gs.upload_all(sb)
+    gd.upload_all(db)
+    O.copy_view(ms, sb, md, db)
+    L.copy_view(gs, gd)
+    for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
+        assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"

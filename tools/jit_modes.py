@@ -11,7 +11,10 @@ n = 1 << 24
 PAIRS = [(R32, "aosoa:8", "aosoa:3"), (R32, "aosoa:3", "aosoa:8"), (R32, "soa-mb", "bytesplit:soa-mb"),
          (R32, "bytesplit:soa-mb", "soa-mb"), (MIXED, "aos-packed", "aosoa:3"), (MIXED, "aos-packed", "soa-mb"),
          (MIXED, "soa-mb", "aos-aligned"), (MIXED, "aosoa:32", "aos-aligned"), (MIXED, "aosoa:8", "aosoa:32"),
-         (MIXED, "bytesplit:soa-mb", "aosoa:32"), (R64, "aos-packed", "aosoa:3")]
+         (MIXED, "bytesplit:soa-mb", "aosoa:32"), (R64, "aos-packed", "aosoa:3"),
+         (MIXED, "aos-packed", "changetype:f64=f32,i8=i64,u16=u8:aosoa:2"), (R32, "changetype:f32=f64:soa-mb", "aosoa:3"),
+         (R32, "changetype:f32=f64:soa-mb", "bytesplit:soa-mb"), (R32, "aosoa:3", "changetype:f32=f64:soa-mb"),
+         ("Record{a:f64,b:u16,c:i8,d:f32}", "aos-packed", "changetype:f64=f32:soa-mb")]
 def t(s, d):
     L.copy_view(s, d)
     torch.cuda.synchronize()
