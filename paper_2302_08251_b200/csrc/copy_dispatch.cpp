@@ -108,12 +108,16 @@ namespace lamhost
         if(!all32(S) || S.heat || D.heat)
             return false;
         const bool sb = hasBits(S), db = hasBits(D);
-        if(sb == db)
+        if(!sb && !db)
             return false;
+        // bit streams on both sides (different widths or formats, or the same computed layout):
+        // unpack into the scratch, pack from it
+        if(sb && db)
+            return true;
         const Lowered& phys = sb ? D : S; // the non-packed side
         for(uint16_t r : phys.roots)
             if(phys.nodes[r].kind != LAMP_PHYS)
-                return false;
+                return true; // byte planes / ChangeType / Split against bits: both halves specialised
         if(recordSide32(phys) && uniformBits(sb ? S : D) && !(std::getenv("LAMB_RECPACK") && std::getenv("LAMB_RECPACK")[0] == '0'))
             return false;
         return !leafContig32(phys);
