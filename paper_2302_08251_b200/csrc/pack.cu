@@ -813,6 +813,16 @@ namespace lamk
             launch_rec<19, 1>(q, pack, grid, smem, s);
         else if(q.E == 5 && q.M == 10)
             launch_rec<16, 2>(q, pack, grid, smem, s);
+        else if(q.E <= 8 && q.M <= 23)
+        {
+            // the branch-free f32 codec (FMT 3); compile-time W for the 8- and 16-bit formats
+            if(q.w == 8)
+                launch_rec<8, 3>(q, pack, grid, smem, s);
+            else if(q.w == 16)
+                launch_rec<16, 3>(q, pack, grid, smem, s);
+            else
+                launch_rec<0, 3>(q, pack, grid, smem, s);
+        }
         else
             launch_rec<0, 4>(q, pack, grid, smem, s);
         count_launch();

@@ -445,3 +445,18 @@ def test_bitpack_float_f32_formats(fmt, phys):
     pb = O.zero_blobs(packed)
     O.write_all(packed, pb, vals)
     run_pair(R32, n, f"bitpack-float:{fmt}", phys, O.read_all(packed, pb))
+
+
+@pytest.mark.parametrize("fmt", ["4,3", "5,2", "3,4", "8,7", "6,9", "2,1"])
+@pytest.mark.parametrize("rec", ["aos-packed", "aosoa:8", "aosoa:4"])
+def test_bitpack_float_record_side_formats(fmt, rec):
+    """Record side <-> minifloat bit streams in one pass (k_rec_pack / k_rec_unpack with the
+    branch-free f32 codec, compile-time W for 8 and 16 bits), both directions, specials included."""
+    n = 2053
+    rng = np.random.default_rng(int(fmt.replace(",", "")) + len(rec))
+    vals = random_values(rng, [8] * 7, n)
+    run_pair(R32, n, rec, f"bitpack-float:{fmt}", vals)
+    packed = O.make(R32, f"i32:[{n}]", f"bitpack-float:{fmt}")
+    pb = O.zero_blobs(packed)
+    O.write_all(packed, pb, vals)
+    run_pair(R32, n, f"bitpack-float:{fmt}", rec, O.read_all(packed, pb))
