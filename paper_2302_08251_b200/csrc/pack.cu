@@ -11,6 +11,8 @@
 //        streams, computed.cpp:363-378, 473-490): a thread owns 4 records, loads them as
 //        16-byte vectors, converts with x86 NaN rules and writes one 32-bit word per plane.
 #include "device_common.cuh"
+
+#include <cstdlib>
 #include "launch.h"
 
 namespace lamk
@@ -108,6 +110,10 @@ namespace lamk
             return lamd::encode_e5m10_f32(v);
         else if constexpr(FMT == 3)
             return lamd::f32_encode_bf(fc, v);
+        else if constexpr(FMT == 5)
+            return lamd::f32_encode_bf(lamd::f32_codec(4, 3), v); // e4m3: every constant an immediate
+        else if constexpr(FMT == 6)
+            return lamd::f32_encode_bf(lamd::f32_codec(5, 2), v); // e5m2
         else
             return static_cast<uint32_t>(lamd::float_encode_f32(v, p.E, p.M));
     }
@@ -139,6 +145,10 @@ namespace lamk
         }
         else if constexpr(FMT == 3)
             return lamd::f32_decode_bf(fc, pat);
+        else if constexpr(FMT == 5)
+            return lamd::f32_decode_bf(lamd::f32_codec(4, 3), pat);
+        else if constexpr(FMT == 6)
+            return lamd::f32_decode_bf(lamd::f32_codec(5, 2), pat);
         else if(p.E <= 8 && p.M <= 23)
             return lamd::float_decode_f32(pat, p.E, p.M);
         else
@@ -218,7 +228,7 @@ namespace lamk
     // W from 10 to 30 but 16); a (256, 4) bound on e8m10 had cost it 17% (profiles/README.md)
     __host__ __device__ constexpr int pack_minb(int W, int FMT)
     {
-        return (FMT == 0 && W >= 10 && W % 2 == 0 && W != 16 && W != 32) || (FMT == 3 && W != 0) ? 2 : 3;
+        return (FMT == 0 && W >= 10 && W % 2 == 0 && W != 16 && W != 32) || ((FMT == 3 || FMT >= 5) && W != 0) ? 2 : 3;
     }
 
     template<int W, int FMT>
@@ -796,6 +806,12 @@ namespace lamk
     }
 
     // kind: 0 int, 1 float
+    static int envNum32(const char* name, int dflt)
+    {
+        const char* e = std::getenv(name);
+        return e ? std::atoi(e) : dflt;
+    }
+
     bool rec_pack(const RecPackParams& q, uint32_t kind, bool pack, cudaStream_t s)
     {
         if(q.groups == 0 || q.w < 1 || q.w > 32 || q.nl < 1 || q.nl > 8 || q.begin % 32
@@ -816,7 +832,11 @@ namespace lamk
         else if(q.E <= 8 && q.M <= 23)
         {
             // the branch-free f32 codec (FMT 3); compile-time W for the 8- and 16-bit formats
-            if(q.w == 8)
+            if(q.E == 4 && q.M == 3 && envNum32("LAMB_PACK_CONSTFMT", 1))
+                launch_rec<8, 5>(q, pack, grid, smem, s);
+            else if(q.E == 5 && q.M == 2 && envNum32("LAMB_PACK_CONSTFMT", 1))
+                launch_rec<8, 6>(q, pack, grid, smem, s);
+            else if(q.w == 8)
                 launch_rec<8, 3>(q, pack, grid, smem, s);
             else if(q.w == 16)
                 launch_rec<16, 3>(q, pack, grid, smem, s);
@@ -891,7 +911,10 @@ namespace lamk
         else if(p.E == 5 && p.M == 10)
             launch_pack<16, 2>(p, pack, grid, smem, s);
         else if(p.E > 8 || p.M > 23
-                || !dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{}))
+                || !((p.E == 4 && p.M == 3 && envNum32("LAMB_PACK_CONSTFMT", 1) ? (launch_pack<8, 5>(p, pack, grid, smem, s), true)
+                      : p.E == 5 && p.M == 2 && envNum32("LAMB_PACK_CONSTFMT", 1) ? (launch_pack<8, 6>(p, pack, grid, smem, s), true)
+                                                                                   : false)
+                     || dispatch_flt(static_cast<int>(p.w), p, pack, grid, smem, s, std::make_integer_sequence<int, 31>{})))
             launch_pack<0, 4>(p, pack, grid, smem, s);
         count_launch();
         lam_cuda_check(cudaGetLastError(), "kernel launch");
