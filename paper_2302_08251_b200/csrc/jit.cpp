@@ -36,6 +36,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace lamjit
@@ -85,7 +86,7 @@ namespace lamjit
         std::mutex g_mu;
         std::map<std::string, cudaKernel_t> g_cache;
         std::map<std::string, cudaKernel_t> g_keyCache; // by plan key (jit.cpp tryCopy)
-        std::map<std::string, char> g_modeCache;         // autotuned staging mode per pair
+        std::map<std::string, std::pair<char, int>> g_modeCache; // autotuned (staging mode, minB) per pair
 
         cudaKernel_t compile(const std::string& src)
         {
@@ -404,7 +405,11 @@ namespace lamjit
         if(autoMode && p.uni && srcWords > 128 && maxK[1] > 8)
             return false;
         // one generated kernel per staging mode; timedMs != nullptr times the launch (autotuning)
-        auto attempt = [&](char mode, float* timedMs) -> bool
+        const char* envMinB = std::getenv("LAMB_JIT_MINB");
+        const int forcedMinB = envMinB ? std::atoi(envMinB) : 0;
+        // minB: CTAs per SM the register allocation must allow (__launch_bounds__ second argument,
+        // 0 = none); prepareOnly: generate and compile, do not launch
+        auto attempt = [&](char mode, int minB, float* timedMs, bool prepareOnly) -> bool
         {
         const bool stageOn = mode != '0';
         const bool stageSide[2] = {mode != 'd', mode != 's'};
@@ -446,6 +451,7 @@ namespace lamjit
         auto put = [&](uint64_t x) { key.append(reinterpret_cast<const char*>(&x), sizeof x); };
         put(G);
         put(static_cast<uint64_t>(static_cast<unsigned char>(mode)));
+        put(static_cast<uint64_t>(minB));
         put(lazySrc);
         put(slab[0]);
         put(slab[1]);
@@ -523,7 +529,7 @@ namespace lamjit
              "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
           << "__device__ __forceinline__ void stg(unsigned long long a, uint4 v) { asm volatile(\"st.global.cs.v4.u32 [%0], "
              "{%1,%2,%3,%4};\" :: \"l\"(a), \"r\"(v.x), \"r\"(v.y), \"r\"(v.z), \"r\"(v.w) : \"memory\"); }\n"
-          << "extern \"C\" __global__ void __launch_bounds__(128) lamjit_copy(const LJP P) {\n"
+          << "extern \"C\" __global__ void __launch_bounds__(128" << (minB ? ", " + std::to_string(minB) : std::string()) << ") lamjit_copy(const LJP P) {\n"
           << " extern __shared__ uint4 lj_sm[];\n"
           << " const unsigned lane = threadIdx.x & 31u;\n"
           << " uint4* ss = lj_sm + (threadIdx.x >> 5) * " << (slab[0] + slab[1]) << "u;\n"
@@ -833,6 +839,8 @@ namespace lamjit
         }
         if(!kern)
             return false;
+        if(prepareOnly)
+            return true;
         // warps per CTA: 4 while the slabs fit 100 KB per CTA
         const char* envCta = std::getenv("LAMB_JIT_CTA_KB");
         const uint32_t ctaBytes = (envCta ? static_cast<uint32_t>(std::atoi(envCta)) : 100) * 1024;
@@ -889,7 +897,7 @@ namespace lamjit
         };
 
         if(!autoMode)
-            return attempt(forcedMode, nullptr);
+            return attempt(forcedMode, forcedMinB, nullptr, false);
         // Staging mode: the heuristic above, or -- the first time a pair is copied at >= 2^22
         // elements outside stream capture -- the fastest of the four modes, each timed on the copy
         // itself (every mode writes the same bytes, so the last timed launch leaves the finished
@@ -912,7 +920,7 @@ namespace lamjit
             pairKey.append(reinterpret_cast<const char*>(srcOfDst.data()), srcOfDst.size() * sizeof(uint32_t));
             pairKey.append(reinterpret_cast<const char*>(boolMask.data()), boolMask.size() * sizeof(uint32_t));
         }
-        char chosen = heuristic;
+        std::pair<char, int> chosen{heuristic, forcedMinB};
         bool decided = false;
         {
             std::lock_guard<std::mutex> lk(g_mu);
@@ -928,25 +936,45 @@ namespace lamjit
         cudaStreamIsCapturing(s, &cap);
         if(!decided && !(tune && tune[0] == '0') && groups * G >= (uint64_t{1} << 22) && cap == cudaStreamCaptureStatusNone)
         {
-            float best = 0;
-            char bestMode = 0;
+            // candidates: 4 staging modes x (no register cap, 3 CTAs per SM); compiled in parallel
+            std::vector<std::pair<char, int>> cand;
             for(char m : {'d', 's', '1', '0'})
+                for(int mb : {0, 3})
+                    cand.emplace_back(m, mb);
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::vector<char> ready(cand.size(), 0);
+            {
+                std::vector<std::thread> th;
+                for(size_t c = 0; c < cand.size(); ++c)
+                    th.emplace_back(
+                        [&, c]
+                        {
+                            cudaSetDevice(dev);
+                            ready[c] = attempt(cand[c].first, cand[c].second, nullptr, true) ? 1 : 0;
+                        });
+                for(auto& t : th)
+                    t.join();
+            }
+            float best = 0;
+            int bestC = -1;
+            for(size_t c = 0; c < cand.size(); ++c)
             {
                 float ms = 0;
-                if(!attempt(m, nullptr)) // warm: module load, first-touch
+                if(!ready[c] || !attempt(cand[c].first, cand[c].second, nullptr, false)) // warm: module load
                     continue;
-                if(attempt(m, &ms) && (bestMode == 0 || ms < best))
+                if(attempt(cand[c].first, cand[c].second, &ms, false) && (bestC < 0 || ms < best))
                 {
                     best = ms;
-                    bestMode = m;
+                    bestC = static_cast<int>(c);
                 }
             }
-            if(bestMode == 0)
+            if(bestC < 0)
                 return false;
             std::lock_guard<std::mutex> lk(g_mu);
-            g_modeCache[pairKey] = bestMode;
+            g_modeCache[pairKey] = cand[bestC];
             return true;
         }
-        return attempt(chosen, nullptr);
+        return attempt(chosen.first, chosen.second, nullptr, false);
     }
 } // namespace lamjit
