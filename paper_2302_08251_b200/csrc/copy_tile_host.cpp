@@ -34,6 +34,7 @@ namespace lamk
         unsigned long long groups;
         unsigned long long facSrc, facDst;
         uint32_t nl, facS, facD;
+        uint32_t sstage; // AoS source loaded warp-coalesced through the smem slice (k_vec_transpose)
     };
     bool vec_transpose(const VecParams& p, uint32_t leafSize, cudaStream_t s);
     bool vec_convert(const VecParams& p, uint32_t ss, uint32_t ds, cudaStream_t s);
@@ -614,6 +615,7 @@ namespace lamhost
         vp.facDst = p.facDst;
         if(vp.groups == 0)
             return false;
+        vp.sstage = vp.s.recordContig == 1 && envNum("LAMB_VEC_SSTAGE", 1) != 0;
         if(!lamk::vec_transpose(vp, p.usize, s))
             return false;
         addAccessCounts(p, S, vp.groups * V, s);

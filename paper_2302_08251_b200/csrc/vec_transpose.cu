@@ -32,6 +32,7 @@ namespace lamk
         unsigned long long groups; // groups of V elements
         unsigned long long facSrc, facDst;
         uint32_t nl, facS, facD;
+        uint32_t sstage; // AoS source loaded warp-coalesced through the smem slice (k_vec_transpose)
     };
 
     template<int V>
@@ -43,8 +44,8 @@ namespace lamk
         return (e0 >> sd.lshift) * sd.bs + (e0 & (sd.lanes - 1)) * (16 / V);
     }
 
-    template<int NL, int V>
-    __global__ void __launch_bounds__(256, 4) k_vec_transpose(const __grid_constant__ VecParams p)
+    template<int NL, int V, int MINB = 4>
+    __global__ void __launch_bounds__(256, MINB) k_vec_transpose(const __grid_constant__ VecParams p)
     {
         constexpr int S = 16 / V; // leaf size in bytes
         using W = typename std::conditional<S == 4, uint32_t, unsigned long long>::type;
@@ -58,11 +59,36 @@ namespace lamk
             // ---- load ----
             if(p.s.recordContig)
             {
-                const uint4* base = reinterpret_cast<const uint4*>(p.s.recBase + e0 * (NL * S));
                 uint4 x[NL];
+                // the warp's 32 groups are one contiguous span of 32*NL vectors: on full warps it
+                // is loaded with 512-byte coalesced loads into the warp's smem slice, and each lane
+                // then reads its NL vectors (lane stride NL*16 B, conflict-free for odd NL)
+                const uint32_t lane = threadIdx.x & 31;
+                const bool fullWarp = p.sstage && __activemask() == 0xFFFFFFFFu && (g - lane) + 32 <= p.groups;
+                if(fullWarp)
+                {
+                    uint4* slice = reinterpret_cast<uint4*>(vsm) + (threadIdx.x >> 5) * (32 * NL);
+                    const uint4* wbase = reinterpret_cast<const uint4*>(p.s.recBase + (e0 - uint64_t(lane) * V) * (NL * S));
+                    uint4 t[NL];
 #pragma unroll
-                for(int k = 0; k < NL; ++k)
-                    x[k] = __ldcs(base + k);
+                    for(int k = 0; k < NL; ++k)
+                        t[k] = __ldcs(wbase + k * 32 + lane);
+#pragma unroll
+                    for(int k = 0; k < NL; ++k)
+                        slice[k * 32 + lane] = t[k];
+                    __syncwarp();
+#pragma unroll
+                    for(int k = 0; k < NL; ++k)
+                        x[k] = slice[lane * NL + k];
+                    __syncwarp(); // the slice may be reused for the destination below
+                }
+                else
+                {
+                    const uint4* base = reinterpret_cast<const uint4*>(p.s.recBase + e0 * (NL * S));
+#pragma unroll
+                    for(int k = 0; k < NL; ++k)
+                        x[k] = __ldcs(base + k);
+                }
 #pragma unroll
                 for(int k = 0; k < NL; ++k)
                 {
@@ -180,7 +206,14 @@ namespace lamk
     template<int NL, int V>
     static void launch_vec(const VecParams& p, unsigned grid, cudaStream_t s)
     {
-        const size_t smem = p.d.recordContig ? 8 * 32 * NL * 16 : 0; // 8 warps x one staged span
+        const size_t smem = (p.d.recordContig || p.sstage) ? 8 * 32 * NL * 16 : 0; // 8 warps x one staged span
+        static const int minb = std::getenv("LAMB_VEC_MINB") ? std::atoi(std::getenv("LAMB_VEC_MINB")) : 3;
+        if constexpr(V == 4 && NL >= 7)
+            if(minb == 3)
+            {
+                k_vec_transpose<NL, V, 3><<<grid, 256, smem, s>>>(p);
+                return;
+            }
         k_vec_transpose<NL, V><<<grid, 256, smem, s>>>(p);
     }
 
