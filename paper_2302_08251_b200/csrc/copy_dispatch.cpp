@@ -209,8 +209,16 @@ namespace lamhost
         static const bool forceTile = std::getenv("LAMB_FORCE_TILE") && std::getenv("LAMB_FORCE_TILE")[0] == '1';
         if(full && sameLayout(a, b) && !forceTile)
         {
+            std::vector<void*> dv(a.blobCount());
+            std::vector<const void*> sv(a.blobCount());
+            std::vector<uint64_t> bv(a.blobCount());
             for(size_t nr = 0; nr < a.blobCount(); ++nr)
-                lam_cuda_check(lamk::blob_copy(dst.blobs[nr], src.blobs[nr], a.blobSize(nr), s), "blob_copy");
+            {
+                dv[nr] = dst.blobs[nr];
+                sv[nr] = src.blobs[nr];
+                bv[nr] = a.blobSize(nr);
+            }
+            lam_cuda_check(lamk::blob_copy_multi(dv.data(), sv.data(), bv.data(), dv.size(), s), "blob_copy");
             return;
         }
         // LAMB_FORCE_GENERIC=1 (tests only): cross-check the specialised kernels against the

@@ -163,6 +163,36 @@ namespace lamk
             __stcs(d + i, __ldcs(s + i));
     }
 
+    // several blobs in one launch (blockIdx.y = blob): the same-layout copy of a multi-blob
+    // mapping (SoA multi-blob: 7 blobs) without a launch gap and a tail per blob
+    struct BlobSegs
+    {
+        uint4* d[16];
+        const uint4* s[16];
+        uint64_t n16[16];
+    };
+    template<int U>
+    __global__ void __launch_bounds__(256) k_blob_copy16_multi(const __grid_constant__ BlobSegs p)
+    {
+        uint4* __restrict__ d = p.d[blockIdx.y];
+        const uint4* __restrict__ s = p.s[blockIdx.y];
+        const uint64_t n16 = p.n16[blockIdx.y];
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        for(; i + (U - 1) * stride < n16; i += U * stride)
+        {
+            uint4 x[U];
+#pragma unroll
+            for(int k = 0; k < U; ++k)
+                x[k] = __ldcs(s + i + k * stride);
+#pragma unroll
+            for(int k = 0; k < U; ++k)
+                __stcs(d + i + k * stride, x[k]);
+        }
+        for(; i < n16; i += stride)
+            __stcs(d + i, __ldcs(s + i));
+    }
+
     __global__ void k_blob_copy1(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, uint64_t n)
     {
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -570,6 +600,48 @@ namespace lamk
                                               rest);
             count_launch();
         }
+        return cudaGetLastError();
+    }
+
+    cudaError_t blob_copy_multi(void* const* dst, const void* const* src, const uint64_t* bytes, size_t n, cudaStream_t s)
+    {
+        // 16-byte aligned, whole-vector blobs go through k_blob_copy16_multi, 16 per launch;
+        // anything else through blob_copy
+        BlobSegs g{};
+        uint32_t cnt = 0;
+        uint64_t maxN = 0;
+        auto flush = [&]
+        {
+            if(cnt == 0)
+                return;
+            const unsigned grid = stream_grid((maxN + 256 * 2 - 1) / (256 * 2), "LAMB_BLOB_CTAS", 0);
+            k_blob_copy16_multi<2><<<dim3(grid, cnt), 256, 0, s>>>(g);
+            count_launch();
+            g = BlobSegs{};
+            cnt = 0;
+            maxN = 0;
+        };
+        for(size_t k = 0; k < n; ++k)
+        {
+            if(bytes[k] == 0)
+                continue;
+            const bool whole = ((reinterpret_cast<uintptr_t>(dst[k]) | reinterpret_cast<uintptr_t>(src[k])) & 15) == 0
+                && bytes[k] % 16 == 0;
+            if(!whole)
+            {
+                const cudaError_t e = blob_copy(dst[k], src[k], bytes[k], s);
+                if(e != cudaSuccess)
+                    return e;
+                continue;
+            }
+            g.d[cnt] = static_cast<uint4*>(dst[k]);
+            g.s[cnt] = static_cast<const uint4*>(src[k]);
+            g.n16[cnt] = bytes[k] / 16;
+            maxN = g.n16[cnt] > maxN ? g.n16[cnt] : maxN;
+            if(++cnt == 16)
+                flush();
+        }
+        flush();
         return cudaGetLastError();
     }
 

@@ -616,6 +616,20 @@ namespace lamhost
         if(vp.groups == 0)
             return false;
         vp.sstage = vp.s.recordContig == 1 && envNum("LAMB_VEC_SSTAGE", 1) != 0;
+        if(!vp.s.recordContig && vp.s.lanes > 1 && (32 * V) % vp.s.lanes == 0 && vp.s.bs == nl * vp.s.lanes * p.usize
+           && envNum("LAMB_VEC_SSTAGE", 1) != 0)
+        {
+            // AoSoA<L> source, leaves in order, no padding: the warp's span is contiguous
+            bool inOrder = true;
+            const unsigned long long b0 = vp.s.leafBase[0];
+            for(uint32_t f = 0; f < nl && inOrder; ++f)
+                inOrder = vp.s.leafBase[f] == b0 + uint64_t(f) * vp.s.lanes * p.usize;
+            if(inOrder && b0 % 16 == 0)
+            {
+                vp.s.recBase = b0;
+                vp.sstage = 2;
+            }
+        }
         if(!lamk::vec_transpose(vp, p.usize, s))
             return false;
         addAccessCounts(p, S, vp.groups * V, s);

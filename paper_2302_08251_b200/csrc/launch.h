@@ -113,6 +113,7 @@ namespace lamk
     cudaError_t heat_account(const lamp_view* v, uint64_t begin, uint64_t end, uint32_t nleaves, cudaStream_t s);
     // byte-exact blob copy (copyView's sameLayout memcpy path)
     cudaError_t blob_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
+    cudaError_t blob_copy_multi(void* const* dst, const void* const* src, const uint64_t* bytes, size_t n, cudaStream_t s);
     cudaError_t read_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, uint64_t* out, size_t n,
                             cudaStream_t s);
     cudaError_t write_values(const lamp_view* v, const uint64_t* lin, const uint32_t* leaf, const uint64_t* in,

@@ -105,11 +105,41 @@ namespace lamk
             }
             else
             {
-                const uint64_t off = leaf_off<V>(p.s, e0);
                 uint4 x[NL];
+                // AoSoA<L> source without padding, L | 32V (sstage 2): the warp's 32V elements are
+                // 32V/L whole blocks, one contiguous span of 32*NL vectors: loaded coalesced into the
+                // slice, then lane t reads leaf f of its elements at vector
+                // (tV / L) * bs/16 + f * L*S/16 + (tV % L) * S/16 (conflict-free for L | 32V)
+                const uint32_t lane = threadIdx.x & 31;
+                const bool fullWarp = p.sstage == 2 && __activemask() == 0xFFFFFFFFu && (g - lane) + 32 <= p.groups;
+                if(fullWarp)
+                {
+                    uint4* slice = reinterpret_cast<uint4*>(vsm) + (threadIdx.x >> 5) * (32 * NL);
+                    const uint64_t ew = e0 - uint64_t(lane) * V;
+                    const uint4* wbase = reinterpret_cast<const uint4*>(p.s.recBase + (ew >> p.s.lshift) * p.s.bs);
+                    uint4 t[NL];
 #pragma unroll
-                for(int f = 0; f < NL; ++f)
-                    x[f] = __ldcs(reinterpret_cast<const uint4*>(p.s.leafBase[f] + off));
+                    for(int k = 0; k < NL; ++k)
+                        t[k] = __ldcs(wbase + k * 32 + lane);
+#pragma unroll
+                    for(int k = 0; k < NL; ++k)
+                        slice[k * 32 + lane] = t[k];
+                    __syncwarp();
+                    const uint32_t el = lane * V;
+                    const uint32_t vi = (el >> p.s.lshift) * (p.s.bs >> 4) + (((el & (p.s.lanes - 1)) * S) >> 4);
+                    const uint32_t fstep = (p.s.lanes * S) >> 4;
+#pragma unroll
+                    for(int f = 0; f < NL; ++f)
+                        x[f] = slice[vi + f * fstep];
+                    __syncwarp(); // the slice may be reused for the destination below
+                }
+                else
+                {
+                    const uint64_t off = leaf_off<V>(p.s, e0);
+#pragma unroll
+                    for(int f = 0; f < NL; ++f)
+                        x[f] = __ldcs(reinterpret_cast<const uint4*>(p.s.leafBase[f] + off));
+                }
 #pragma unroll
                 for(int f = 0; f < NL; ++f)
                 {
