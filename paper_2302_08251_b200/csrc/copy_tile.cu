@@ -951,8 +951,8 @@ namespace lamk
         extern __shared__ __align__(16) uint8_t wsm[];
         // chunk -> stream table (host-built, shared by the CTA's warps)
         __shared__ __align__(16) uint8_t cst[1024];
-        __shared__ uint16_t s_pad[LAMT_MAX_STREAMS];
-        __shared__ unsigned long long s_base[8][LAMT_MAX_STREAMS];
+        __shared__ uint16_t s_pad[LAMT_WT_MAX_STREAMS];
+        __shared__ unsigned long long s_base[8][LAMT_WT_MAX_STREAMS];
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t warp = threadIdx.x >> 5;
         const uint32_t ns = p.nsrc, nd = p.ndst;

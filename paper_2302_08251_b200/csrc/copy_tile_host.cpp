@@ -401,6 +401,8 @@ namespace lamhost
     static bool tryWarpTile(const lamt_params& p, const Lowered& S, const Lowered& D, const DeviceImage& si,
                             DeviceImage& di, uint64_t begin, uint64_t end, cudaStream_t s)
     {
+        if(p.nsrc + p.ndst > LAMT_WT_MAX_STREAMS)
+            return false;
         const uint64_t unit = lcm64(lcm64(S.shardUnit, D.shardUnit), 32);
         double bpe = 0;
         for(uint32_t k = 0; k < p.nsrc + p.ndst; ++k)

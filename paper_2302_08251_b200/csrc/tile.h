@@ -13,7 +13,8 @@
 #include <stdint.h>
 
 #define LAMT_MAX_LEAVES 32
-#define LAMT_MAX_STREAMS 64
+#define LAMT_MAX_STREAMS 128   // plan streams (byte planes of wide records: 2 x 42 planes)
+#define LAMT_WT_MAX_STREAMS 64 // streams the warp-tile engine (k_warp_tile) takes
 #define LAMT_MAX_TERMS 8
 
 #define LAMT_K_PHYS 0

@@ -113,6 +113,8 @@ BOOLREC = "Record{a:bool,b:u8,c:bool,d:f32,e:bool}"
     (BOOLREC, "aos-packed", "soa-mb"), (BOOLREC, "soa-mb", "aos-aligned"), (BOOLREC, "aosoa:16", "aos-packed"),
     (MIXED, "aos-packed", "soa-mb"), (MIXED, "soa-mb", "aos-packed"), (MIXED, "aosoa:8", "aos-packed"),
     (MIXED, "aos-packed", "bytesplit:soa-mb"), (BOOLREC, "bytesplit:soa-mb", "aos-aligned"),
+    # more than 64 plan streams (42 byte planes per side)
+    (MIXED, "bytesplit:soa-mb", "bytesplit:soa-mb"), (MIXED, "bytesplit:soa-mb", "bytesplit:aosoa:16"),
 ])
 def test_jit_bool_bytes_canonicalise(schema, a, b, tmp_path, monkeypatch):
     """Source blobs of random bytes (bool bytes 0x02..0xFF included): the generated kernel writes

@@ -1,0 +1,3 @@
+O=gpurun_out/r2bx
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_jit.py tests/test_gpu_copy.py tests/test_gpu_guard.py -q -x > $O/tests.log 2>&1
