@@ -111,9 +111,23 @@ namespace lamhost
         if(!sb && !db)
             return false;
         // bit streams on both sides (different widths or formats, or the same computed layout):
-        // unpack into the scratch, pack from it
+        // k_repack32 when every leaf is one field of <= 32 bits (f32 formats E <= 8, M <= 23),
+        // else unpack into the scratch and pack from it
         if(sb && db)
-            return true;
+        {
+            const char* rp = std::getenv("LAMB_REPACK");
+            if(rp && rp[0] == '0')
+                return true;
+            for(const Lowered* L : {&S, &D})
+                for(uint16_t r : L->roots)
+                {
+                    const lamp_node& nd = L->nodes[r];
+                    const bool fltOk = rp && rp[0] == '2' && nd.kind == LAMP_BITS_FLT && nd.a >= 1 && nd.a <= 8 && nd.b <= 23;
+                    if(nd.kind == LAMP_BITS_INT ? nd.a > 32 : !fltOk)
+                        return true;
+                }
+            return false;
+        }
         const Lowered& phys = sb ? D : S; // the non-packed side
         for(uint16_t r : phys.roots)
             if(phys.nodes[r].kind != LAMP_PHYS)

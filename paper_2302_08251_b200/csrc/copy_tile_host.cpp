@@ -916,6 +916,62 @@ namespace lamhost
         return lamk::rec_pack(q, kind, packDir, s);
     }
 
+    // bit stream -> bit stream for every leaf (4-byte leaf types, fields <= 32 bits, float formats
+    // E <= 8, M <= 23): k_repack32, one launch per leaf
+    static bool tryRepack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
+                          const Lowered& S, const Lowered& D, cudaStream_t s)
+    {
+        if(begin % 32 || envNum("LAMB_REPACK", 1) == 0)
+            return false;
+        const uint64_t groups = (end - begin) / 32;
+        if(groups == 0)
+            return false;
+        std::vector<lamk::RepackParams> jobs;
+        for(uint32_t f = 0; f < p.nleaves; ++f)
+        {
+            const lamt_leaf& L = p.leaf[f];
+            const bool sb = L.skind == LAMT_K_BITS_INT || L.skind == LAMT_K_BITS_FLT;
+            const bool db = L.dkind == LAMT_K_BITS_INT || L.dkind == LAMT_K_BITS_FLT;
+            if(!sb || !db || L.skind != L.dkind || L.stype != L.ltype || L.dtype != L.ltype || scalarSize(L.ltype) != 4)
+                return false;
+            const bool flt = L.skind == LAMT_K_BITS_FLT;
+            // minifloat -> minifloat measured faster staged through the SoA scratch, where both halves
+            // run the compile-time-format codecs (tools/repack_cmp.py); LAMB_REPACK=2 forces this path
+            if(flt && envNum("LAMB_REPACK", 1) != 2)
+                return false;
+            if(flt && (L.ltype != F32 || L.sE > 8 || L.sM > 23 || L.dE > 8 || L.dM > 23 || L.sE < 1 || L.dE < 1))
+                return false;
+            lamk::RepackParams j{};
+            j.kind = flt ? 1 : 0;
+            j.ws = flt ? 1u + L.sE + L.sM : L.sE;
+            j.wd = flt ? 1u + L.dE + L.dM : L.dE;
+            j.sE = flt ? L.sE : 8;
+            j.sM = flt ? L.sM : 23;
+            j.dE = flt ? L.dE : 8;
+            j.dM = flt ? L.dM : 23;
+            j.ssgn = L.ssigned;
+            const lamt_stream& ss = p.st[L.s[0].stream];
+            const lamt_stream& ds = p.st[L.d[0].stream];
+            if(j.ws < 1 || j.ws > 32 || j.wd < 1 || j.wd > 32 || ss.bs != j.ws || ds.bs != j.wd || ss.gptr % 4 || ds.gptr % 4)
+                return false;
+            j.src = ss.gptr;
+            j.dst = ds.gptr;
+            j.begin = begin;
+            j.groups = groups;
+            jobs.push_back(j);
+        }
+        for(const auto& j : jobs)
+            if(!lamk::repack32(j, s))
+                return false;
+        addAccessCounts(p, S, groups * 32, s);
+        const uint64_t doneEnd = begin + groups * 32;
+        if(doneEnd < end)
+            lam_cuda_check(lamk::generic_copy(si.hdr, di.hdr, doneEnd, end, static_cast<uint32_t>(S.roots.size()), S.fac,
+                                              D.fac, s, false),
+                           "generic_copy(tail)");
+        return true;
+    }
+
     // K3/K4: every leaf physical (SoA or AoSoA with 32 | L) <-> bit stream: 4-byte leaves with fields
     // <= 32 bits through k_pack32/k_unpack32, 1/2/8-byte leaves and wider fields through packv.cu
     static bool tryPack(const lamt_params& p, uint64_t begin, uint64_t end, const DeviceImage& si, DeviceImage& di,
@@ -1274,6 +1330,8 @@ namespace lamhost
         }
         if(p.uni && envNum("LAMB_VEC", 1) != 0 && tryVec(p, begin, end, si, di, S, D, s))
             return trace("vec"), true;
+        if(!p.uni && tryRepack(p, begin, end, si, di, S, D, s))
+            return trace("repack"), true;
         if(!p.uni && tryPack(p, begin, end, si, di, S, D, s))
             return trace("pack"), true;
         if(!p.uni && trySplit(p, begin, end, si, di, S, D, s))

@@ -59,6 +59,18 @@ namespace lamk
     };
     bool vec_multi(const VMParams& p, uint32_t leafSize, cudaStream_t s);
 
+    // bit stream -> bit stream, one leaf (pack.cu k_repack32)
+    struct RepackParams
+    {
+        unsigned long long src, dst;      // bit streams (word 0 = element 0)
+        unsigned long long begin, groups; // first element (multiple of 32), groups of 32
+        uint32_t ws, wd;                  // field widths 1..32
+        uint32_t kind;                    // 0 int, 1 float (E <= 8, M <= 23 on both sides)
+        uint32_t sE, sM, dE, dM;
+        uint32_t ssgn; // int: sign-extend the source field (signed leaf type)
+    };
+    bool repack32(const RepackParams& p, cudaStream_t s);
+
 
 
     int sm_count(int device);

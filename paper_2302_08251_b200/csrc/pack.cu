@@ -897,6 +897,103 @@ namespace lamk
         return hit;
     }
 
+    // ---- bit stream -> bit stream (different widths / formats, or the same computed layout) ----
+    // copyView reads each value from the source field (decode / sign-extend) and writes it to the
+    // destination field (encode / truncate); a thread owns 32 values = ws source words and wd
+    // destination words.  The warp's 32*ws source words and 32*wd destination words are
+    // contiguous: they move with coalesced accesses through lane rows of stride ws|1 / wd|1
+    // (conflict-free), so every bit crosses HBM once, without the SoA scratch round trip.
+    __global__ void __launch_bounds__(256) k_repack32(const __grid_constant__ RepackParams p)
+    {
+        extern __shared__ __align__(16) uint32_t rsm[];
+        const uint32_t ws = p.ws, wd = p.wd, wsp = ws | 1u, wdp = wd | 1u;
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t* srow = rsm + (threadIdx.x >> 5) * 32 * (wsp + wdp);
+        uint32_t* drow = srow + 32 * wsp;
+        const uint32_t smag = static_cast<uint32_t>(((1ull << 32) + ws - 1) / ws);
+        const uint32_t dmag = static_cast<uint32_t>(((1ull << 32) + wd - 1) / wd);
+        const uint32_t smask = ws >= 32 ? 0xFFFFFFFFu : ((1u << ws) - 1u);
+        const uint32_t dmask = wd >= 32 ? 0xFFFFFFFFu : ((1u << wd) - 1u);
+        const lamd::F32Codec cs = lamd::f32_codec(p.sE, p.sM), cd = lamd::f32_codec(p.dE, p.dM);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.src);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(p.dst);
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32; // whole warps iterate together
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const uint64_t warpG = g - lane;
+            const uint32_t live = static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint32_t* ws0 = src + (p.begin / 32 + warpG) * ws;
+            // t / ws by a multiply-high (exact for t < 1024, ws <= 32)
+            for(uint32_t t = lane; t < live * ws; t += 32)
+            {
+                const uint32_t r = __umulhi(t, smag);
+                srow[r * wsp + (t - r * ws)] = __ldcs(ws0 + t);
+            }
+            __syncwarp();
+            if(lane < live)
+            {
+                const uint32_t* my = srow + lane * wsp;
+                uint32_t* out = drow + lane * wdp;
+                unsigned long long acc = my[0], oacc = 0;
+                uint32_t nb = 32, k = 1, onb = 0, ok = 0;
+#pragma unroll 4
+                for(int i = 0; i < 32; ++i)
+                {
+                    if(nb < ws)
+                    {
+                        acc |= static_cast<unsigned long long>(my[k < ws ? k : ws - 1]) << nb;
+                        ++k;
+                        nb += 32;
+                    }
+                    uint32_t v = static_cast<uint32_t>(acc) & smask;
+                    acc >>= ws;
+                    nb -= ws;
+                    if(p.kind)
+                        v = lamd::f32_encode_bf(cd, lamd::f32_decode_bf(cs, v));
+                    else
+                    {
+                        if(p.ssgn && ws < 32)
+                        {
+                            const uint32_t sb = 1u << (ws - 1);
+                            v = (v ^ sb) - sb;
+                        }
+                        v &= dmask;
+                    }
+                    oacc |= static_cast<unsigned long long>(v) << onb;
+                    onb += wd;
+                    if(onb >= 32)
+                    {
+                        out[ok++] = static_cast<uint32_t>(oacc);
+                        oacc >>= 32;
+                        onb -= 32;
+                    }
+                }
+            }
+            __syncwarp();
+            uint32_t* wd0 = dst + (p.begin / 32 + warpG) * wd;
+            for(uint32_t t = lane; t < live * wd; t += 32)
+            {
+                const uint32_t r = __umulhi(t, dmag);
+                __stcs(wd0 + t, drow[r * wdp + (t - r * wd)]);
+            }
+            __syncwarp();
+        }
+    }
+
+    bool repack32(const RepackParams& p, cudaStream_t s)
+    {
+        if(p.groups == 0 || p.ws < 1 || p.ws > 32 || p.wd < 1 || p.wd > 32)
+            return false;
+        const size_t smem = static_cast<size_t>(8) * 32 * ((p.ws | 1u) + (p.wd | 1u)) * sizeof(uint32_t);
+        lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_repack32), smem), "opt_in_smem");
+        const unsigned grid = stream_grid((p.groups + 255) / 256, "LAMB_PACK_CTAS", 32);
+        k_repack32<<<grid, 256, smem, s>>>(p);
+        count_launch();
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
+    }
+
     bool pack32(const PackParams& p, bool pack, cudaStream_t s)
     {
         if(p.groups == 0 || p.w < 1 || p.w > 32)

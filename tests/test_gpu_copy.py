@@ -460,3 +460,25 @@ def test_bitpack_float_record_side_formats(fmt, rec):
     pb = O.zero_blobs(packed)
     O.write_all(packed, pb, vals)
     run_pair(R32, n, f"bitpack-float:{fmt}", rec, O.read_all(packed, pb))
+
+
+@pytest.mark.parametrize("schema,a,b", [
+    ("Record{v:u32,w:i32}", "bitpack-int:11", "bitpack-int:7"),
+    ("Record{v:u32,w:i32}", "bitpack-int:5", "bitpack-int:29"),
+    ("Record{v:u32,w:i32}", "bitpack-int:13", "bitpack-int:13"),
+    (R32, "bitpack-float:4,3", "bitpack-float:5,10"),
+    (R32, "bitpack-float:8,10", "bitpack-float:4,3"),
+    (R32, "bitpack-float:5,2", "bitpack-float:5,2"),
+    (R32, "bitpack-float:6,9", "bitpack-float:8,23"),
+])
+@pytest.mark.parametrize("n", [1000, 70001])
+def test_bitpack_to_bitpack(schema, a, b, n):
+    """Bit stream -> bit stream in one pass (k_repack32): decode / sign-extend each source field,
+    encode / truncate into the destination field, tail bits untouched."""
+    rng = np.random.default_rng(n + len(a) + len(b))
+    types = [l.type for l in O.Schema.parse(schema).leaves]
+    vals = random_values(rng, types, n)
+    src = O.make(schema, f"i32:[{n}]", a)
+    sb = O.zero_blobs(src)
+    O.write_all(src, sb, vals)
+    run_pair(schema, n, a, b, O.read_all(src, sb))
