@@ -165,3 +165,28 @@ def test_jit_conversions_raw_bytes(schema, a, b, tmp_path, monkeypatch):
     L.copy_view(gs, gd)
     for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
         assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
+
+
+@pytest.mark.parametrize("a,b", [("aos-packed", "soa-mb"), ("soa-mb", "aos-aligned"), ("aosoa:8", "bytesplit:soa-mb")])
+def test_jit_host_pipeline(a, b, tmp_path, monkeypatch):
+    """lam_copy_host (host blobs chunked through the GPU, chunk views with shifted bases) on pairs
+    the generated kernels serve, with a FieldAccessCount destination."""
+    from paper_2302_08251_b200 import lamina as L
+    dump = str(tmp_path / "jit.cu")
+    monkeypatch.setenv("LAMB_JIT_DUMP", dump)
+    n = 3_000_017
+    ext = f"i32:[{n}]"
+    rng = np.random.default_rng(23)
+    types = [l.type for l in O.Schema.parse(MIX4).leaves]
+    vals = random_values(rng, types, n)
+    ms, md = O.make(MIX4, ext, a), O.make(MIX4, ext, b, wrap=1)
+    sb = O.zero_blobs(ms)
+    O.write_all(ms, sb, vals)
+    db = O.zero_blobs(md)
+    O.copy_view(ms, sb, md, db)
+    got = [np.zeros_like(x) for x in db]
+    _, dc = L.copy_view_host(L.Layout(MIX4, ext, a), sb, L.Layout(MIX4, ext, b, wrap=1), got)
+    for nr, (x, y) in enumerate(zip(got, db)):
+        assert np.array_equal(x, y), f"blob {nr}"
+    assert np.array_equal(dc, O.counters(md))
+    assert _dump_size(dump) > 0
