@@ -557,11 +557,17 @@ namespace lamjit
             a << "[" << l.rb << "u + lane * " << l.KP << "u + " << v << "u]";
             return a.str();
         };
-        auto coop = [&](const Span& sp, const Lay& l, size_t idx, bool load, const char* slabName, const char* fn)
+        // holeMask (destination preload): bit v set = vector v of a group has bytes copyView never
+        // writes; only those are read back (all of them when K > 64)
+        auto coop = [&](const Span& sp, const Lay& l, size_t idx, bool load, const char* slabName, const char* fn,
+                        uint64_t holeMask = ~0ull)
         {
             o << "  { const unsigned long long a = P.base[" << idx << "] + gw * " << sp.gstride << "ull;\n"
               << "#pragma unroll\n   for(unsigned j = 0; j < " << l.K << "u; ++j) { const unsigned i = lane + 32u * j; "
-              << "if(i < cnt * " << l.K << "u) ";
+              << "if(i < cnt * " << l.K << "u";
+            if(holeMask != ~0ull)
+                o << " && ((0x" << std::hex << holeMask << std::dec << "ull >> (i % " << l.K << "u)) & 1ull)";
+            o << ") ";
             if(load)
                 o << slabName << "[" << l.rb << "u + (i / " << l.K << "u) * " << l.KP << "u + i % " << l.K << "u] = " << fn
                   << "(a + 16ull * i); } }\n";
@@ -639,10 +645,16 @@ namespace lamjit
         for(size_t k = 0; k < sv[1].size(); ++k)
         {
             bool holes = false;
+            uint64_t mask = 0;
             for(uint32_t v = 0; v < lay[1][k].K; ++v)
-                holes |= holeVec[sv[1][k].word0 / 4 + v];
+            {
+                const bool h = holeVec[sv[1][k].word0 / 4 + v];
+                holes |= h;
+                if(h && v < 64)
+                    mask |= 1ull << v;
+            }
             if(lay[1][k].staged && holes)
-                coop(sv[1][k], lay[1][k], sv[0].size() + k, true, "sd", "ldo");
+                coop(sv[1][k], lay[1][k], sv[0].size() + k, true, "sd", "ldo", lay[1][k].K <= 64 ? mask : ~0ull);
         }
         o << "  __syncwarp();\n  if(act) {\n";
         if(lazySrc)
