@@ -10,6 +10,8 @@
 #include "device_common.cuh"
 #include "launch.h"
 
+#include <cstdlib>
+
 namespace lamk
 {
     struct PlaneParams
@@ -21,25 +23,60 @@ namespace lamk
     };
 
     template<int NL, int SB, bool CVT>
-    __global__ void __launch_bounds__(256) k_rec_to_planes(const __grid_constant__ PlaneParams p)
+    __global__ void __launch_bounds__(256) k_rec_to_planes(const __grid_constant__ PlaneParams p, int stage)
     {
         constexpr int PB = CVT ? 4 : SB;          // plane bytes per leaf
         constexpr int NV = NL * SB * 4 / 16;      // 16-byte vectors per 4 records
+        constexpr int NVP = NV | 1;               // lane row stride in the slice (conflict-free)
         using PV = typename std::conditional<PB == 8, unsigned long long, uint32_t>::type;
+        extern __shared__ __align__(16) uint4 rsl[];
+        const uint32_t lane = threadIdx.x & 31;
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < p.groups; g += stride)
         {
             const uint64_t e0 = p.begin + g * 4;
-            const uint4* src = reinterpret_cast<const uint4*>(p.rec + e0 * (NL * SB));
             uint32_t w[NV * 4];
-#pragma unroll
-            for(int q = 0; q < NV; ++q)
+            // full warps: the warp's 32 x 4 records are one contiguous span of 32*NV vectors,
+            // loaded with 512-byte coalesced loads into the warp's slice, then read back per lane
+            const bool fullWarp = stage && __activemask() == 0xFFFFFFFFu && (g - lane) + 32 <= p.groups;
+            if(fullWarp)
             {
-                const uint4 x = __ldcs(src + q);
-                w[4 * q] = x.x;
-                w[4 * q + 1] = x.y;
-                w[4 * q + 2] = x.z;
-                w[4 * q + 3] = x.w;
+                uint4* slice = rsl + (threadIdx.x >> 5) * (32 * NVP);
+                const uint4* wsrc = reinterpret_cast<const uint4*>(p.rec + (e0 - uint64_t(lane) * 4) * (NL * SB));
+                uint4 t[NV];
+#pragma unroll
+                for(int q = 0; q < NV; ++q)
+                    t[q] = __ldcs(wsrc + q * 32 + lane);
+#pragma unroll
+                for(int q = 0; q < NV; ++q)
+                {
+                    const uint32_t i = q * 32 + lane;
+                    slice[(i / NV) * NVP + i % NV] = t[q];
+                }
+                __syncwarp();
+#pragma unroll
+                for(int q = 0; q < NV; ++q)
+                {
+                    const uint4 x = slice[lane * NVP + q];
+                    w[4 * q] = x.x;
+                    w[4 * q + 1] = x.y;
+                    w[4 * q + 2] = x.z;
+                    w[4 * q + 3] = x.w;
+                }
+                __syncwarp();
+            }
+            else
+            {
+                const uint4* src = reinterpret_cast<const uint4*>(p.rec + e0 * (NL * SB));
+#pragma unroll
+                for(int q = 0; q < NV; ++q)
+                {
+                    const uint4 x = __ldcs(src + q);
+                    w[4 * q] = x.x;
+                    w[4 * q + 1] = x.y;
+                    w[4 * q + 2] = x.z;
+                    w[4 * q + 3] = x.w;
+                }
             }
             PV v[4][NL]; // value of leaf f of element q
 #pragma unroll
@@ -136,7 +173,14 @@ namespace lamk
     {
         constexpr int NV = NL * SB * 4 / 16;
         if(toPlanes)
-            k_rec_to_planes<NL, SB, CVT><<<stream_grid((p.groups + 255) / 256, "LAMB_PLANES_CTAS", 0), 256, 0, s>>>(p);
+        {
+            // LAMB_PLANES_SSTAGE=0: per-thread record loads (no slice)
+            static const int stage = std::getenv("LAMB_PLANES_SSTAGE") ? std::atoi(std::getenv("LAMB_PLANES_SSTAGE")) : 1;
+            const size_t smem = stage ? 8 * 32 * (NV | 1) * sizeof(uint4) : 0;
+            if(stage)
+                lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_rec_to_planes<NL, SB, CVT>), smem), "opt_in_smem");
+            k_rec_to_planes<NL, SB, CVT><<<stream_grid((p.groups + 255) / 256, "LAMB_PLANES_CTAS", 0), 256, smem, s>>>(p, stage);
+        }
         else
         {
             const size_t smem = 8 * 32 * NV * sizeof(uint4);
