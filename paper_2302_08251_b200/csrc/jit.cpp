@@ -1,25 +1,40 @@
-// Run-time specialised copy kernels for physical layout pairs (NVRTC).
+// Run-time specialised copy kernels for layout pairs (NVRTC).
 //
-// The reference's mappings are run-time objects (mapping.hpp:44-155); LLAMA, the library the
-// paper describes, resolves them at compile time.  For the physical pairs the fixed kernels do
-// not cover -- records with mixed leaf sizes and unaligned packed leaves, AoSoA lane counts no
-// vector group fits, padded destinations -- this path does what LLAMA's compile-time mappings
-// do: it generates a kernel for the exact pair of lowered layouts, with every block stride,
-// lane count and leaf offset a literal, compiles it with NVRTC for sm_100a (once per pair,
-// cached) and launches it.
+// The reference's mappings are run-time objects (mapping.hpp:44-155). LLAMA, the library the
+// paper describes, resolves them at compile time. For the pairs the fixed kernels do not cover,
+// this path does what LLAMA's compile-time mappings do. Those pairs are records with mixed leaf
+// sizes, padded destinations, byte planes against anything but a packed record, ChangeType
+// leaves, and AoSoA lane counts no vector group fits. The path generates a kernel for the exact
+// pair of lowered layouts, with every block stride, lane count and leaf offset a literal. It
+// compiles the kernel with NVRTC for sm_100a, once per pair and cached, and launches it.
 //
-// The generated kernel: a thread owns G consecutive elements, chosen so that for every stream
-// of both sides the bytes of those elements are whole 16-byte vectors (G/L whole blocks of a
-// record / AoSoA<L> stream, or one run of G values of a leaf inside an AoSoA<L> block).  It
-// loads every source vector (ld.global.cs.v4), assembles every destination word with PRMT byte
-// permutes whose selectors are compile-time constants, and stores every destination vector
-// (st.global.cs.v4).  Destination bytes copyView never writes (padding) come from the
-// destination's own old words, loaded first.  The semantics are copyView's fieldwise loop
-// (view.cpp:184-188) on physical leaves: a byte permutation of the leaf bytes.  Bool leaves
-// (canonicalised on read) and conversions stay with the general engines.
+// The generated kernel:
+// - A thread owns G consecutive elements. G is chosen so that, for every stream of both sides,
+//   the bytes of those elements are whole 16-byte vectors: G/L whole blocks of a record or
+//   AoSoA<L> stream ("block span"), or one run of G values of a leaf inside an AoSoA<L> block
+//   ("run span"). A side is physical leaves or byte planes (Bytesplit term k = byte k).
+// - Every destination word is assembled from source words by PRMT byte permutes with
+//   compile-time selectors. Bool bytes are canonicalised (__vcmpne4).
+// - ChangeType leaves (f32 <-> f64, integer widen / narrow) are converted in registers with the
+//   reference's rules (scalar.hpp:295-319).
+// - Destination bytes copyView never writes (padding) come from the destination's own words,
+//   read first.
+// - A destination span that is byte for byte a source span is a warp-coalesced pass-through copy.
+// - Block spans of more than one vector per thread can move through warp-private shared-memory
+//   slabs (coalesced 16-byte accesses, odd lane stride).
+// - The staging mode (destination slabs, source slabs, both, none) and a register cap are
+//   autotuned on the first copy of a pair at >= 2^22 elements: eight variants, compiled in
+//   parallel and timed on the copy itself. Smaller copies use a heuristic.
+// The semantics are copyView's fieldwise loop (view.cpp:184-188).
 //
-// NVRTC is loaded with dlopen; when it is absent or a compile fails the pair falls back to the
+// NVRTC is loaded with dlopen. When it is absent or a compile fails, the pair falls back to the
 // warp-tile engine (never to the CPU).
+//
+// Knobs:
+// - LAMB_JIT=0 disables this path.
+// - LAMB_JIT_STAGE=1|s|d|0 forces a staging mode, and LAMB_JIT_MINB a register cap.
+// - LAMB_JIT_TUNE=0 turns autotuning off.
+// - LAMB_JIT_DUMP=file appends the generated sources to that file; LAMB_JIT_LOG=1 prints compile errors.
 #include "capi_internal.hpp"
 #include "launch.h"
 #include "tile.h"
