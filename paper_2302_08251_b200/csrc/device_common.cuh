@@ -51,9 +51,10 @@ namespace lamd
     // ---- conversions (ScalarValue::convertTo) -----------------------------------------
     LAM_DEV uint64_t f32_to_f64_bits(uint32_t b)
     {
-        if((b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu) != 0u)
-            return (uint64_t(b >> 31) << 63) | 0x7FF8000000000000ull | (uint64_t(b & 0x007FFFFFu) << 29);
-        return static_cast<uint64_t>(__double_as_longlong(static_cast<double>(__uint_as_float(b))));
+        // branch-free: the NaN pattern (quiet bit set, payload kept) is selected, not branched to
+        const uint64_t nan = (uint64_t(b >> 31) << 63) | 0x7FF8000000000000ull | (uint64_t(b & 0x007FFFFFu) << 29);
+        const uint64_t cvt = static_cast<uint64_t>(__double_as_longlong(static_cast<double>(__uint_as_float(b))));
+        return (b & 0x7FFFFFFFu) > 0x7F800000u ? nan : cvt;
     }
     LAM_DEV uint32_t f64_to_f32_bits(uint64_t b)
     {
