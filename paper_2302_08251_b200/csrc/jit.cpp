@@ -158,8 +158,9 @@ namespace lamjit
         unsigned long long base = 0; // run: leaf-run base (stream + inblock); block: stream + (begin/L)*bs
         uint64_t gstride = 0;        // block: bytes per group
         uint32_t lsh = 0, bs = 0, lmask = 0, ls = 0; // run: base + (e0 >> lsh)*bs + (e0 & lmask)*ls
-        uint32_t bytes = 0;          // multiple of 16
+        uint32_t bytes = 0;          // multiple of 16 (a half span occupies 16 in the word space)
         uint32_t word0 = 0;          // first word of the span in the side's word space
+        bool half = false;           // block span of 8 bytes per group (words 2, 3 are padding)
     };
 
     bool tryCopy(const lamt_params& p, uint64_t begin, uint64_t end, uint64_t* doneEnd, cudaStream_t s)
@@ -216,6 +217,8 @@ namespace lamjit
         std::vector<Span> sv[2];
         std::vector<int> spanOfStream[2];
         // leaf f, element j, byte b -> (span word index, byte) on each side
+        const char* envHalf = std::getenv("LAMB_JIT_HALF");
+        const bool halfOk = !(envHalf && envHalf[0] == '0');
         auto build = [&](uint32_t G, bool src, std::vector<Span>& spans, std::vector<int>& sos,
                          std::vector<uint32_t>& wordOf) -> bool
         {
@@ -244,7 +247,15 @@ namespace lamjit
                             sp.base = st.gptr + (begin / L) * st.bs;
                             sp.gstride = uint64_t(G / L) * st.bs;
                             sp.bytes = static_cast<uint32_t>(sp.gstride);
-                            if(sp.bytes % 16 || sp.base % 16 || sp.gstride % 16 || words + sp.bytes / 4 > 4096)
+                            if(sp.bytes == 8 && sp.base % 8 == 0 && halfOk)
+                            {
+                                // 8 bytes per group (a 1-byte SoA leaf at G = 8): one 8-byte access
+                                sp.half = true;
+                                sp.bytes = 16;
+                            }
+                            else if(sp.bytes % 16 || sp.base % 16 || sp.gstride % 16)
+                                return false;
+                            if(words + sp.bytes / 4 > 4096)
                                 return false;
                             sp.word0 = words;
                             words += sp.bytes / 4;
@@ -348,6 +359,12 @@ namespace lamjit
                 }
             }
         // destination vectors with holes are preloaded
+        // words 2, 3 of a half destination span are never stored: don't care, not holes
+        constexpr uint32_t kDontCare = 0xFFFFFFFEu;
+        for(const Span& sp : sv[1])
+            if(sp.half)
+                for(uint32_t b = 8; b < 16; ++b)
+                    srcOfDst[size_t(sp.word0) * 4 + b] = kDontCare;
         std::vector<bool> holeVec(dWords / 4, false);
         for(uint32_t w = 0; w < dWords; ++w)
             for(uint32_t b = 0; b < 4; ++b)
@@ -367,10 +384,11 @@ namespace lamjit
             for(size_t k = 0; k < sv[0].size(); ++k)
             {
                 const Span& sk = sv[0][k];
-                if(srcPassed[k] || sk.word0 != (s0 >> 2) || sk.bytes != dm.bytes)
+                if(srcPassed[k] || sk.word0 != (s0 >> 2) || sk.bytes != dm.bytes || sk.half != dm.half)
                     continue;
                 bool same = true;
-                for(uint32_t w = 0; w < dm.bytes / 4 && same; ++w)
+                // half spans: only their first 8 bytes are real (words 2, 3 don't care)
+                for(uint32_t w = 0; w < (dm.half ? 2u : dm.bytes / 4) && same; ++w)
                 {
                     same = boolMask[dm.word0 + w] == 0;
                     for(uint32_t b = 0; b < 4 && same; ++b)
@@ -477,7 +495,7 @@ namespace lamjit
             {
                 const Span& sp = sv[side][k];
                 const Lay& l = lay[side][k];
-                put(sp.run);
+                put(sp.run | (uint64_t(sp.half) << 1));
                 put(sp.gstride);
                 put((uint64_t(sp.lsh) << 32) | sp.bs);
                 put((uint64_t(sp.lmask) << 32) | sp.ls);
@@ -540,6 +558,12 @@ namespace lamjit
              "(e & mask) * ls + 16ull * v; }\n"
           << "__device__ __forceinline__ uint4 ldg(unsigned long long a) { uint4 v; asm volatile(\"ld.global.cs.v4.u32 "
              "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
+          << "__device__ __forceinline__ uint4 ldg8(unsigned long long a) { uint4 v; v.z = 0u; v.w = 0u; asm volatile(\"ld.global.cs.v2.u32 "
+             "{%0,%1}, [%2];\" : \"=r\"(v.x), \"=r\"(v.y) : \"l\"(a)); return v; }\n"
+          << "__device__ __forceinline__ uint4 ldo8(unsigned long long a) { uint4 v; v.z = 0u; v.w = 0u; asm volatile(\"ld.global.v2.u32 "
+             "{%0,%1}, [%2];\" : \"=r\"(v.x), \"=r\"(v.y) : \"l\"(a)); return v; }\n"
+          << "__device__ __forceinline__ void stg8(unsigned long long a, uint4 v) { asm volatile(\"st.global.cs.v2.u32 [%0], "
+             "{%1,%2};\" :: \"l\"(a), \"r\"(v.x), \"r\"(v.y) : \"memory\"); }\n"
           << "__device__ __forceinline__ uint4 ldo(unsigned long long a) { uint4 v; asm volatile(\"ld.global.v4.u32 "
              "{%0,%1,%2,%3}, [%4];\" : \"=r\"(v.x), \"=r\"(v.y), \"=r\"(v.z), \"=r\"(v.w) : \"l\"(a)); return v; }\n"
           << "__device__ __forceinline__ void stg(unsigned long long a, uint4 v) { asm volatile(\"st.global.cs.v4.u32 [%0], "
@@ -599,7 +623,7 @@ namespace lamjit
             {
                 std::ostringstream a;
                 if(!sp.run)
-                    a << "(pb" << idx << " + 16ull * " << i << ")";
+                    a << "(pb" << idx << " + " << (sp.half ? 8 : 16) << "ull * " << i << ")";
                 else
                     a << "lj_run(P.base[" << idx << "], P.begin + (gw + " << i << " / " << K << "u) * " << G << "ull, " << sp.lsh
                       << "u, " << sp.bs << "ull, " << sp.lmask << "ull, " << sp.ls << "ull, " << i << " % " << K << "u)";
@@ -630,15 +654,15 @@ namespace lamjit
                     const uint32_t j = pv[q].second, K = lay[1][m].K;
                     const std::string i = "i" + std::to_string(q - b0);
                     o << "   uint4 t" << q - b0 << "; const unsigned " << i << " = lane + " << 32 * j << "u; if(" << i << " < cnt * " << K
-                      << "u) t" << q - b0 << " = ldg(" << passAddr(sv[0][k], k, i, K) << ");\n";
+                      << "u) t" << q - b0 << " = " << (sv[0][k].half ? "ldg8" : "ldg") << "(" << passAddr(sv[0][k], k, i, K) << ");\n";
                 }
                 for(size_t q = b0; q < b1; ++q)
                 {
                     const size_t m = pv[q].first;
                     const uint32_t K = lay[1][m].K;
                     const std::string i = "i" + std::to_string(q - b0);
-                    o << "   if(" << i << " < cnt * " << K << "u) stg(" << passAddr(sv[1][m], sv[0].size() + m, i, K) << ", t" << q - b0
-                      << ");\n";
+                    o << "   if(" << i << " < cnt * " << K << "u) " << (sv[1][m].half ? "stg8" : "stg") << "("
+                      << passAddr(sv[1][m], sv[0].size() + m, i, K) << ", t" << q - b0 << ");\n";
                 }
                 o << "  }\n";
             }
@@ -651,7 +675,7 @@ namespace lamjit
                     o << "  uint4 S" << k << "_" << v << " = make_uint4(0u, 0u, 0u, 0u);\n";
                 o << "  if(act) { const unsigned long long a = " << addr(sv[0][k], k) << ";";
                 for(uint32_t v = 0; v < lay[0][k].K; ++v)
-                    o << " S" << k << "_" << v << " = ldg(a + " << 16 * v << "ull);";
+                    o << " S" << k << "_" << v << " = " << (sv[0][k].half ? "ldg8" : "ldg") << "(a + " << 16 * v << "ull);";
                 o << " }\n";
             }
         for(size_t k = 0; k < sv[0].size(); ++k)
@@ -790,7 +814,8 @@ namespace lamjit
             }
             else if(lazySrc && !emitted[w / 4])
             {
-                o << "   const uint4 S" << k << "_" << v << " = ldg(as" << k << " + " << 16 * v << "ull);\n";
+                o << "   const uint4 S" << k << "_" << v << " = " << (sv[0][k].half ? "ldg8" : "ldg") << "(as" << k << " + " << 16 * v
+                  << "ull);\n";
                 emitted[w / 4] = true;
             }
             static const char* comp = "xyzw";
@@ -815,7 +840,8 @@ namespace lamjit
                     if(l.staged)
                         o << "   const uint4 " << oldName << " = sd" << slot(l, v) << ";\n";
                     else
-                        o << "   const uint4 " << oldName << " = ldo(" << ad << " + " << 16 * v << "ull);\n";
+                        o << "   const uint4 " << oldName << " = " << (sp.half ? "ldo8" : "ldo") << "(" << ad << " + " << 16 * v
+                          << "ull);\n";
                 }
                 std::string dn[4];
                 for(uint32_t c = 0; c < 4; ++c)
@@ -826,7 +852,12 @@ namespace lamjit
                     for(uint32_t b = 0; b < 4; ++b)
                     {
                         const uint32_t sw = srcOfDst[size_t(w) * 4 + b];
-                        if(sw == 0xFFFFFFFFu)
+                        if(sw == kDontCare)
+                        {
+                            var[b] = "0u";
+                            byt[b] = 0;
+                        }
+                        else if(sw == 0xFFFFFFFFu)
                         {
                             var[b] = oldName + "." + "xyzw"[c];
                             byt[b] = b;
@@ -845,7 +876,7 @@ namespace lamjit
                 if(l.staged)
                     o << "   sd" << slot(l, v) << " = " << val << ";\n";
                 else
-                    o << "   stg(" << ad << " + " << 16 * v << "ull, " << val << ");\n";
+                    o << "   " << (sp.half ? "stg8" : "stg") << "(" << ad << " + " << 16 * v << "ull, " << val << ");\n";
             }
         }
         o << "  }\n  __syncwarp();\n";
@@ -936,7 +967,7 @@ namespace lamjit
             for(int side = 0; side < 2; ++side)
                 for(const Span& sp : sv[side])
                 {
-                    put(sp.run);
+                    put(sp.run | (uint64_t(sp.half) << 1));
                     put(sp.gstride);
                     put((uint64_t(sp.lsh) << 32) | sp.bs);
                     put((uint64_t(sp.lmask) << 32) | sp.ls);
