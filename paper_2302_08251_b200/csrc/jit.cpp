@@ -12,7 +12,9 @@
 // - A thread owns G consecutive elements. G is chosen so that, for every stream of both sides,
 //   the bytes of those elements are whole 16-byte vectors: G/L whole blocks of a record or
 //   AoSoA<L> stream ("block span"), or one run of G values of a leaf inside an AoSoA<L> block
-//   ("run span"). A side is physical leaves or byte planes (Bytesplit term k = byte k).
+//   ("run span"). A block span of exactly 8 bytes per group (a 1-byte SoA leaf or byte plane at
+//   G = 8) is accessed with 8-byte vectors. A side is physical leaves or byte planes (Bytesplit
+//   term k = byte k).
 // - Every destination word is assembled from source words by PRMT byte permutes with
 //   compile-time selectors. Bool bytes are canonicalised (__vcmpne4).
 // - ChangeType leaves (f32 <-> f64, integer widen / narrow) are converted in registers with the
@@ -34,6 +36,7 @@
 // - LAMB_JIT=0 disables this path.
 // - LAMB_JIT_STAGE=1|s|d|0 forces a staging mode, and LAMB_JIT_MINB a register cap.
 // - LAMB_JIT_TUNE=0 turns autotuning off.
+// - LAMB_JIT_HALF=0 disables 8-byte spans (1-byte leaves at G = 8).
 // - LAMB_JIT_DUMP=file appends the generated sources to that file; LAMB_JIT_LOG=1 prints compile errors.
 #include "capi_internal.hpp"
 #include "launch.h"
