@@ -276,7 +276,12 @@ namespace lamjit
                         sp.lmask = L - 1;
                         sp.ls = t.ls;
                         sp.bytes = G * t.size;
-                        if(t.ls != t.size || sp.bytes % 16 || sp.base % 16 || st.bs % 16)
+                        if(t.ls == t.size && sp.bytes == 8 && sp.base % 8 == 0 && st.bs % 8 == 0 && halfOk)
+                        {
+                            sp.half = true; // 8 bytes per group: one 8-byte access
+                            sp.bytes = 16;
+                        }
+                        else if(t.ls != t.size || sp.bytes % 16 || sp.base % 16 || st.bs % 16)
                             return false;
                         sp.word0 = words;
                         words += sp.bytes / 4;

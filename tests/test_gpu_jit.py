@@ -190,3 +190,27 @@ def test_jit_host_pipeline(a, b, tmp_path, monkeypatch):
         assert np.array_equal(x, y), f"blob {nr}"
     assert np.array_equal(dc, O.counters(md))
     assert _dump_size(dump) > 0
+
+
+@pytest.mark.parametrize("a,b", [("aosoa:16", "aos-packed"), ("soa-mb", "aosoa:32"), ("aosoa:32", "bytesplit:soa-mb"),
+                                 ("aosoa:16", "aosoa:32")])
+def test_jit_half_spans(a, b, tmp_path, monkeypatch):
+    """8-byte spans (1-byte leaves at G = 8, in SoA blobs and inside AoSoA blocks) against the
+    oracle, random bytes in both views (bool canonicalisation, untouched padding)."""
+    from paper_2302_08251_b200 import lamina as L
+    dump = str(tmp_path / "jit.cu")
+    monkeypatch.setenv("LAMB_JIT_DUMP", dump)
+    n = 9001
+    ext = f"i32:[{n}]"
+    ms, md = O.make(MIXED, ext, a), O.make(MIXED, ext, b)
+    rng = np.random.default_rng(29)
+    sb = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(ms)]
+    db = [rng.integers(0, 256, x.size, dtype=np.uint8) for x in O.zero_blobs(md)]
+    gs, gd = L.View(L.Layout(MIXED, ext, a)), L.View(L.Layout(MIXED, ext, b))
+    gs.upload_all(sb)
+    gd.upload_all(db)
+    O.copy_view(ms, sb, md, db)
+    L.copy_view(gs, gd)
+    for nr, (x, y) in enumerate(zip(gd.download_all(), db)):
+        assert np.array_equal(x, y), f"{a} -> {b} blob {nr}: {np.flatnonzero(x != y)[:8]}"
+    assert _dump_size(dump) > 0
