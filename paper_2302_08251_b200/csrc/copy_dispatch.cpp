@@ -122,7 +122,9 @@ namespace lamhost
                 for(uint16_t r : L->roots)
                 {
                     const lamp_node& nd = L->nodes[r];
-                    const bool fltOk = rp && rp[0] == '2' && nd.kind == LAMP_BITS_FLT && nd.a >= 1 && nd.a <= 8 && nd.b <= 23;
+                    const bool fast = (nd.a == 8 && nd.b == 10) || (nd.a == 5 && nd.b == 10) || (nd.a == 4 && nd.b == 3)
+                        || (nd.a == 5 && nd.b == 2);
+                    const bool fltOk = nd.kind == LAMP_BITS_FLT && nd.a >= 1 && nd.a <= 8 && nd.b <= 23 && (fast || (rp && rp[0] == '2'));
                     if(nd.kind == LAMP_BITS_INT ? nd.a > 32 : !fltOk)
                         return true;
                 }

@@ -935,9 +935,12 @@ namespace lamhost
             if(!sb || !db || L.skind != L.dkind || L.stype != L.ltype || L.dtype != L.ltype || scalarSize(L.ltype) != 4)
                 return false;
             const bool flt = L.skind == LAMT_K_BITS_FLT;
-            // minifloat -> minifloat measured faster staged through the SoA scratch, where both halves
-            // run the compile-time-format codecs (tools/repack_cmp.py); LAMB_REPACK=2 forces this path
-            if(flt && envNum("LAMB_REPACK", 1) != 2)
+            // minifloat -> minifloat: one pass when both formats have compile-time codecs (e8m10,
+            // e5m10, e4m3, e5m2; k_repack_flt); other formats measured faster staged through the SoA
+            // scratch (tools/repack_cmp.py), LAMB_REPACK=2 forces the runtime-format one-pass kernel
+            auto fastFmt = [](uint32_t E, uint32_t M)
+            { return (E == 8 && M == 10) || (E == 5 && M == 10) || (E == 4 && M == 3) || (E == 5 && M == 2); };
+            if(flt && envNum("LAMB_REPACK", 1) != 2 && !(fastFmt(L.sE, L.sM) && fastFmt(L.dE, L.dM)))
                 return false;
             if(flt && (L.ltype != F32 || L.sE > 8 || L.sM > 23 || L.dE > 8 || L.dM > 23 || L.sE < 1 || L.dE < 1))
                 return false;
@@ -961,7 +964,7 @@ namespace lamhost
             jobs.push_back(j);
         }
         for(const auto& j : jobs)
-            if(!lamk::repack32(j, s))
+            if(!(j.kind == 1 && envNum("LAMB_REPACK", 1) != 2 ? lamk::repack_flt_fast(j, s) : lamk::repack32(j, s)))
                 return false;
         addAccessCounts(p, S, groups * 32, s);
         const uint64_t doneEnd = begin + groups * 32;

@@ -70,6 +70,8 @@ namespace lamk
         uint32_t ssgn; // int: sign-extend the source field (signed leaf type)
     };
     bool repack32(const RepackParams& p, cudaStream_t s);
+    // minifloat -> minifloat with compile-time formats (e8m10, e5m10, e4m3, e5m2 on both sides)
+    bool repack_flt_fast(const RepackParams& p, cudaStream_t s);
 
 
 

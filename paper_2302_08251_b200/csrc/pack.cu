@@ -981,6 +981,148 @@ namespace lamk
         }
     }
 
+    // minifloat -> minifloat with both formats compile-time (FMT 1 e8m10 / 2 e5m10 / 5 e4m3 /
+    // 6 e5m2): the same warp structure as k_repack32, widths and codecs fully unrolled
+    template<int FS>
+    __device__ __forceinline__ uint32_t rp_dec(uint32_t pat)
+    {
+        if constexpr(FS == 1)
+        {
+            const uint32_t sign = (pat >> 18) << 31;
+            if((pat & 0x3FC00u) == 0x3FC00u && (pat & 0x3FFu))
+                return sign | 0x7FC00000u;
+            return sign | ((pat & 0x3FFFFu) << 13);
+        }
+        else if constexpr(FS == 2)
+        {
+            if((pat & 0x7C00u) == 0x7C00u && (pat & 0x3FFu))
+                return ((pat >> 15) << 31) | 0x7FC00000u;
+            return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(pat))));
+        }
+        else if constexpr(FS == 5)
+            return lamd::f32_decode_bf(lamd::f32_codec(4, 3), pat);
+        else
+            return lamd::f32_decode_bf(lamd::f32_codec(5, 2), pat);
+    }
+    template<int FD>
+    __device__ __forceinline__ uint32_t rp_enc(uint32_t v)
+    {
+        if constexpr(FD == 1)
+            return lamd::encode_e8m10_f32(v);
+        else if constexpr(FD == 2)
+            return lamd::encode_e5m10_f32(v);
+        else if constexpr(FD == 5)
+            return lamd::f32_encode_bf(lamd::f32_codec(4, 3), v);
+        else
+            return lamd::f32_encode_bf(lamd::f32_codec(5, 2), v);
+    }
+    template<int FS, int FD>
+    __global__ void __launch_bounds__(256) k_repack_flt(const __grid_constant__ RepackParams p)
+    {
+        constexpr uint32_t WS = FS == 1 ? 19 : FS == 2 ? 16 : 8, WD = FD == 1 ? 19 : FD == 2 ? 16 : 8;
+        constexpr uint32_t WSP = WS | 1u, WDP = WD | 1u;
+        extern __shared__ __align__(16) uint32_t fsm[];
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t* srow = fsm + (threadIdx.x >> 5) * 32 * (WSP + WDP);
+        uint32_t* drow = srow + 32 * WSP;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.src);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(p.dst);
+        const uint64_t gEnd = (p.groups + 31) / 32 * 32;
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        for(uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < gEnd; g += stride)
+        {
+            const uint64_t warpG = g - lane;
+            const uint32_t live = static_cast<uint32_t>(p.groups > warpG ? (p.groups - warpG < 32 ? p.groups - warpG : 32) : 0);
+            const uint32_t* ws0 = src + (p.begin / 32 + warpG) * WS;
+            for(uint32_t t = lane; t < live * WS; t += 32)
+                srow[(t / WS) * WSP + t % WS] = __ldcs(ws0 + t);
+            __syncwarp();
+            if(lane < live)
+            {
+                const uint32_t* my = srow + lane * WSP;
+                uint32_t wv[WS], ov[WD];
+#pragma unroll
+                for(uint32_t k = 0; k < WS; ++k)
+                    wv[k] = my[k];
+#pragma unroll
+                for(uint32_t k = 0; k < WD; ++k)
+                    ov[k] = 0;
+#pragma unroll
+                for(uint32_t i = 0; i < 32; ++i)
+                {
+                    const uint32_t bit = i * WS, k = bit >> 5, sh = bit & 31;
+                    uint32_t pat = wv[k] >> sh;
+                    if(sh + WS > 32)
+                        pat |= wv[k + 1] << (32 - sh);
+                    pat &= (1u << WS) - 1u;
+                    const uint32_t e = rp_enc<FD>(rp_dec<FS>(pat));
+                    const uint32_t ob = i * WD, ok = ob >> 5, osh = ob & 31;
+                    ov[ok] |= e << osh;
+                    if(osh + WD > 32)
+                        ov[ok + 1] |= e >> (32 - osh);
+                }
+                uint32_t* out = drow + lane * WDP;
+#pragma unroll
+                for(uint32_t k = 0; k < WD; ++k)
+                    out[k] = ov[k];
+            }
+            __syncwarp();
+            uint32_t* wd0 = dst + (p.begin / 32 + warpG) * WD;
+            for(uint32_t t = lane; t < live * WD; t += 32)
+                __stcs(wd0 + t, drow[(t / WD) * WDP + t % WD]);
+            __syncwarp();
+        }
+    }
+
+    // the compile-time format code of (E, M), or 0
+    static int fast_fmt(uint32_t E, uint32_t M)
+    {
+        return E == 8 && M == 10 ? 1 : E == 5 && M == 10 ? 2 : E == 4 && M == 3 ? 5 : E == 5 && M == 2 ? 6 : 0;
+    }
+
+    template<int FS, int FD>
+    static void launch_repack_flt(const RepackParams& p, cudaStream_t s)
+    {
+        constexpr uint32_t WS = FS == 1 ? 19 : FS == 2 ? 16 : 8, WD = FD == 1 ? 19 : FD == 2 ? 16 : 8;
+        const size_t smem = static_cast<size_t>(8) * 32 * ((WS | 1u) + (WD | 1u)) * sizeof(uint32_t);
+        lam_cuda_check(opt_in_smem(reinterpret_cast<const void*>(k_repack_flt<FS, FD>), smem), "opt_in_smem");
+        k_repack_flt<FS, FD><<<stream_grid((p.groups + 255) / 256, "LAMB_PACK_CTAS", 32), 256, smem, s>>>(p);
+    }
+
+    template<int FS>
+    static bool dispatch_repack_flt_d(int fd, const RepackParams& p, cudaStream_t s)
+    {
+        switch(fd)
+        {
+        case 1: launch_repack_flt<FS, 1>(p, s); return true;
+        case 2: launch_repack_flt<FS, 2>(p, s); return true;
+        case 5: launch_repack_flt<FS, 5>(p, s); return true;
+        case 6: launch_repack_flt<FS, 6>(p, s); return true;
+        default: return false;
+        }
+    }
+
+    bool repack_flt_fast(const RepackParams& p, cudaStream_t s)
+    {
+        const int fs = fast_fmt(p.sE, p.sM), fd = fast_fmt(p.dE, p.dM);
+        if(p.groups == 0 || !fs || !fd)
+            return false;
+        bool ok = false;
+        switch(fs)
+        {
+        case 1: ok = dispatch_repack_flt_d<1>(fd, p, s); break;
+        case 2: ok = dispatch_repack_flt_d<2>(fd, p, s); break;
+        case 5: ok = dispatch_repack_flt_d<5>(fd, p, s); break;
+        case 6: ok = dispatch_repack_flt_d<6>(fd, p, s); break;
+        default: return false;
+        }
+        if(!ok)
+            return false;
+        count_launch();
+        lam_cuda_check(cudaGetLastError(), "kernel launch");
+        return true;
+    }
+
     bool repack32(const RepackParams& p, cudaStream_t s)
     {
         if(p.groups == 0 || p.ws < 1 || p.ws > 32 || p.wd < 1 || p.wd > 32)
