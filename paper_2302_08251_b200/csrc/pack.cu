@@ -1055,7 +1055,20 @@ namespace lamk
                     if(sh + WS > 32)
                         pat |= wv[k + 1] << (32 - sh);
                     pat &= (1u << WS) - 1u;
-                    const uint32_t e = rp_enc<FD>(rp_dec<FS>(pat));
+                    uint32_t e;
+                    if constexpr(FS == FD)
+                    {
+                        // same format: decode then encode is the identity (every such minifloat is an
+                        // exact f32) except that a NaN comes back as the canonical quiet NaN
+                        // (sign | all-ones exponent | 1 << (M - 1), bitpack.cpp:107-115)
+                        constexpr uint32_t M = FS == 1 || FS == 2 ? 10 : FS == 5 ? 3 : 2;
+                        constexpr uint32_t EXP = ((1u << (WS - 1)) - 1u) & ~((1u << M) - 1u);
+                        constexpr uint32_t MAN = (1u << M) - 1u;
+                        const bool nan = (pat & EXP) == EXP && (pat & MAN);
+                        e = nan ? ((pat & (1u << (WS - 1))) | EXP | (1u << (M - 1))) : pat;
+                    }
+                    else
+                        e = rp_enc<FD>(rp_dec<FS>(pat));
                     const uint32_t ob = i * WD, ok = ob >> 5, osh = ob & 31;
                     ov[ok] |= e << osh;
                     if(osh + WD > 32)

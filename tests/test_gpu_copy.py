@@ -470,6 +470,8 @@ def test_bitpack_float_record_side_formats(fmt, rec):
     (R32, "bitpack-float:8,10", "bitpack-float:4,3"),
     (R32, "bitpack-float:5,2", "bitpack-float:5,2"),
     (R32, "bitpack-float:6,9", "bitpack-float:8,23"),
+    (R32, "bitpack-float:4,3", "bitpack-float:4,3"), (R32, "bitpack-float:8,10", "bitpack-float:8,10"),
+    (R32, "bitpack-float:5,10", "bitpack-float:5,10"),
 ])
 @pytest.mark.parametrize("n", [1000, 70001])
 def test_bitpack_to_bitpack(schema, a, b, n):

@@ -8,7 +8,7 @@ PEAK = peaks()[0]
 n = 1 << 26
 for schema, a, b in [("Record{v:u32,w:i32}", "bitpack-int:11", "bitpack-int:7"), ("Record{v:u32,w:i32}", "bitpack-int:13", "bitpack-int:13"),
                      ("Record{v:u32,w:i32}", "bitpack-int:3", "bitpack-int:31"), (R32, "bitpack-float:5,10", "bitpack-float:5,10"),
-                     (R32, "bitpack-float:4,3", "bitpack-float:5,10"), (R32, "bitpack-float:8,10", "bitpack-float:4,3")]:
+                     (R32, "bitpack-float:4,3", "bitpack-float:5,10"), (R32, "bitpack-float:8,10", "bitpack-float:4,3"), (R32, "bitpack-float:4,3", "bitpack-float:4,3")]:
     la, lb = L.Layout(schema, f"i32:[{n}]", a), L.Layout(schema, f"i32:[{n}]", b)
     s, d = L.View(la), L.View(lb)
     _fill(L, s, 1)
