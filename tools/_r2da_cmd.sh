@@ -1,4 +1,4 @@
-O=gpurun_out/r2cx
+O=gpurun_out/r2da
 mkdir -p $O
 timeout 2000 python -m pytest tests -m gpu -q -x --durations=5 > $O/pytest.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
